@@ -1,0 +1,771 @@
+/*
+ * gf_oracle.c -- CPU double-precision ORACLE for the Gabor Fields hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_2602_05081_b200/) never imports, links or runs it,
+ * and this file shares no code, header, table or constant generator with it.
+ *
+ * Plain, slow, obviously-correct: brute force over ALL primitives (no BVH),
+ * every quantity in double, each function citing the passage it follows.
+ * Citations "P:Lnnn" are lines of PAPER.md (arXiv 2602.05081, LaTeX source);
+ * readings where the paper is silent/garbled are the C-numbers of DESIGN.md §3.
+ *
+ *   kernel ............ Eq. 6        g = (8pi^3|S|)^-1/2 e^{-1/2 x'S^-1 x} cos(w.x)
+ *   modulation ........ P:L183                        w_vec = R S^-1 (w,w,w)^T
+ *   extinction ........ Eq. 1        kappa = sum alpha_i K_i, K_i bounded by ellipsoid (C7)
+ *   optical depth ..... Eq. 2-3       tau_i = alpha_i int K_i dt ; T = exp(-sum tau_i)
+ *   segment integral .. App. A finite form, scalars a,beta,gamma,B,delta
+ *   complex erf ....... Eq. 13 Maclaurin series, run to convergence in double (C5)
+ *   segments .......... Eq. 4        entry/exit events, active set per segment
+ *   free flight ....... Eq. 5, bisection, first crossing (C16/C17)
+ *   masks ............. P:L344-L350                  visible iff (V_r & V_l) != 0 (32-bit groups, C24)
+ *   level strategies .. Table B1, readings C13/C14
+ *   orient. strategies  Table B2, readings C11/C12/C15
+ *   pipeline .......... P:L352-L365 (sample mask, intersect, distance sample / integrate, reweight, recurse)
+ *   tomography ........ P:L363 (accumulate tau, exp after all samples)
+ *   Philox4x32-10 ..... counter RNG (Salmon et al. 2011); same stream layout as the GPU
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fPIC -shared -o liboracle.so gf_oracle.c -lm -lpthread
+ */
+#include <complex.h>
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_PI 3.14159265358979323846
+#define OR_MAXG 32
+
+/* ------------------------------------------------------------------------- */
+/* Scene                                                                      */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int n, P, K, G;
+    double *mu;    /* 3n  kernel mean                                   */
+    double *sinv;  /* 9n  Sigma^-1 = R S^-2 R^T (row major)             */
+    double *wvec;  /* 3n  omega_vec = R S^-1 (w,w,w)^T         */
+    double *norm;  /* n   (8 pi^3 |Sigma|)^-1/2  (Eq. 6)                 */
+    double *alpha; /* n   kernel weight alpha_i (Eq. 1)                  */
+    double *E2;    /* n   squared whitened extent (C7/C8; default 3^2)   */
+    int *group;    /* n   group id g(l,b) (C10/C11/C24)                  */
+    int *bin;      /* n   orientation bin (derived if not given)         */
+    float bin_axes[3 * 32];
+} or_scene;
+
+/* quaternion (x,y,z,w) -> rotation matrix R (row major), normalised in double */
+static void quat_to_R(const float *qf, double R[9]) {
+    double x = qf[0], y = qf[1], z = qf[2], w = qf[3];
+    double nn = sqrt(x * x + y * y + z * z + w * w);
+    x /= nn; y /= nn; z /= nn; w /= nn;
+    R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
+/* Orientation bin (C11): argmax_k |d . o_k| with d = direction of omega_vec,
+ * ties -> lower k.  Integer decided by floating point, so it is taken in fp32
+ * (the kernel's precision, task rule) with explicit fmaf so that no contraction
+ * choice of the compiler changes it.  d is taken unnormalised (argmax is scale
+ * free): d = R S^-1 (1,1,1)^T. */
+static int derive_bin_f32(const float *qf, const float *sf, int K, const float *axes) {
+    float x = qf[0], y = qf[1], z = qf[2], w = qf[3];
+    float nn = sqrtf(fmaf(x, x, fmaf(y, y, fmaf(z, z, w * w))));
+    x = x / nn; y = y / nn; z = z / nn; w = w / nn;
+    float R[9];
+    R[0] = 1.0f - 2.0f * fmaf(y, y, z * z); R[1] = 2.0f * fmaf(x, y, -(w * z)); R[2] = 2.0f * fmaf(x, z, w * y);
+    R[3] = 2.0f * fmaf(x, y, w * z);        R[4] = 1.0f - 2.0f * fmaf(x, x, z * z); R[5] = 2.0f * fmaf(y, z, -(w * x));
+    R[6] = 2.0f * fmaf(x, z, -(w * y));     R[7] = 2.0f * fmaf(y, z, w * x);     R[8] = 1.0f - 2.0f * fmaf(x, x, y * y);
+    float i0 = 1.0f / sf[0], i1 = 1.0f / sf[1], i2 = 1.0f / sf[2];
+    float d[3];
+    for (int r = 0; r < 3; ++r) d[r] = fmaf(R[3 * r + 0], i0, fmaf(R[3 * r + 1], i1, R[3 * r + 2] * i2));
+    int best = 0; float bestv = -1.0f;
+    for (int k = 0; k < K; ++k) {
+        const float *o = axes + 3 * k;
+        float a = fabsf(fmaf(d[0], o[0], fmaf(d[1], o[1], d[2] * o[2])));
+        if (a > bestv) { bestv = a; best = k; }
+    }
+    return best;
+}
+
+/* Build the per-primitive double data.  level/bin may be NULL (bin==NULL or
+ * 255 -> derived, level==NULL -> omega==0 ? 0 : 1).  Returns NULL on bad input. */
+or_scene *or_scene_create(int n, const float *mu, const float *quat, const float *scale,
+                          const float *alpha, const float *omega, const float *extent,
+                          const uint8_t *level, const uint8_t *bin, int P, int K,
+                          const float *bin_axes) {
+    if (n < 0 || P < 1 || K < 1 || 1 + (P - 1) * K > OR_MAXG) return NULL;
+    or_scene *s = (or_scene *)calloc(1, sizeof(or_scene));
+    s->n = n; s->P = P; s->K = K; s->G = 1 + (P - 1) * K;
+    if (bin_axes) memcpy(s->bin_axes, bin_axes, sizeof(float) * 3 * K);
+    size_t nn = n > 0 ? (size_t)n : 1;
+    s->mu = malloc(sizeof(double) * 3 * nn);   s->sinv = malloc(sizeof(double) * 9 * nn);
+    s->wvec = malloc(sizeof(double) * 3 * nn); s->norm = malloc(sizeof(double) * nn);
+    s->alpha = malloc(sizeof(double) * nn);    s->E2 = malloc(sizeof(double) * nn);
+    s->group = malloc(sizeof(int) * nn);       s->bin = malloc(sizeof(int) * nn);
+    for (int i = 0; i < n; ++i) {
+        double R[9];
+        quat_to_R(quat + 4 * i, R);
+        double sx[3] = {scale[3 * i], scale[3 * i + 1], scale[3 * i + 2]};
+        /* Sigma = R S S^T R^T  ->  Sigma^-1 = R S^-2 R^T */
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) {
+                double acc = 0;
+                for (int k = 0; k < 3; ++k) acc += R[3 * r + k] * R[3 * c + k] / (sx[k] * sx[k]);
+                s->sinv[9 * i + 3 * r + c] = acc;
+            }
+        /* omega_vec = R S^-1 (w,w,w)^T */
+        double w = omega[i];
+        for (int r = 0; r < 3; ++r) {
+            double acc = 0;
+            for (int k = 0; k < 3; ++k) acc += R[3 * r + k] * w / sx[k];
+            s->wvec[3 * i + r] = acc;
+        }
+        /* |Sigma|^(1/2) = s1 s2 s3 ; (8 pi^3 |Sigma|)^(-1/2) (Eq. 6) */
+        s->norm[i] = 1.0 / sqrt(8.0 * OR_PI * OR_PI * OR_PI * sx[0] * sx[0] * sx[1] * sx[1] * sx[2] * sx[2]);
+        for (int k = 0; k < 3; ++k) s->mu[3 * i + k] = mu[3 * i + k];
+        s->alpha[i] = alpha[i];
+        double E = extent ? extent[i] : 3.0;
+        s->E2[i] = E * E;
+        int l = level ? level[i] : (omega[i] == 0.0f ? 0 : 1);
+        if (l >= P) l = P - 1;
+        int b = (bin && bin[i] != 255) ? bin[i] : (l == 0 ? 0 : derive_bin_f32(quat + 4 * i, scale + 3 * i, K, s->bin_axes));
+        if (b >= K) b = K - 1;
+        s->bin[i] = b;
+        s->group[i] = (l == 0) ? 0 : 1 + (l - 1) * K + b;  /* C24 group id */
+    }
+    return s;
+}
+
+void or_scene_destroy(or_scene *s) {
+    if (!s) return;
+    free(s->mu); free(s->sinv); free(s->wvec); free(s->norm); free(s->alpha); free(s->E2);
+    free(s->group); free(s->bin); free(s);
+}
+
+int or_scene_groups(const or_scene *s, int *group_out, int *bin_out) {
+    for (int i = 0; i < s->n; ++i) { group_out[i] = s->group[i]; if (bin_out) bin_out[i] = s->bin[i]; }
+    return s->n;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Kernel evaluation, Eq. 6, truncated at the ellipsoid (C7)     */
+/* ------------------------------------------------------------------------- */
+double or_eval_kernel(const or_scene *s, int i, const double x[3], int truncated) {
+    double d[3] = {x[0] - s->mu[3 * i], x[1] - s->mu[3 * i + 1], x[2] - s->mu[3 * i + 2]};
+    const double *M = s->sinv + 9 * i;
+    double q = 0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) q += d[r] * M[3 * r + c] * d[c];
+    if (truncated && q > s->E2[i]) return 0.0;
+    const double *wv = s->wvec + 3 * i;
+    return s->norm[i] * exp(-0.5 * q) * cos(wv[0] * d[0] + wv[1] * d[1] + wv[2] * d[2]);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Complex erf by its Maclaurin series, Eq. 13:                 */
+/*   erf(z) = 2/sqrt(pi) sum_n (-1)^n z^(2n+1) / (n! (2n+1))                    */
+/* run to convergence (term < 1e-17 |sum|, <= 200 terms) -- reading C5.       */
+/* ------------------------------------------------------------------------- */
+double complex or_erf(double complex z) {
+    double complex zz = z * z;
+    /* domain guard: the alternating series loses ~|z|^2/ln(10) digits; beyond |z|^2 = 24 the
+       double result is no longer trustworthy to 1e-8, so fail loudly (NaN) instead. */
+    if (cabs(zz) > 24.0) return NAN + I * NAN;
+    double complex p = z;   /* (-1)^n z^(2n+1) / n! */
+    double complex sum = z;
+    for (int n = 1; n < 200; ++n) {
+        p = p * (-zz) / (double)n;
+        double complex term = p / (double)(2 * n + 1);
+        sum += term;
+        if (cabs(term) < 1e-17 * cabs(sum)) break;
+    }
+    return sum * (2.0 / sqrt(OR_PI));
+}
+
+void or_erf_parts(double re, double im, double *out) {
+    double complex r = or_erf(re + I * im);
+    out[0] = creal(r); out[1] = cimag(r);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Per (ray, primitive) scalars, App. A                          */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    double a, beta, gamma, B, delta;
+    double r2;          /* gamma - beta^2/a : squared perpendicular distance */
+    int hit;            /* chord of the ellipsoid intersects [t0,t1] with positive length */
+    double tin, tout;   /* chord clipped to [t0,t1] */
+} or_pair;
+
+static void pair_setup(const or_scene *s, int i, const double o[3], const double v[3],
+                       double t0, double t1, or_pair *p) {
+    const double *M = s->sinv + 9 * i;
+    double d[3] = {o[0] - s->mu[3 * i], o[1] - s->mu[3 * i + 1], o[2] - s->mu[3 * i + 2]};
+    double Mv[3], Md[3];
+    for (int r = 0; r < 3; ++r) {
+        Mv[r] = M[3 * r] * v[0] + M[3 * r + 1] * v[1] + M[3 * r + 2] * v[2];
+        Md[r] = M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2];
+    }
+    p->a = v[0] * Mv[0] + v[1] * Mv[1] + v[2] * Mv[2];      /* a     = v^T S^-1 v */
+    p->beta = v[0] * Md[0] + v[1] * Md[1] + v[2] * Md[2];   /* beta  = v^T S^-1 d */
+    p->gamma = d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];  /* gamma = d^T S^-1 d */
+    const double *wv = s->wvec + 3 * i;
+    p->B = wv[0] * v[0] + wv[1] * v[1] + wv[2] * v[2];      /* B     = w^T v */
+    p->delta = wv[0] * d[0] + wv[1] * d[1] + wv[2] * d[2];  /* delta = w^T d */
+    /* perpendicular distance^2, computed from the closest-approach offset
+       (d + tc v) to avoid the gamma - beta^2/a cancellation for far origins */
+    double tc = -p->beta / p->a;
+    double dc[3] = {d[0] + tc * v[0], d[1] + tc * v[1], d[2] + tc * v[2]};
+    double r2 = 0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) r2 += dc[r] * M[3 * r + c] * dc[c];
+    p->r2 = r2;
+    /* ellipsoid: a t^2 + 2 beta t + gamma <= E^2  (C7) */
+    p->hit = 0;
+    if (r2 < s->E2[i]) {
+        double ht = sqrt((s->E2[i] - r2) / p->a);
+        double ta = tc - ht, tb = tc + ht;
+        if (ta < t0) ta = t0;
+        if (tb > t1) tb = t1;
+        if (tb > ta) { p->hit = 1; p->tin = ta; p->tout = tb; }
+    }
+}
+
+/* App. A finite-domain closed form, alpha NOT applied:
+ *   I = (8pi^3|S|)^-1/2 Re{ e^{i delta} e^{-gamma/2} sqrt(pi/2a) e^{(-beta+iB)^2/2a}
+ *                          [erf(sqrt(a/2) t1 - zeta) - erf(sqrt(a/2) t0 - zeta)] },
+ *   zeta = (-beta + iB)/sqrt(2a).
+ * The exponentials are combined before evaluation,
+ *   e^{-gamma/2} e^{(-beta+iB)^2/2a} = e^{-r2/2} e^{-B^2/2a} e^{-i beta B/a},
+ * so that e^{beta^2/2a} (which overflows for far origins) is never formed. */
+static double seg_integral(const or_scene *s, int i, const or_pair *p, double ta, double tb) {
+    if (!(tb > ta)) return 0.0;
+    double a = p->a, sq2a = sqrt(2.0 * a);
+    double complex zeta = (-p->beta + I * p->B) / sq2a;
+    double complex z1 = sqrt(a / 2.0) * tb - zeta;
+    double complex z0 = sqrt(a / 2.0) * ta - zeta;
+    double complex derf = or_erf(z1) - or_erf(z0);
+    double mag = exp(-0.5 * p->r2 - p->B * p->B / (2.0 * a));
+    double phase = p->delta - p->beta * p->B / a;
+    double complex val = cexp(I * phase) * derf;
+    return s->norm[i] * sqrt(OR_PI / (2.0 * a)) * mag * creal(val);
+}
+
+/* Public: integral of kernel i (alpha not applied, truncated at E) along
+   o + t v over [t0,t1]. */
+double or_prim_integral(const or_scene *s, int i, const float *ray_o, const float *ray_v,
+                        double t0, double t1) {
+    double o[3] = {ray_o[0], ray_o[1], ray_o[2]}, v[3] = {ray_v[0], ray_v[1], ray_v[2]};
+    or_pair p;
+    pair_setup(s, i, o, v, t0, t1, &p);
+    if (!p.hit) return 0.0;
+    return seg_integral(s, i, &p, p.tin, p.tout);
+}
+
+/* Untruncated full-line integral: App. A boxed infinite limit. */
+double or_prim_integral_infinite(const or_scene *s, int i, const float *ray_o, const float *ray_v) {
+    double o[3] = {ray_o[0], ray_o[1], ray_o[2]}, v[3] = {ray_v[0], ray_v[1], ray_v[2]};
+    or_pair p;
+    pair_setup(s, i, o, v, -INFINITY, INFINITY, &p);
+    double a = p.a;
+    return s->norm[i] * sqrt(2.0 * OR_PI / a) * exp(-0.5 * p.r2) * exp(-p.B * p.B / (2.0 * a)) *
+           cos(p.delta - p.beta * p.B / a);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Brute-force optical depth, Eq. 2-3 with masks                */
+/* ------------------------------------------------------------------------- */
+typedef struct { double s, c; } neum;  /* Neumaier compensated sum */
+static void neum_add(neum *n, double x) {
+    double t = n->s + x;
+    if (fabs(n->s) >= fabs(x)) n->c += (n->s - t) + x; else n->c += (x - t) + n->s;
+    n->s = t;
+}
+static double neum_get(const neum *n) { return n->s + n->c; }
+
+/* tau = sum over visible i of w_g(i) alpha_i int K_i ; also A = sum |.| and per-group tau */
+static double trace_one(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
+                        uint32_t mask, const float *wts, double *abs_out, double *grp_out, int *nhits) {
+    neum tau = {0, 0}, A = {0, 0};
+    neum grp[OR_MAXG];
+    memset(grp, 0, sizeof(grp));
+    int nh = 0;
+    for (int i = 0; i < s->n; ++i) {
+        int g = s->group[i];
+        if (!((mask >> g) & 1u)) continue;
+        or_pair p;
+        pair_setup(s, i, o, v, t0, t1, &p);
+        if (!p.hit) continue;
+        ++nh;
+        double w = wts ? (double)wts[g] : 1.0;
+        double ti = w * s->alpha[i] * seg_integral(s, i, &p, p.tin, p.tout);
+        neum_add(&tau, ti);
+        neum_add(&A, fabs(ti));
+        neum_add(&grp[g], ti);
+    }
+    if (abs_out) *abs_out = neum_get(&A);
+    if (grp_out)
+        for (int g = 0; g < s->G; ++g) grp_out[g] = neum_get(&grp[g]);
+    if (nhits) *nhits = nh;
+    return neum_get(&tau);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Thread pool helper                                                          */
+/* ------------------------------------------------------------------------- */
+typedef void (*or_work_fn)(void *ctx, long idx);
+typedef struct { or_work_fn fn; void *ctx; long n; long next; pthread_mutex_t mu; } or_pool;
+static void *pool_worker(void *arg) {
+    or_pool *pl = (or_pool *)arg;
+    for (;;) {
+        pthread_mutex_lock(&pl->mu);
+        long i = pl->next++;
+        pthread_mutex_unlock(&pl->mu);
+        if (i >= pl->n) break;
+        pl->fn(pl->ctx, i);
+    }
+    return NULL;
+}
+static void run_parallel(or_work_fn fn, void *ctx, long n, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    or_pool pl = {fn, ctx, n, 0};
+    pthread_mutex_init(&pl.mu, NULL);
+    if (nthreads == 1) { pool_worker(&pl); pthread_mutex_destroy(&pl.mu); return; }
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, pool_worker, &pl);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&pl.mu);
+}
+
+typedef struct {
+    const or_scene *s; const float *rays; uint32_t mask; const float *wts;
+    double *tau, *A, *grp; int *nhits;
+} trace_ctx;
+static void trace_work(void *c, long r) {
+    trace_ctx *t = (trace_ctx *)c;
+    const float *ry = t->rays + 8 * r;
+    double o[3] = {ry[0], ry[1], ry[2]}, v[3] = {ry[4], ry[5], ry[6]};
+    double A;
+    double grp[OR_MAXG];
+    int nh;
+    t->tau[r] = trace_one(t->s, o, v, ry[3], ry[7], t->mask, t->wts, &A, grp, &nh);
+    if (t->A) t->A[r] = A;
+    if (t->grp) memcpy(t->grp + (size_t)r * t->s->G, grp, sizeof(double) * t->s->G);
+    if (t->nhits) t->nhits[r] = nh;
+}
+
+/* rays: n x 8 floats (ox,oy,oz,tmin,dx,dy,dz,tmax). wts: G floats or NULL (=1). */
+void or_trace(const or_scene *s, const float *rays, long n, uint32_t mask, const float *wts,
+              double *tau, double *A, double *grp, int *nhits, int nthreads) {
+    trace_ctx c = {s, rays, mask, wts, tau, A, grp, nhits};
+    run_parallel(trace_work, &c, n, nthreads);
+}
+
+/* candidate set of one ray (prims whose clipped chord has positive length) */
+int or_candidates(const or_scene *s, const float *ray, uint32_t mask, int *ids, int cap, double *r2_out) {
+    double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};
+    int m = 0;
+    for (int i = 0; i < s->n; ++i) {
+        if (!((mask >> s->group[i]) & 1u)) continue;
+        or_pair p;
+        pair_setup(s, i, o, v, ray[3], ray[7], &p);
+        if (!p.hit) continue;
+        if (m < cap) { ids[m] = i; if (r2_out) r2_out[m] = p.r2 / s->E2[i]; }
+        ++m;
+    }
+    return m;
+}
+
+/* r2/E2 of a given (ray, prim) pair, for grazing classification of set differences */
+double or_pair_r2_rel(const or_scene *s, int i, const float *ray) {
+    double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};
+    or_pair p;
+    pair_setup(s, i, o, v, ray[3], ray[7], &p);
+    return p.r2 / s->E2[i];
+}
+
+/* ------------------------------------------------------------------------- */
+/* Philox4x32-10 (Salmon et al., SC'11), written independently of the GPU one */
+/* ------------------------------------------------------------------------- */
+void or_philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Stream layout: uniform k of stream st at path vertex d of
+   (pixel, sample) = word (k&3) of Philox(ctr=(pixel, sample, d, st<<16 | k>>2),
+   key=(seed_lo, seed_hi)), mapped to (x>>8)*2^-24 in [0,1) (C16). */
+enum { ST_EXT = 0, ST_NEE = 1, ST_SCAT = 2, ST_CAM = 3 };
+static uint32_t stream_word(uint64_t seed, uint32_t pix, uint32_t smp, uint32_t d, uint32_t st, uint32_t k) {
+    uint32_t ctr[4] = {pix, smp, d, (st << 16) | (k >> 2)};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t o[4];
+    or_philox(ctr, key, o);
+    return o[k & 3];
+}
+static float u01(uint32_t x) { return (float)(x >> 8) * (1.0f / 16777216.0f); }
+
+float or_uniform(uint64_t seed, uint32_t pix, uint32_t smp, uint32_t d, uint32_t st, uint32_t k) {
+    return u01(stream_word(seed, pix, smp, d, st, k));
+}
+
+/* ------------------------------------------------------------------------- */
+/* LOD policies: Table B1 (levels) x Table B2 (orientation bins)              */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    uint32_t static_mask;
+    int32_t level_strategy;  /* 0 DET 1 UNIFORM 2 POWERLAW 3 UNIFORM_CV 4 POWERLAW_CV 5 POWERLAW_CV_ACCUM */
+    float beta;
+    int32_t orient_strategy; /* 0 DET 1 THRESH_CULL 2 UNIFORM 3 IMPORTANCE 4 THRESH_UNIFORM */
+    float delta;
+} or_policy;
+
+/* Evaluate a policy for one ray segment.  ul = level uniform; uo[l-1] = the
+   orientation uniform of Gabor level l; dir = ray direction (fp32); f0[g] =
+   representative whitened frequency of group g (C12).  Writes mask and G
+   weights (weights of unselected groups are 0). */
+void or_policy_eval(const or_scene *s, const or_policy *pol, const float dir[3], float ul, const float *uo,
+                    const float *f0, uint32_t *mask_out, float *w_out) {
+    int P = s->P, K = s->K, G = s->G;
+    double lw[8];       /* per-level weight; 0 = level not selected */
+    for (int l = 0; l < 8; ++l) lw[l] = 0.0;
+    double om = 1.0 - pol->beta;
+    uint32_t m24 = (uint32_t)(ul * 16777216.0f);  /* exact: ul = m24 * 2^-24 */
+    switch (pol->level_strategy) {
+    case 1: { /* Uniform: level floor(u P), weight P (Table B1 row 2) */
+        int j = (int)(((uint64_t)m24 * (uint64_t)P) >> 24);
+        lw[j] = P;
+        break;
+    }
+    case 2: { /* Power law: x = u^(1/(1-beta)), bucket [j/P,(j+1)/P], weight 1/(b^(1-b)-a^(1-b)) (C13) */
+        int j = 0;
+        for (int k = 1; k < P; ++k) if ((double)ul >= pow((double)k / P, om)) j = k;
+        lw[j] = 1.0 / (pow((double)(j + 1) / P, om) - pow((double)j / P, om));
+        break;
+    }
+    case 3: { /* Uniform + CV: level 0 (w=1) + one of 1..P-1, weight P-1 */
+        lw[0] = 1.0;
+        if (P > 1) { int j = 1 + (int)(((uint64_t)m24 * (uint64_t)(P - 1)) >> 24); lw[j] = P - 1; }
+        break;
+    }
+    case 4: { /* Power law + CV: level 0 (w=1) + Gabor level from P-1 power-law buckets (C13) */
+        lw[0] = 1.0;
+        if (P > 1) {
+            int Q = P - 1, k = 0;
+            for (int q = 1; q < Q; ++q) if ((double)ul >= pow((double)q / Q, om)) k = q;
+            lw[1 + k] = 1.0 / (pow((double)(k + 1) / Q, om) - pow((double)k / Q, om));
+        }
+        break;
+    }
+    case 5: { /* Power law + CV (Accum.): k by power law, render levels 0..k, w_j = 1/(1-(j/P)^(1-b)) (C14) */
+        int kk = 0;
+        for (int q = 1; q < P; ++q) if ((double)ul >= pow((double)q / P, om)) kk = q;
+        for (int j = 0; j <= kk; ++j) lw[j] = 1.0 / (1.0 - pow((double)j / P, om));
+        break;
+    }
+    default: /* Deterministic */
+        for (int l = 0; l < P; ++l) lw[l] = 1.0;
+    }
+    uint32_t mask = 0;
+    float w[OR_MAXG];
+    for (int g = 0; g < G; ++g) w[g] = 0.0f;
+    if (lw[0] != 0.0) { mask |= 1u; w[0] = (float)lw[0]; }  /* Gaussians never orientation-masked (C15) */
+    for (int l = 1; l < P; ++l) {
+        if (lw[l] == 0.0) continue;
+        float bw[32];
+        for (int b = 0; b < K; ++b) bw[b] = 0.0f;
+        float a[32];
+        for (int b = 0; b < K; ++b) {
+            const float *o = s->bin_axes + 3 * b;
+            a[b] = fabsf(fmaf(dir[0], o[0], fmaf(dir[1], o[1], dir[2] * o[2])));  /* a_i = |v . o_i| */
+        }
+        float u = uo[l - 1];
+        uint32_t mu24 = (uint32_t)(u * 16777216.0f);
+        switch (pol->orient_strategy) {
+        case 1: /* Threshold culling: bins with a_i <= delta, weight 1 */
+            for (int b = 0; b < K; ++b) if (a[b] <= pol->delta) bw[b] = 1.0f;
+            break;
+        case 2: { /* Uniform: one bin, weight K */
+            int b = (int)(((uint64_t)mu24 * (uint64_t)K) >> 24);
+            bw[b] = (float)K;
+            break;
+        }
+        case 3: { /* Importance: p_i = w_i/W, weight W/w_i, w_i = exp(-f0^2 a_i^2 / 2) (C12) */
+            float wi[32], W = 0.0f;
+            for (int b = 0; b < K; ++b) {
+                float f = f0 ? f0[1 + (l - 1) * K + b] : 0.0f;
+                float x = f * a[b];
+                wi[b] = expf(-0.5f * (x * x));
+                W += wi[b];
+            }
+            if (!(W > 0.0f) || !isfinite(W)) { /* degenerate -> uniform fallback */
+                int b = (int)(((uint64_t)mu24 * (uint64_t)K) >> 24);
+                bw[b] = (float)K;
+            } else {
+                float t = u * W, c = 0.0f;
+                int pick = K - 1;
+                for (int b = 0; b < K; ++b) { c += wi[b]; if (t < c) { pick = b; break; } }
+                bw[pick] = W / wi[pick];
+            }
+            break;
+        }
+        case 4: { /* Threshold + uniform: a_i <= delta weight 1; one of the rest, weight N_above */
+            int nab = 0;
+            for (int b = 0; b < K; ++b) { if (a[b] <= pol->delta) bw[b] = 1.0f; else ++nab; }
+            if (nab > 0) {
+                int pickn = (int)(((uint64_t)mu24 * (uint64_t)nab) >> 24), c = 0;
+                for (int b = 0; b < K; ++b)
+                    if (!(a[b] <= pol->delta)) { if (c == pickn) { bw[b] = (float)nab; break; } ++c; }
+            }
+            break;
+        }
+        default:
+            for (int b = 0; b < K; ++b) bw[b] = 1.0f;
+        }
+        for (int b = 0; b < K; ++b) {
+            if (bw[b] == 0.0f) continue;
+            int g = 1 + (l - 1) * K + b;
+            mask |= 1u << g;
+            w[g] = (float)(lw[l] * (double)bw[b]);
+        }
+    }
+    mask &= pol->static_mask;
+    for (int g = 0; g < G; ++g) { if (!((mask >> g) & 1u)) w[g] = 0.0f; w_out[g] = w[g]; }
+    *mask_out = mask;
+}
+
+/* batch form for the unbiasedness pins: n draws, uo has (P-1) uniforms per draw */
+void or_policy_eval_batch(const or_scene *s, const or_policy *pol, const float *dirs, const float *ul,
+                          const float *uo, const float *f0, long n, uint32_t *masks, float *w) {
+    for (long i = 0; i < n; ++i)
+        or_policy_eval(s, pol, dirs + 3 * i, ul[i], uo + (size_t)i * (s->P > 1 ? s->P - 1 : 1), f0, masks + i,
+                       w + (size_t)i * s->G);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Free-flight distance sampling, Eq. 5 by segments (Eq. 4) and  */
+/* bisection.  t* = first t with cumulative tau >= tau* (C17).        */
+/* ------------------------------------------------------------------------- */
+typedef struct { double t; int id; int kind; } or_event;  /* kind 0 enter, 1 exit */
+static int ev_cmp(const void *x, const void *y) {
+    const or_event *a = (const or_event *)x, *b = (const or_event *)y;
+    if (a->t < b->t) return -1;
+    if (a->t > b->t) return 1;
+    if (a->id != b->id) return a->id < b->id ? -1 : 1;
+    return a->kind - b->kind;
+}
+
+typedef struct { int idx; or_pair p; double w; } or_active;
+
+static double active_sum(const or_scene *s, const or_active *act, const int *on, int nact, double ta, double tb) {
+    neum acc = {0, 0};
+    for (int k = 0; k < nact; ++k) {
+        if (!on[k]) continue;
+        const or_active *A = act + k;
+        double lo = ta > A->p.tin ? ta : A->p.tin, hi = tb < A->p.tout ? tb : A->p.tout;
+        neum_add(&acc, A->w * s->alpha[A->idx] * seg_integral(s, A->idx, &A->p, lo, hi));
+    }
+    return neum_get(&acc);
+}
+
+/* returns 1 and *t_out on collision, 0 on escape; *tau_total = tau over the
+   whole ray if escaped (for diagnostics). */
+int or_free_flight(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
+                   uint32_t mask, const float *wts, double xi, double *t_out) {
+    double tstar = -log1p(-xi);  /* tau* = -ln(1 - xi)  (Eq. 5) */
+    if (tstar <= 0.0) { *t_out = t0; return 1; }
+    int cap = 64, nact = 0;
+    or_active *act = malloc(sizeof(or_active) * cap);
+    for (int i = 0; i < s->n; ++i) {
+        int g = s->group[i];
+        if (!((mask >> g) & 1u)) continue;
+        or_pair p;
+        pair_setup(s, i, o, v, t0, t1, &p);
+        if (!p.hit) continue;
+        if (nact == cap) { cap *= 2; act = realloc(act, sizeof(or_active) * cap); }
+        act[nact].idx = i; act[nact].p = p; act[nact].w = wts ? wts[g] : 1.0;
+        ++nact;
+    }
+    or_event *ev = malloc(sizeof(or_event) * (2 * nact + 1));
+    for (int k = 0; k < nact; ++k) {
+        ev[2 * k].t = act[k].p.tin;  ev[2 * k].id = k; ev[2 * k].kind = 0;
+        ev[2 * k + 1].t = act[k].p.tout; ev[2 * k + 1].id = k; ev[2 * k + 1].kind = 1;
+    }
+    qsort(ev, 2 * nact, sizeof(or_event), ev_cmp);
+    int *on = calloc(nact > 0 ? nact : 1, sizeof(int));
+    double cum = 0.0;
+    int found = 0;
+    for (int e = 0; e < 2 * nact; ++e) {
+        /* apply the event, then the segment [ev[e].t, ev[e+1].t] has a constant active set */
+        on[ev[e].id] = ev[e].kind == 0;
+        if (e + 1 >= 2 * nact) break;
+        double ta = ev[e].t, tb = ev[e + 1].t;
+        if (!(tb > ta)) continue;
+        double seg = active_sum(s, act, on, nact, ta, tb);
+        if (cum + seg >= tstar) {
+            /* bisection in the bracketing segment to |dt| <= 1e-12 (1+|t|) */
+            double lo = ta, hi = tb;
+            for (int it = 0; it < 200 && (hi - lo) > 1e-12 * (1.0 + fabs(lo)); ++it) {
+                double mid = 0.5 * (lo + hi);
+                double f = cum + active_sum(s, act, on, nact, ta, mid) - tstar;
+                if (f >= 0.0) hi = mid; else lo = mid;
+            }
+            *t_out = 0.5 * (lo + hi);
+            found = 1;
+            break;
+        }
+        cum += seg;
+    }
+    free(on); free(ev); free(act);
+    return found;
+}
+
+int or_free_flight_f(const or_scene *s, const float *ray, uint32_t mask, const float *wts, double xi, double *t_out) {
+    double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};
+    return or_free_flight(s, o, v, ray[3], ray[7], mask, wts, xi, t_out);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Path estimator -- tomography, single and multiple scattering */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int32_t mode;          /* 0 TOMO, 1 SCATTER */
+    int32_t width, height, max_depth, jitter;
+    float cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3];  /* right/up pre-scaled by tan(fov/2)(*aspect) */
+    float albedo, hg_g, sun_dir[3], sun_E, env_L;
+    uint64_t seed;
+    or_policy ext, nee;
+    const float *group_f0;  /* G floats (C12), may be NULL */
+} or_render_desc;
+
+/* camera ray in fp32 with explicit fused ops (bit-identical to the GPU) */
+static void camera_ray(const or_render_desc *d, int px, int py, float jx, float jy, float o[3], float v[3]) {
+    float fx = (float)px + jx, fy = (float)py + jy;
+    float iw2 = 2.0f / (float)d->width, ih2 = 2.0f / (float)d->height;
+    float sx = fmaf(fx, iw2, -1.0f), sy = fmaf(-fy, ih2, 1.0f);
+    float r[3];
+    for (int k = 0; k < 3; ++k) r[k] = fmaf(sy, d->cam_up[k], fmaf(sx, d->cam_right[k], d->cam_fwd[k]));
+    float len = sqrtf(fmaf(r[0], r[0], fmaf(r[1], r[1], r[2] * r[2])));
+    for (int k = 0; k < 3; ++k) { v[k] = r[k] / len; o[k] = d->cam_pos[k]; }
+}
+
+/* Henyey-Greenstein phase function (reading C19) */
+static double hg_eval(double g, double cost) {
+    double den = 1.0 + g * g - 2.0 * g * cost;
+    return (1.0 - g * g) / (4.0 * OR_PI * den * sqrt(den));
+}
+static void hg_sample(double g, const double v[3], double u1, double u2, double out[3]) {
+    double cost;
+    if (fabs(g) < 1e-3) cost = 1.0 - 2.0 * u1;
+    else { double q = (1.0 - g * g) / (1.0 - g + 2.0 * g * u1); cost = (1.0 + g * g - q * q) / (2.0 * g); }
+    if (cost > 1.0) cost = 1.0;
+    if (cost < -1.0) cost = -1.0;
+    double sint = sqrt(fmax(0.0, 1.0 - cost * cost)), phi = 2.0 * OR_PI * u2;
+    /* orthonormal basis around v (Duff et al. 2017) */
+    double sgn = v[2] >= 0.0 ? 1.0 : -1.0;
+    double a = -1.0 / (sgn + v[2]), b = v[0] * v[1] * a;
+    double t1[3] = {1.0 + sgn * v[0] * v[0] * a, sgn * b, -sgn * v[0]};
+    double t2[3] = {b, sgn + v[1] * v[1] * a, -v[1]};
+    for (int k = 0; k < 3; ++k) out[k] = sint * cos(phi) * t1[k] + sint * sin(phi) * t2[k] + cost * v[k];
+    double n = sqrt(out[0] * out[0] + out[1] * out[1] + out[2] * out[2]);
+    for (int k = 0; k < 3; ++k) out[k] /= n;
+}
+
+static void eval_pol(const or_scene *s, const or_render_desc *d, const or_policy *pol, const float dir[3],
+                     uint32_t pix, uint32_t smp, uint32_t dep, uint32_t st, uint32_t k_level,
+                     uint32_t *mask, float *w) {
+    float ul = or_uniform(d->seed, pix, smp, dep, st, k_level);
+    float uo[8];
+    for (int l = 1; l < s->P; ++l) uo[l - 1] = or_uniform(d->seed, pix, smp, dep, st, k_level + l);
+    or_policy_eval(s, pol, dir, ul, uo, d->group_f0, mask, w);
+}
+
+/* one (pixel, sample) path; returns the estimate, *nrays = ray queries traced */
+double or_path(const or_scene *s, const or_render_desc *d, uint32_t pix, uint32_t smp, int *nrays) {
+    int px = (int)(pix % (uint32_t)d->width), py = (int)(pix / (uint32_t)d->width);
+    float jx = 0.5f, jy = 0.5f;
+    if (d->jitter) { jx = or_uniform(d->seed, pix, smp, 0, ST_CAM, 0); jy = or_uniform(d->seed, pix, smp, 0, ST_CAM, 1); }
+    float of[3], vf[3];
+    camera_ray(d, px, py, jx, jy, of, vf);
+    int nr = 0;
+    uint32_t mask;
+    float w[OR_MAXG];
+    if (d->mode == 0) {  /* tomography: tau-hat of the camera ray */
+        eval_pol(s, d, &d->ext, vf, pix, smp, 0, ST_EXT, 1, &mask, w);
+        double o[3] = {of[0], of[1], of[2]}, v[3] = {vf[0], vf[1], vf[2]};
+        double tau = trace_one(s, o, v, 0.0, INFINITY, mask, w, NULL, NULL, NULL);
+        if (nrays) *nrays = 1;
+        return tau;
+    }
+    double o[3] = {of[0], of[1], of[2]}, v[3] = {vf[0], vf[1], vf[2]};
+    double beta = 1.0, L = 0.0;
+    double sun[3] = {d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]};
+    for (int dep = 0; dep < d->max_depth; ++dep) {
+        float vfl[3] = {(float)v[0], (float)v[1], (float)v[2]};
+        eval_pol(s, d, &d->ext, vfl, pix, smp, dep, ST_EXT, 1, &mask, w);
+        double xi = or_uniform(d->seed, pix, smp, dep, ST_EXT, 0);
+        double tstar;
+        ++nr;
+        if (!or_free_flight(s, o, v, 0.0, INFINITY, mask, w, xi, &tstar)) {
+            L += beta * d->env_L;  /* escape -> environment */
+            break;
+        }
+        double x[3] = {o[0] + tstar * v[0], o[1] + tstar * v[1], o[2] + tstar * v[2]};
+        /* next-event estimation toward the directional light with its own policy */
+        uint32_t mn;
+        float wn[OR_MAXG];
+        eval_pol(s, d, &d->nee, d->sun_dir, pix, smp, dep, ST_NEE, 0, &mn, wn);
+        double tn = trace_one(s, x, sun, 0.0, INFINITY, mn, wn, NULL, NULL, NULL);
+        ++nr;
+        double cost = v[0] * sun[0] + v[1] * sun[1] + v[2] * sun[2];
+        L += beta * d->albedo * hg_eval(d->hg_g, cost) * exp(-tn) * d->sun_E;
+        if (dep + 1 >= d->max_depth) break;
+        double nv[3];
+        hg_sample(d->hg_g, v, or_uniform(d->seed, pix, smp, dep, ST_SCAT, 0), or_uniform(d->seed, pix, smp, dep, ST_SCAT, 1), nv);
+        beta *= d->albedo;
+        for (int k = 0; k < 3; ++k) { o[k] = x[k]; v[k] = nv[k]; }
+    }
+    if (nrays) *nrays = nr;
+    return L;
+}
+
+typedef struct {
+    const or_scene *s; const or_render_desc *d; const int32_t *pix; int spp_begin, spp_count;
+    double *out; int *nrays;
+} render_ctx;
+static void render_work(void *c, long idx) {
+    render_ctx *r = (render_ctx *)c;
+    long p = idx / r->spp_count, k = idx % r->spp_count;
+    int nr = 0;
+    r->out[idx] = or_path(r->s, r->d, (uint32_t)r->pix[p], (uint32_t)(r->spp_begin + k), &nr);
+    if (r->nrays) r->nrays[idx] = nr;
+}
+
+/* out[p*spp_count + k] = estimate of sample spp_begin+k at probe pixel pix[p] */
+void or_render_probes(const or_scene *s, const or_render_desc *d, const int32_t *pix, long n_probe,
+                      int spp_begin, int spp_count, double *out, int *nrays, int nthreads) {
+    render_ctx c = {s, d, pix, spp_begin, spp_count, out, nrays};
+    run_parallel(render_work, &c, n_probe * spp_count, nthreads);
+}
+
+/* camera ray exposed for tests */
+void or_camera_ray(const or_render_desc *d, int px, int py, float jx, float jy, float *o, float *v) {
+    camera_ray(d, px, py, jx, jy, o, v);
+}
+double or_hg_eval(double g, double cost) { return hg_eval(g, cost); }
+void or_hg_sample(double g, const double *v, double u1, double u2, double *out) { hg_sample(g, v, u1, u2, out); }
+size_t or_sizeof_render_desc(void) { return sizeof(or_render_desc); }
+size_t or_sizeof_policy(void) { return sizeof(or_policy); }

@@ -1,0 +1,297 @@
+"""Seeded synthetic inputs shared by the CUDA path and the oracle.
+
+This module holds NONE of the method's arithmetic (no kernel, integral,
+whitening, bin/group derivation, mask sampling or RNG of the method): it only
+draws primitive parameters, rays and camera frames with numpy's seeded
+generators, following the recipe of DESIGN.md §6.  Both the
+product path (bench.py, tests) and the oracle (tests) consume its output.
+
+Scene dict keys (SoA, fp32 unless stated):
+  n, P (pyramid levels, level 0 = Gaussians), K (orientation bins per Gabor level),
+  mu[n,3], quat[n,4] (x,y,z,w, unit), scale[n,3] (>0), alpha[n] (>=0), omega[n] (>=0),
+  extent[n] (whitened radius E, 3 = the paper's 3 sigma bound), level u8[n],
+  bin u8[n] (255 = let each side derive it), bin_axes[K,3].
+"""
+import math
+
+import numpy as np
+
+P_DEFAULT = 4
+K_DEFAULT = 3
+SCENE_SEED = 0x5EED0000
+RENDER_SEED = 0xC0FFEE00
+TWO_PI_32 = (2.0 * math.pi) ** 1.5  # (2 pi)^(3/2): peak density -> alpha conversion of Eq. 6's normalisation
+
+
+def bin_axes(K):
+    """Representative orientation axes o_k (reading C11): K=3 -> x,y,z; K=6 -> icosahedral axes."""
+    if K == 3:
+        return np.eye(3, dtype=np.float32)
+    if K == 6:
+        p = (1.0 + 5 ** 0.5) / 2.0
+        v = np.array([[0, 1, p], [0, -1, p], [1, p, 0], [-1, p, 0], [p, 0, 1], [-p, 0, 1]], np.float64)
+        return (v / np.linalg.norm(v, axis=1, keepdims=True)).astype(np.float32)
+    if K == 1:
+        return np.array([[0, 0, 1]], np.float32)
+    raise ValueError("K must be 1, 3 or 6")
+
+
+def random_quats(rng, n):
+    """Uniform random unit quaternions (Shoemake 1992), (x,y,z,w)."""
+    u1, u2, u3 = rng.random(n), rng.random(n), rng.random(n)
+    a, b = np.sqrt(1 - u1), np.sqrt(u1)
+    q = np.stack([a * np.sin(2 * np.pi * u2), a * np.cos(2 * np.pi * u2),
+                  b * np.sin(2 * np.pi * u3), b * np.cos(2 * np.pi * u3)], axis=1)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    return q.astype(np.float32)
+
+
+def _alpha_from_peak(peak, scale):
+    """alpha such that the peak of alpha*K_i is `peak` (K_i's own normalisation, Eq. 6)."""
+    return (peak * TWO_PI_32 * np.prod(scale.astype(np.float64), axis=1)).astype(np.float32)
+
+
+def _finish(mu, quat, scale, peak, omega, level, P=P_DEFAULT, K=K_DEFAULT, extent=3.0, name=""):
+    n = mu.shape[0]
+    scale = scale.astype(np.float32)
+    return {
+        "name": name, "n": n, "P": P, "K": K,
+        "mu": np.ascontiguousarray(mu, np.float32),
+        "quat": np.ascontiguousarray(quat, np.float32),
+        "scale": np.ascontiguousarray(scale, np.float32),
+        "alpha": _alpha_from_peak(np.asarray(peak, np.float64), scale),
+        "omega": np.ascontiguousarray(omega, np.float32),
+        "extent": np.full(n, extent, np.float32),
+        "level": np.ascontiguousarray(level, np.uint8),
+        "bin": np.full(n, 255, np.uint8),
+        "bin_axes": bin_axes(K),
+    }
+
+
+def scene_cfg1(seed=SCENE_SEED + 1, n=1000, density=1.1):
+    """Config 1: 1k random primitives in [-1,1]^3; 20% Gaussians, Gabors in 3 scale bands."""
+    rng = np.random.default_rng(seed)
+    n0 = n // 5
+    level = np.concatenate([np.zeros(n0, np.uint8), rng.integers(1, 4, n - n0).astype(np.uint8)])
+    band = {0: (0.12, 0.2), 1: (0.12, 0.2), 2: (0.08, 0.12), 3: (0.05, 0.08)}
+    lo = np.array([band[int(l)][0] for l in level])
+    hi = np.array([band[int(l)][1] for l in level])
+    base = np.exp(rng.uniform(np.log(lo), np.log(hi)))
+    scale = base[:, None] * np.exp(rng.normal(0, 0.25, (n, 3)))
+    mu = rng.uniform(-1, 1, (n, 3))
+    omega = np.where(level == 0, 0.0, rng.uniform(0.7, 1.5, n))
+    amp = np.array([1.0, 0.5, 0.35, 0.25])[level]
+    peak = density * np.where(level == 0, rng.uniform(0.5, 1.0, n), amp)
+    return _finish(mu, random_quats(rng, n), scale, peak, omega, level, name="cfg1")
+
+
+def scene_cfg1p(seed=SCENE_SEED + 101, n_pairs=500, density=1.5):
+    """Config 1p: paired-positive scene (reading C18): each Gabor gets a level-0 Gaussian with
+    identical mu, q, s, E and alpha_G >= alpha_gabor, so kappa >= 0 for masks containing level 0."""
+    rng = np.random.default_rng(seed)
+    level_g = rng.integers(1, 4, n_pairs).astype(np.uint8)
+    band = {1: (0.12, 0.2), 2: (0.08, 0.12), 3: (0.05, 0.08)}
+    lo = np.array([band[int(l)][0] for l in level_g])
+    hi = np.array([band[int(l)][1] for l in level_g])
+    base = np.exp(rng.uniform(np.log(lo), np.log(hi)))
+    scale = base[:, None] * np.exp(rng.normal(0, 0.25, (n_pairs, 3)))
+    mu = rng.uniform(-1, 1, (n_pairs, 3))
+    quat = random_quats(rng, n_pairs)
+    omega = rng.uniform(0.7, 1.5, n_pairs)
+    peak_gabor = density * np.array([0, 0.5, 0.35, 0.25])[level_g]
+    peak_gauss = peak_gabor * rng.uniform(1.0, 1.5, n_pairs)
+    return _finish(np.concatenate([mu, mu]), np.concatenate([quat, quat]), np.concatenate([scale, scale]),
+                   np.concatenate([peak_gauss, peak_gabor]), np.concatenate([np.zeros(n_pairs), omega]),
+                   np.concatenate([np.zeros(n_pairs, np.uint8), level_g]), name="cfg1p")
+
+
+# --- config 2: "bunny-like" union of ellipsoids ---------------------------------------------
+_BUNNY = [  # (centre, radii)
+    ((0.0, -0.2, 0.0), (0.6, 0.5, 0.45)),    # body
+    ((0.45, 0.25, 0.0), (0.3, 0.28, 0.28)),  # head
+    ((0.5, 0.7, 0.1), (0.08, 0.3, 0.06)),    # ear
+    ((0.5, 0.7, -0.1), (0.08, 0.3, 0.06)),   # ear
+    ((-0.6, -0.1, 0.0), (0.12, 0.12, 0.12)),  # tail
+]
+
+
+def _bunny_f(x):
+    """approximate signed distance to the union of the bunny ellipsoids (shape function, not the method)."""
+    f = np.full(x.shape[0], np.inf)
+    for c, r in _BUNNY:
+        c, r = np.asarray(c), np.asarray(r)
+        f = np.minimum(f, (np.linalg.norm((x - c) / r, axis=1) - 1.0) * r.min())
+    return f
+
+
+def _sample_where(rng, n, pred, lo, hi):
+    out = []
+    need = n
+    while need > 0:
+        x = rng.uniform(lo, hi, (max(4 * need, 1024), 3))
+        x = x[pred(x)]
+        out.append(x[:need])
+        need -= len(out[-1])
+    return np.concatenate(out)[:n]
+
+
+def scene_bunny(seed=SCENE_SEED + 2, counts=(1500, 10500, 28000, 60000),
+                s_levels=(0.09, 0.03, 0.015, 0.0075), name="cfg2", density=2.2):
+    """Config 2 (and the config-5 asset): L0 Gaussians inside the union, Gabor levels 1..3 in a
+    surface shell |f| < 6 s_l."""
+    rng = np.random.default_rng(seed)
+    lo, hi = np.array([-0.9, -0.85, -0.6]), np.array([0.9, 1.1, 0.6])
+    mus, scales, levels, peaks, omegas = [], [], [], [], []
+    for l, cnt in enumerate(counts):
+        s_l = s_levels[l]
+        if l == 0:
+            pts = _sample_where(rng, cnt, lambda x: _bunny_f(x) < -0.5 * s_l, lo, hi)
+        else:
+            pts = _sample_where(rng, cnt, lambda x, s=s_l: np.abs(_bunny_f(x)) < 6 * s, lo - 0.1, hi + 0.1)
+        mus.append(pts)
+        scales.append(s_l * np.exp(rng.normal(0, 0.25, (cnt, 3))))
+        levels.append(np.full(cnt, l, np.uint8))
+        if l == 0:
+            peaks.append(density * rng.uniform(0.5, 1.0, cnt))
+            omegas.append(np.zeros(cnt))
+        else:
+            peaks.append(density * np.full(cnt, (0.5, 0.35, 0.25)[l - 1]))
+            omegas.append(rng.uniform(0.7, 1.5, cnt))
+    n = sum(counts)
+    return _finish(np.concatenate(mus), random_quats(rng, n), np.concatenate(scales), np.concatenate(peaks),
+                   np.concatenate(omegas), np.concatenate(levels), name=name)
+
+
+def scene_cfg2(seed=SCENE_SEED + 2):
+    return scene_bunny(seed=seed)
+
+
+def empty_scene(P=P_DEFAULT, K=K_DEFAULT):
+    z = np.zeros((0, 3), np.float32)
+    return _finish(z, np.zeros((0, 4), np.float32), z, np.zeros(0), np.zeros(0), np.zeros(0, np.uint8), P, K,
+                   name="empty")
+
+
+def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
+    """32-bit group mask selecting whole pyramid levels: level 0 -> bit 0, Gabor level l ->
+    bits 1+(l-1)K .. (l)K (the group numbering g(l,b) of DESIGN.md §5; paper V_l = 2^l)."""
+    m = 0
+    for l in levels:
+        if l == 0:
+            m |= 1
+        else:
+            for b in range(K):
+                m |= 1 << (1 + (l - 1) * K + b)
+    return m
+
+
+def group_f0(scene):
+    """Representative whitened frequency per group (reading C12): median of sqrt(3)*omega over the
+    members of the group's level (all bins of a level share it). Input parameter of the
+    Importance orientation strategy."""
+    P, K = scene["P"], scene["K"]
+    G = 1 + (P - 1) * K
+    out = np.zeros(G, np.float32)
+    for l in range(1, P):
+        sel = scene["level"] == l
+        med = float(np.median(scene["omega"][sel])) * math.sqrt(3.0) if sel.any() else 0.0
+        for b in range(K):
+            out[1 + (l - 1) * K + b] = med
+    return out
+
+
+# --- rays and cameras ---------------------------------------------------------------------
+def camera(eye, look, up, vfov_deg, width, height):
+    """Pinhole frame as fp32 vectors (pos, fwd, right*tan*aspect, up*tan) -- the numbers both sides
+    consume, so that their fp32 camera rays are bit-identical."""
+    eye, look, up = (np.asarray(a, np.float64) for a in (eye, look, up))
+    fwd = look - eye
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, up)
+    right /= np.linalg.norm(right)
+    upv = np.cross(right, fwd)
+    th = math.tan(math.radians(vfov_deg) / 2)
+    return {"cam_pos": eye.astype(np.float32), "cam_fwd": fwd.astype(np.float32),
+            "cam_right": (right * th * width / height).astype(np.float32),
+            "cam_up": (upv * th).astype(np.float32), "width": width, "height": height}
+
+
+def policy(static_mask=0xFFFFFFFF, level_strategy=0, beta=0.0, orient_strategy=0, delta=1.0):
+    return {"static_mask": static_mask & 0xFFFFFFFF, "level_strategy": level_strategy, "beta": beta,
+            "orient_strategy": orient_strategy, "delta": delta}
+
+
+SUN = (np.array([1.0, 1.0, 0.5]) / np.linalg.norm([1.0, 1.0, 0.5])).astype(np.float32)
+
+
+def render_desc_cfg1(width=64, height=64, seed=RENDER_SEED + 1):
+    d = camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, width, height)
+    d.update(mode=0, max_depth=1, jitter=0, albedo=1.0, hg_g=0.0, sun_dir=SUN, sun_E=0.0, env_L=0.0, seed=seed,
+             ext=policy(), nee=policy())
+    return d
+
+
+CFG2_LOD_LEVELS = ([0], [0, 1], [0, 1, 2], [0, 1, 2, 3])
+
+
+def render_desc_cfg2(mask_index=3, width=1024, height=1024, seed=RENDER_SEED + 2):
+    """Config 2: single scattering, one of the 4 static LOD masks (levels {0},{0,1},{0..2},{0..3})."""
+    d = camera((0, 0.3, 3.2), (0, 0.05, 0), (0, 1, 0), 40.0, width, height)
+    m = level_mask(CFG2_LOD_LEVELS[mask_index])
+    d.update(mode=1, max_depth=1, jitter=1, albedo=0.8, hg_g=0.0, sun_dir=SUN, sun_E=3.0, env_L=0.2,
+             seed=seed + 0x100 * mask_index, ext=policy(static_mask=m), nee=policy(static_mask=m))
+    return d
+
+
+def camera_rays_f64(desc, px, py, jx=0.5, jy=0.5):
+    """Camera rays computed in float64 numpy from the fp32 frame (for picking test rays; the
+    kernels and the oracle each compute their own fp32 camera rays)."""
+    px, py = np.asarray(px, np.float64), np.asarray(py, np.float64)
+    sx = 2 * (px + jx) / desc["width"] - 1
+    sy = 1 - 2 * (py + jy) / desc["height"]
+    d = (desc["cam_fwd"][None].astype(np.float64) + sx[:, None] * desc["cam_right"][None]
+         + sy[:, None] * desc["cam_up"][None])
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = np.broadcast_to(desc["cam_pos"].astype(np.float64), d.shape)
+    return o, d
+
+
+def rays_through_box(seed, n, lo=-1.0, hi=1.0, dist=4.0, tmin=0.0, tmax=np.inf):
+    """n rays (n x 8 fp32) from a sphere of radius `dist` aimed at random points in the box."""
+    rng = np.random.default_rng(seed)
+    tgt = rng.uniform(lo, hi, (n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = tgt - dist * d
+    return pack_rays(o, d, tmin, tmax)
+
+
+def pack_rays(o, d, tmin=0.0, tmax=np.inf):
+    n = o.shape[0]
+    d = np.asarray(d, np.float64)
+    d = d / np.linalg.norm(d, axis=1, keepdims=True)
+    r = np.zeros((n, 8), np.float32)
+    r[:, 0:3] = o
+    r[:, 3] = tmin
+    r[:, 4:7] = d
+    r[:, 7] = tmax
+    return r
+
+
+def far_origin_pairs(seed, n, ratio, s_lo=0.005, s_hi=0.05):
+    """Far-origin stress set: single primitives of scale s in [s_lo,s_hi] placed at
+    random, rays starting |o-mu|/s = ratio away, passing within the 3-sigma ellipsoid."""
+    rng = np.random.default_rng(seed)
+    s = np.exp(rng.uniform(np.log(s_lo), np.log(s_hi), n))
+    scale = s[:, None] * np.exp(rng.normal(0, 0.25, (n, 3)))
+    mu = rng.uniform(-1, 1, (n, 3))
+    quat = random_quats(rng, n)
+    omega = rng.uniform(0.7, 1.5, n)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    off = rng.normal(size=(n, 3))
+    off -= (off * d).sum(1, keepdims=True) * d
+    off /= np.linalg.norm(off, axis=1, keepdims=True)
+    off *= (rng.uniform(0, 2.0, n) * s)[:, None]  # perpendicular miss distance, world units
+    o = mu + off - (ratio * s)[:, None] * d
+    return {"mu": mu, "quat": quat, "scale": scale, "omega": omega, "rays": pack_rays(o, d)}
