@@ -1,0 +1,242 @@
+/*
+ * gf.h -- C ABI of the B200-native Gabor Fields hot path (arXiv 2602.05081).
+ *
+ * One shared library, libgf.so (paper_2602_05081_b200/libgf.so), hand-written
+ * sm_100a CUDA kernels behind plain C entry points: no torch types, only
+ * pointers, sizes and a CUDA stream handle.  Citations "P:Lnnn" are lines of
+ * PAPER.md; "C<n>" are the readings listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Memory ownership: the CALLER allocates every buffer (the library never
+ *    calls cudaMalloc after gf_create).  Pointers documented as "device" must
+ *    be device (or managed) memory of the context's device; "host" pointers are
+ *    read during the call only.  The context keeps non-owning pointers to the
+ *    workspaces passed to gf_load_primitives / gf_build_bvh; they must outlive
+ *    the context or the next gf_load_primitives.
+ *  - Streams: every call enqueues asynchronously on `stream` (a cudaStream_t,
+ *    NULL = legacy default stream).  Only gf_load_primitives and gf_build_bvh
+ *    synchronise the stream (to surface data errors found on the device).
+ *  - Errors: a non-GF_OK status is returned synchronously for argument / state
+ *    errors; gf_last_error(ctx) then holds a message.  Asynchronous CUDA faults
+ *    surface as GF_E_CUDA at the next call.  No exception or abort crosses the ABI.
+ *  - Thread safety: one context per device and per host thread at a time;
+ *    distinct contexts are independent.
+ *  - Determinism: results are bitwise deterministic for a given (scene, rays,
+ *    policies, seed, shard layout).
+ */
+#ifndef GF_H
+#define GF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GF_ABI_VERSION 1
+#define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
+#define GF_MAX_LEVELS 8
+
+typedef enum {
+    GF_OK = 0,
+    GF_E_INVALID_ARGUMENT = 1,    /* null/ill-sized argument, n < 0, bad enum value              */
+    GF_E_STATE = 2,               /* call order: trace/render before load + build               */
+    GF_E_SINGULAR_COVARIANCE = 3, /* scale <= 0, non-finite, or cond(S) > 1e6           */
+    GF_E_INVALID_RAY = 4,         /* (reserved: rays are not validated on the hot path)           */
+    GF_E_INVALID_BOUNDS = 5,      /* extent E <= 0 or non-finite                                  */
+    GF_E_MASK_OVERFLOW = 6,       /* G = 1 + (P-1) K > 32 groups (C24)                             */
+    GF_E_INVALID_STRATEGY = 7,    /* beta not in [0,1), delta not in [0,1], unknown strategy      */
+    GF_E_ASSIGNMENT = 8,          /* level >= P or bin >= K in the input, bad quaternion norm     */
+    GF_E_CUDA = 9,                /* CUDA runtime error (message in gf_last_error)                */
+    GF_E_OUT_OF_MEMORY = 10       /* a caller workspace is smaller than the queried size          */
+} gf_status;
+
+typedef struct gf_ctx gf_ctx;   /* opaque, one per CUDA device */
+typedef void *gf_stream;        /* cudaStream_t */
+
+/* ---- context ------------------------------------------------------------ */
+int gf_abi_version(void);
+const char *gf_status_string(gf_status s);
+/* Create a context on CUDA device `cuda_device`.  Allocates its small
+ * internal state (error flag, counters) once. */
+gf_status gf_create(int cuda_device, gf_ctx **out);
+void gf_destroy(gf_ctx *ctx);
+/* message of the last non-OK status returned for this context ("" if none) */
+const char *gf_last_error(const gf_ctx *ctx);
+
+/* ---- sizes -------------------------------------------------------------- */
+/* Bytes the caller must provide for n primitives: prim_bytes for
+ * gf_load_primitives, bvh_bytes + scratch_bytes for gf_build_bvh.  Pure
+ * host computation except the radix-sort temp size (needs a CUDA device). */
+gf_status gf_query_workspace(int64_t n_prims, size_t *prim_bytes, size_t *bvh_bytes, size_t *scratch_bytes);
+
+/* ---- a1: primitive ingest + pyramid partition ----------- */
+/* Primitive arrays, DEVICE pointers, structure of arrays, fp32:
+ *   mu[3n] kernel means; quat[4n] unit quaternions (x,y,z,w), |q| = 1 +- 1e-5;
+ *   scale[3n] principal standard deviations s (> 0, max/min <= 1e6);
+ *   alpha[n] kernel weights (Eq. 1, >= 0); omega[n] modulation scalar (P:L183:
+ *   omega_vec = R S^-1 (omega,omega,omega)^T, >= 0; 0 = Gaussian);
+ *   extent[n] whitened truncation radius E (C7/C8), NULL -> 3 (the 3 sigma bound);
+ *   level[n] pyramid level (0 = Gaussians), NULL -> derived from level_cutoffs (C10);
+ *   bin[n] orientation bin, NULL or 255 -> derived: argmax_k |omega_vec . o_k| in fp32 (C11). */
+typedef struct {
+    const float *mu, *quat, *scale, *alpha, *omega, *extent;
+    const uint8_t *level, *bin;
+} gf_prims;
+
+/* Pyramid description, HOST pointers:
+ *   n_levels P (1..8), n_bins K (>= 1), G = 1 + (P-1) K <= 32 groups;
+ *   group id g(0,*) = 0, g(l,b) = 1 + (l-1) K + b  (C24);
+ *   bin_axes[3K] unit axes o_k (C11);
+ *   level_cutoffs[P-2] ascending world peak frequencies f0 = |omega_vec| separating
+ *     Gabor levels 1..P-1 (used only when prims.level == NULL; may be NULL otherwise);
+ *   group_f0[G] representative whitened frequency per group for the Importance
+ *     orientation strategy (C12); NULL -> 0 (uniform importance). */
+typedef struct {
+    int32_t n_levels;
+    int32_t n_bins;
+    const float *bin_axes;
+    const float *level_cutoffs;
+    const float *group_f0;
+} gf_pyramid;
+
+/* Convert n primitives into the 64-byte device records (W = S^-1 R^T whitening,
+ * c = alpha/(2 pi s1 s2 s3), E^2, group) stored in prim_ws (device, >= prim_bytes).
+ * Validates on the device and synchronises `stream`; returns the first error
+ * class found (GF_E_SINGULAR_COVARIANCE, GF_E_INVALID_BOUNDS, GF_E_ASSIGNMENT).
+ * n == 0 is valid (empty scene: every ray has tau = 0). Invalidates the BVH. */
+gf_status gf_load_primitives(gf_ctx *ctx, const gf_prims *prims, int64_t n, const gf_pyramid *pyr,
+                             void *prim_ws, size_t prim_ws_bytes, gf_stream stream);
+
+/* ---- a2: bounds + LBVH build ------------------------------- */
+/* Conservative world AABBs of the ellipsoids, 64-bit keys (group << 57 | Morton57
+ * of the centre), radix sort (CUB), Karras hierarchy, bottom-up refit with group
+ * masks, collapse to leaves of <= 4 single-group primitives, depth-first layout
+ * with escape links.  Group bits are the top key bits, so the top of the tree
+ * routes by group: one tree playing the role of the paper's per-level GAS +
+ * masked TLAS.  bvh_ws (device, >= bvh_bytes) holds the nodes and the reordered
+ * primitives and must stay alive; scratch (device, >= scratch_bytes) may be
+ * reused after the call.  Synchronises `stream`. */
+gf_status gf_build_bvh(gf_ctx *ctx, void *bvh_ws, size_t bvh_ws_bytes, void *scratch, size_t scratch_bytes,
+                       gf_stream stream);
+
+/* ---- a3: LOD policy (Tables B1/B2) ------------- */
+typedef enum {
+    GF_LEVEL_DETERMINISTIC = 0, GF_LEVEL_UNIFORM = 1, GF_LEVEL_POWERLAW = 2, GF_LEVEL_UNIFORM_CV = 3,
+    GF_LEVEL_POWERLAW_CV = 4, GF_LEVEL_POWERLAW_CV_ACCUM = 5
+} gf_level_strategy;
+typedef enum {
+    GF_ORIENT_DETERMINISTIC = 0, GF_ORIENT_THRESHOLD_CULL = 1, GF_ORIENT_UNIFORM = 2,
+    GF_ORIENT_IMPORTANCE = 3, GF_ORIENT_THRESHOLD_UNIFORM = 4
+} gf_orient_strategy;
+
+/* Per ray segment: mask = (stochastic level x orientation draw) & static_mask;
+ * group weight w_g = w_level * w_bin (reciprocal probabilities, readings C13-C15).
+ * Deterministic/Deterministic with static_mask = the static LOD masks. */
+typedef struct {
+    uint32_t static_mask;
+    int32_t level_strategy;   /* gf_level_strategy */
+    float beta;               /* power-law shape, [0,1) */
+    int32_t orient_strategy;  /* gf_orient_strategy */
+    float delta;              /* alignment threshold, [0,1] */
+} gf_lod_policy;
+
+/* Set the policy of camera/extension segments (`ext`) and of next-event /
+ * shadow segments (`nee`, NULL -> same as ext; "Zero NEE" = static_mask 1,
+ * P:L365).  Host pointers; takes effect for later calls. */
+gf_status gf_set_lod_mask(gf_ctx *ctx, const gf_lod_policy *ext, const gf_lod_policy *nee);
+
+/* ---- a4-a7: masked traversal + fused line integral + transmittance -------- */
+/* rays: device, n x 8 fp32 (ox,oy,oz,tmin, dx,dy,dz,tmax), |d| = 1, tmin < tmax,
+ * tmax may be +inf.  tau_out: device n fp32 optical depth tau = sum_i w_g alpha_i
+ * int_tmin^tmax K_i (Eq. 2, App. A closed form, C3-C5), accumulated in fp64.
+ * T_out: device n fp32 exp(-tau) (Eq. 3) or NULL.  The `ext` policy applies;
+ * stochastic strategies draw uniforms (seed, pixel = ray index, sample 0,
+ * depth 0, stream 0).  counters_out: device n x 3 uint32
+ * (nodes visited, primitives tested, hits) or NULL. */
+gf_status gf_trace_transmittance(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, float *tau_out,
+                                 float *T_out, uint32_t *counters_out, gf_stream stream);
+
+#define GF_TRACE_BRUTE_FORCE 1u   /* test path: test every primitive, no BVH */
+/* As gf_trace_transmittance with flags (GF_TRACE_BRUTE_FORCE). */
+gf_status gf_trace_transmittance_ex(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, uint32_t flags,
+                                    float *tau_out, float *T_out, uint32_t *counters_out, gf_stream stream);
+
+/* Candidate sets (test path, C21): for each ray, the ORIGINAL indices of the
+ * primitives accepted by the fp32 ellipsoid predicate (traversal order),
+ * ids[r * capacity + k], count[r] = total (may exceed capacity: truncated). */
+gf_status gf_trace_candidates(gf_ctx *ctx, const float *rays, int64_t n, uint32_t flags, int32_t *ids,
+                              int32_t capacity, int32_t *count, gf_stream stream);
+
+/* ---- a8-a10: free flight + scatter loop + accumulation -------------------- */
+typedef enum { GF_MODE_TOMOGRAPHY = 0, GF_MODE_SCATTER = 1 } gf_render_mode;
+typedef enum { GF_SHARD_NONE = 0, GF_SHARD_TILES = 1, GF_SHARD_SAMPLES = 2 } gf_shard_kind;
+
+/* Camera: pinhole; for pixel (px,py) and jitter (jx,jy) in [0,1):
+ *   sx = (px+jx) (2/W) - 1, sy = 1 - (py+jy)(2/H), d = normalize(fwd + sx right + sy up)
+ * with right/up pre-scaled by tan(vfov/2) (*aspect), evaluated in fp32 with
+ * correctly rounded operations.  jitter = 0 -> pixel centres.
+ * TOMOGRAPHY: per sample tau-hat of the camera ray.
+ * SCATTER: free flight (Eq. 5, bins + safeguarded Newton, C17), NEE to the
+ *   directional light (sun_dir towards the light, irradiance sun_E) with the
+ *   nee policy, Henyey-Greenstein phase (g), grey albedo, constant env_L on
+ *   escape, max_depth vertices (1 = single scattering), no Russian roulette (C19).
+ * RNG: Philox4x32-10, key = seed, counter = (pixel, sample, depth, stream<<16 | k>>2). */
+typedef struct {
+    int32_t mode;               /* gf_render_mode */
+    int32_t width, height;
+    int32_t max_depth;          /* >= 1 (SCATTER) */
+    int32_t jitter;             /* 0 = pixel centres */
+    int32_t spp_begin, spp_count;
+    int32_t shard_kind;         /* gf_shard_kind */
+    int32_t shard_rank, shard_world;
+    const int32_t *probe_pixels; /* device, n_probe pixel indices (y*W+x) or NULL = full image */
+    int64_t n_probe;
+    float cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3];
+    float albedo, hg_g, sun_dir[3], sun_E, env_L;
+    uint64_t seed;
+} gf_render_desc;
+
+/* Device scratch needed by gf_render for `desc`. */
+gf_status gf_render_scratch_bytes(gf_ctx *ctx, const gf_render_desc *desc, size_t *bytes);
+
+/* Render.  accum (device fp32):
+ *   full image (probe_pixels == NULL): H*W*2, accum[2p] += sum of estimates,
+ *     accum[2p+1] += sum of squared estimates over this call's samples of pixel p
+ *     (only the shard's pixels/samples are touched; caller zeroes it);
+ *   probes: n_probe * spp_count, accum[i*spp_count + k] = estimate of sample
+ *     spp_begin + k at probe i (overwritten).
+ * ray_counts: device uint64[2] or NULL, += (camera+extension rays, NEE rays). */
+gf_status gf_render(gf_ctx *ctx, const gf_render_desc *desc, float *accum, void *scratch, size_t scratch_bytes,
+                    uint64_t *ray_counts, gf_stream stream);
+
+/* ---- measurement (bench.py roofline / launch counts) ---------------------- */
+#define GF_PROFILE_TIMING 1u  /* record CUDA events around every kernel launch (on its stream)   */
+#define GF_PROFILE_WORK 2u    /* use the counting kernel variants (work[] below; slower)          */
+/* Stages: 0 gen (camera rays), 1 ffA (free flight, binned tau), 2 ffB (root find), 3 nee (shadow
+ * rays + phase sampling), 4 finish (queue rotation + accumulation), 5 tomo, 6 trace
+ * (gf_trace_transmittance), 7 build (unused). */
+typedef struct {
+    uint64_t launches;           /* kernels launched by the library since the last reset        */
+    uint64_t stage_launches[8];
+    double stage_ms[8];          /* summed event time per stage (GF_PROFILE_TIMING)             */
+    uint64_t work[8][12];        /* GF_PROFILE_WORK, per stage: nodes visited, primitives tested,
+                                    hits, complex-erf endpoint evaluations (Eq. 13 series), real
+                                    erf evaluations (Omega = 0), Gauss-Legendre fallbacks, ffB
+                                    overflow brackets, root-finder evaluations, paths/rays, 3 spare */
+} gf_stats;
+gf_status gf_set_profiling(gf_ctx *ctx, uint32_t flags);
+/* Synchronises the context's device, fills *out, optionally resets the counters. */
+gf_status gf_get_stats(gf_ctx *ctx, gf_stats *out, int32_t reset);
+
+/* ---- e: multi-GPU shard assignment (host only, no device) ---------------- */
+/* Owner rank of pixel (px,py) under tile-interleaved sharding (32x32 tiles, tile t -> rank t mod world). */
+int32_t gf_shard_pixel_owner(int32_t px, int32_t py, int32_t width, int32_t height, int32_t world);
+/* Owner rank of sample s under sample-interleaved sharding (s mod world). */
+int32_t gf_shard_sample_owner(int32_t s, int32_t world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GF_H */

@@ -1,0 +1,469 @@
+// gf_api.cu -- the C ABI (include/gf.h): context, validation, workspaces, orchestration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gf.h"
+#include "gf_internal.h"
+
+using namespace gfk;
+
+struct gf_ctx {
+    int device = 0;
+    std::string err;
+    uint32_t* d_err = nullptr;            // [4] load error bits, first bad index
+    unsigned long long* d_rays = nullptr;  // [2] dummy ray counters
+    // scene
+    bool loaded = false, built = false;
+    int64_t n = 0;
+    SceneDev sc{};
+    GPrim* prims = nullptr;  // input order (prim_ws)
+    GNode* nodes = nullptr;  // bvh_ws
+    GPrim* sorted = nullptr;
+    uint32_t n_nodes = 0;
+    float root[6] = {0, 0, 0, 0, 0, 0};
+    // policies
+    gf_lod_policy ext{0xFFFFFFFFu, 0, 0.0f, 0, 1.0f}, nee{0xFFFFFFFFu, 0, 0.0f, 0, 1.0f};
+    PolicyDev dext{}, dnee{};
+    // measurement
+    uint32_t prof = 0;
+    StageTimer timer;
+    unsigned long long* d_work = nullptr;  // [8 stages][kWorkSlots]
+    double stage_ms[N_STAGES] = {};
+};
+
+cudaEvent_t StageTimer::ev() {
+    if (pool_used == pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        pool.push_back(e);
+    }
+    return pool[pool_used++];
+}
+void StageTimer::pre(int stage, cudaStream_t st, cudaEvent_t& a) {
+    ++launches;
+    ++stage_launches[stage];
+    if (!on) return;
+    a = ev();
+    cudaEventRecord(a, st);
+}
+void StageTimer::post(int stage, cudaStream_t st, cudaEvent_t a) {
+    if (!on) return;
+    cudaEvent_t b = ev();
+    cudaEventRecord(b, st);
+    recs.push_back({stage, a, b});
+}
+
+// fold recorded events into per-stage milliseconds (synchronises on the events)
+static void harvest(gf_ctx* c) {
+    StageTimer& T = c->timer;
+    for (auto& r : T.recs) {
+        float ms = 0.0f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        c->stage_ms[r.stage] += ms;
+    }
+    T.recs.clear();
+    T.pool_used = 0;
+}
+
+static gf_status fail(gf_ctx* c, gf_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+static gf_status cuda_fail(gf_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, GF_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define GF_CUDA(c, call, where)                              \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
+    } while (0)
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static PolicyDev make_policy_dev(const gf_lod_policy& p, int P) {
+    PolicyDev d{};
+    d.static_mask = p.static_mask;
+    d.ls = p.level_strategy;
+    d.os = p.orient_strategy;
+    d.delta = p.delta;
+    const double om = 1.0 - (double)p.beta;  // same expression as the decision rule
+    for (int j = 0; j <= P && j <= kMaxLevels; ++j) d.th[j] = std::pow((double)j / P, om);
+    for (int j = 0; j < P && j < kMaxLevels; ++j) {
+        d.w_pl[j] = (float)(1.0 / (std::pow((double)(j + 1) / P, om) - std::pow((double)j / P, om)));
+        d.w_acc[j] = (float)(1.0 / (1.0 - std::pow((double)j / P, om)));
+    }
+    if (P > 1) {
+        const int Q = P - 1;
+        for (int k = 0; k <= Q && k <= kMaxLevels; ++k) d.psi[k] = std::pow((double)k / Q, om);
+        for (int k = 0; k < Q && k < kMaxLevels; ++k)
+            d.w_plcv[k] = (float)(1.0 / (std::pow((double)(k + 1) / Q, om) - std::pow((double)k / Q, om)));
+    }
+    return d;
+}
+
+static gf_status check_policy(gf_ctx* c, const gf_lod_policy& p) {
+    if (p.level_strategy < 0 || p.level_strategy > 5 || p.orient_strategy < 0 || p.orient_strategy > 4)
+        return fail(c, GF_E_INVALID_STRATEGY, "unknown strategy");
+    if (!(p.beta >= 0.0f && p.beta < 1.0f)) return fail(c, GF_E_INVALID_STRATEGY, "beta must be in [0,1)");
+    if (!(p.delta >= 0.0f && p.delta <= 1.0f)) return fail(c, GF_E_INVALID_STRATEGY, "delta must be in [0,1]");
+    return GF_OK;
+}
+
+static gf_status check_sticky(gf_ctx* c) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "pending CUDA error");
+    return GF_OK;
+}
+
+extern "C" {
+
+int gf_abi_version(void) { return GF_ABI_VERSION; }
+
+const char* gf_status_string(gf_status s) {
+    switch (s) {
+    case GF_OK: return "ok";
+    case GF_E_INVALID_ARGUMENT: return "invalid argument";
+    case GF_E_STATE: return "invalid call order";
+    case GF_E_SINGULAR_COVARIANCE: return "singular covariance";
+    case GF_E_INVALID_RAY: return "invalid ray";
+    case GF_E_INVALID_BOUNDS: return "invalid bounds";
+    case GF_E_MASK_OVERFLOW: return "mask overflow";
+    case GF_E_INVALID_STRATEGY: return "invalid strategy";
+    case GF_E_ASSIGNMENT: return "assignment error";
+    case GF_E_CUDA: return "CUDA error";
+    case GF_E_OUT_OF_MEMORY: return "workspace too small";
+    }
+    return "unknown status";
+}
+
+gf_status gf_create(int cuda_device, gf_ctx** out) {
+    if (!out) return GF_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return GF_E_CUDA;
+    if ((e = cudaSetDevice(cuda_device)) != cudaSuccess) return GF_E_CUDA;
+    gf_ctx* c = new gf_ctx();
+    c->device = cuda_device;
+    if (cudaMalloc(&c->d_err, 4 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&c->d_rays, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->d_work, 8 * kWorkSlots * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(c->d_work, 0, 8 * kWorkSlots * sizeof(unsigned long long)) != cudaSuccess) {
+        delete c;
+        return GF_E_CUDA;
+    }
+    c->dext = make_policy_dev(c->ext, 4);
+    c->dnee = make_policy_dev(c->nee, 4);
+    *out = c;
+    return GF_OK;
+}
+
+void gf_destroy(gf_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    harvest(c);
+    for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
+    cudaFree(c->d_err);
+    cudaFree(c->d_rays);
+    cudaFree(c->d_work);
+    delete c;
+}
+
+const char* gf_last_error(const gf_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+gf_status gf_query_workspace(int64_t n, size_t* prim_bytes, size_t* bvh_bytes, size_t* scratch_bytes) {
+    if (n < 0 || n >= (1 << 24)) return GF_E_INVALID_ARGUMENT;
+    if (prim_bytes) *prim_bytes = align256(sizeof(GPrim) * (size_t)std::max<int64_t>(n, 1));
+    if (bvh_bytes)
+        *bvh_bytes = align256(sizeof(GPrim) * (size_t)std::max<int64_t>(n, 1)) +
+                     align256(sizeof(GNode) * (size_t)std::max<int64_t>(2 * n, 1));
+    if (scratch_bytes) {
+        if (n > 0) {
+            int ndev = 0;
+            if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return GF_E_CUDA;
+        }
+        *scratch_bytes = gf_scratch_layout(n, nullptr).total_bytes;
+    }
+    return GF_OK;
+}
+
+gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_pyramid* pyr, void* prim_ws,
+                             size_t bytes, gf_stream stream) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (!p || !pyr || n < 0) return fail(c, GF_E_INVALID_ARGUMENT, "null argument or n < 0");
+    if (n >= (1 << 24)) return fail(c, GF_E_INVALID_ARGUMENT, "n must be < 2^24");
+    if (n > 0 && (!p->mu || !p->quat || !p->scale || !p->alpha || !p->omega || !prim_ws))
+        return fail(c, GF_E_INVALID_ARGUMENT, "null primitive array");
+    const int P = pyr->n_levels, K = pyr->n_bins;
+    if (P < 1 || P > kMaxLevels || K < 1 || K > 16) return fail(c, GF_E_INVALID_ARGUMENT, "bad n_levels / n_bins");
+    if (1 + (P - 1) * K > GF_MAX_GROUPS) return fail(c, GF_E_MASK_OVERFLOW, "1 + (P-1) K > 32 groups");
+    if (!pyr->bin_axes) return fail(c, GF_E_INVALID_ARGUMENT, "bin_axes required");
+    if (n > 0 && !p->level && P > 2 && !pyr->level_cutoffs)
+        return fail(c, GF_E_INVALID_ARGUMENT, "level_cutoffs required when level == NULL");
+    size_t need = 0;
+    gf_query_workspace(n, &need, nullptr, nullptr);
+    if (bytes < need) return fail(c, GF_E_OUT_OF_MEMORY, "prim_ws too small");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    c->loaded = c->built = false;
+    LoadArgs A{};
+    A.n = n; A.mu = p->mu; A.quat = p->quat; A.scale = p->scale; A.alpha = p->alpha; A.omega = p->omega;
+    A.extent = p->extent; A.level = p->level; A.bin = p->bin; A.P = P; A.K = K;
+    for (int i = 0; i < P - 2 && pyr->level_cutoffs; ++i) A.cutoffs[i] = pyr->level_cutoffs[i];
+    for (int i = 0; i < 3 * K; ++i) A.axes[i] = pyr->bin_axes[i];
+    uint32_t init[4] = {0u, 0xFFFFFFFFu, 0u, 0u};
+    GF_CUDA(c, cudaMemcpyAsync(c->d_err, init, sizeof(init), cudaMemcpyHostToDevice, st), "memcpy");
+    GF_CUDA(c, gf_launch_load(A, prim_ws, c->d_err, st), "k_load_prims");
+    uint32_t herr[4];
+    GF_CUDA(c, cudaMemcpyAsync(herr, c->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st), "memcpy");
+    GF_CUDA(c, cudaStreamSynchronize(st), "load sync");
+    if (herr[0]) {
+        char msg[160];
+        snprintf(msg, sizeof(msg), "invalid primitive (first index %u, error bits 0x%x)", herr[1], herr[0]);
+        if (herr[0] & 1u) return fail(c, GF_E_SINGULAR_COVARIANCE, msg);
+        if (herr[0] & 2u) return fail(c, GF_E_INVALID_BOUNDS, msg);
+        if (herr[0] & 12u) return fail(c, GF_E_ASSIGNMENT, msg);
+        return fail(c, GF_E_INVALID_ARGUMENT, msg);
+    }
+    c->n = n;
+    c->sc.P = P; c->sc.K = K; c->sc.G = 1 + (P - 1) * K;
+    for (int i = 0; i < 3 * K; ++i) c->sc.axes[i] = pyr->bin_axes[i];
+    for (int g = 0; g < kMaxGroups; ++g) c->sc.f0[g] = (pyr->group_f0 && g < c->sc.G) ? pyr->group_f0[g] : 0.0f;
+    c->prims = (GPrim*)prim_ws;
+    c->dext = make_policy_dev(c->ext, P);
+    c->dnee = make_policy_dev(c->nee, P);
+    c->loaded = true;
+    return GF_OK;
+}
+
+gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch, size_t scratch_bytes,
+                       gf_stream stream) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (!c->loaded) return fail(c, GF_E_STATE, "gf_build_bvh before gf_load_primitives");
+    size_t nb = 0, ns = 0;
+    if (gf_status s = gf_query_workspace(c->n, nullptr, &nb, &ns)) return fail(c, s, "workspace query failed");
+    if (c->n > 0 && (!bvh_ws || !scratch)) return fail(c, GF_E_INVALID_ARGUMENT, "null workspace");
+    if (bvh_bytes < nb || scratch_bytes < ns) return fail(c, GF_E_OUT_OF_MEMORY, "bvh_ws or scratch too small");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    char* base = (char*)bvh_ws;
+    c->sorted = (GPrim*)base;
+    c->nodes = (GNode*)(base + align256(sizeof(GPrim) * (size_t)std::max<int64_t>(c->n, 1)));
+    BuildScratch S = gf_scratch_layout(c->n, (char*)scratch);
+    uint32_t nn = 0;
+    GF_CUDA(c, gf_launch_build(c->prims, c->n, S, c->nodes, c->sorted, &nn, c->root, st), "gf_build_bvh");
+    c->n_nodes = nn;
+    c->built = true;
+    return GF_OK;
+}
+
+gf_status gf_set_lod_mask(gf_ctx* c, const gf_lod_policy* ext, const gf_lod_policy* nee) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (!ext) return fail(c, GF_E_INVALID_ARGUMENT, "ext policy required");
+    if (gf_status s = check_policy(c, *ext)) return s;
+    if (nee)
+        if (gf_status s = check_policy(c, *nee)) return s;
+    c->ext = *ext;
+    c->nee = nee ? *nee : *ext;
+    const int P = c->loaded ? c->sc.P : 4;
+    c->dext = make_policy_dev(c->ext, P);
+    c->dnee = make_policy_dev(c->nee, P);
+    return GF_OK;
+}
+
+static gf_status trace_common(gf_ctx* c, const float* rays, int64_t n, TraceArgs& A, uint32_t flags) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (!c->loaded || (!c->built && !(flags & GF_TRACE_BRUTE_FORCE)))
+        return fail(c, GF_E_STATE, "trace before gf_load_primitives / gf_build_bvh");
+    if (n < 0 || (n > 0 && !rays)) return fail(c, GF_E_INVALID_ARGUMENT, "bad rays");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    A = TraceArgs{};
+    const bool brute = flags & GF_TRACE_BRUTE_FORCE;
+    A.nodes = c->nodes;
+    A.n_nodes = c->built ? c->n_nodes : 0;
+    A.prims = brute ? c->prims : c->sorted;
+    A.n_prims = c->n;
+    A.pol = c->dext;
+    A.sc = c->sc;
+    A.rays = rays;
+    A.n = n;
+    return GF_OK;
+}
+
+gf_status gf_trace_transmittance_ex(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, uint32_t flags,
+                                    float* tau_out, float* T_out, uint32_t* counters, gf_stream stream) {
+    TraceArgs A;
+    if (gf_status s = trace_common(c, rays, n, A, flags)) return s;
+    if (n > 0 && !tau_out) return fail(c, GF_E_INVALID_ARGUMENT, "tau_out required");
+    A.seed = seed;
+    A.tau = tau_out;
+    A.T = T_out;
+    A.counters = counters;
+    A.work = (c->prof & GF_PROFILE_WORK) ? c->d_work : nullptr;
+    cudaEvent_t ev;
+    c->timer.pre(STAGE_TRACE, (cudaStream_t)stream, ev);
+    GF_CUDA(c, gf_launch_trace(A, flags & GF_TRACE_BRUTE_FORCE, counters != nullptr, (cudaStream_t)stream),
+            "k_trace");
+    c->timer.post(STAGE_TRACE, (cudaStream_t)stream, ev);
+    return GF_OK;
+}
+
+gf_status gf_trace_transmittance(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, float* tau_out,
+                                 float* T_out, uint32_t* counters, gf_stream stream) {
+    return gf_trace_transmittance_ex(c, rays, n, seed, 0u, tau_out, T_out, counters, stream);
+}
+
+gf_status gf_trace_candidates(gf_ctx* c, const float* rays, int64_t n, uint32_t flags, int32_t* ids,
+                              int32_t capacity, int32_t* count, gf_stream stream) {
+    TraceArgs A;
+    if (gf_status s = trace_common(c, rays, n, A, flags)) return s;
+    if (capacity < 0 || (n > 0 && (!count || (capacity > 0 && !ids))))
+        return fail(c, GF_E_INVALID_ARGUMENT, "bad candidate buffers");
+    A.cand_ids = ids;
+    A.cand_cap = capacity;
+    A.cand_count = count;
+    GF_CUDA(c, gf_launch_candidates(A, flags & GF_TRACE_BRUTE_FORCE, (cudaStream_t)stream), "k_candidates");
+    return GF_OK;
+}
+
+static int64_t render_paths(const gf_render_desc* d) {
+    if (d->probe_pixels) return d->n_probe;
+    const int64_t tx = (d->width + 31) / 32, ty = (d->height + 31) / 32, tiles = tx * ty;
+    if (d->shard_kind == GF_SHARD_TILES) {
+        const int64_t mine = tiles > d->shard_rank ? (tiles - d->shard_rank + d->shard_world - 1) / d->shard_world : 0;
+        return mine * 1024;
+    }
+    return tiles * 1024;
+}
+
+static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
+    if (!d) return fail(c, GF_E_INVALID_ARGUMENT, "null desc");
+    if (d->mode != GF_MODE_TOMOGRAPHY && d->mode != GF_MODE_SCATTER) return fail(c, GF_E_INVALID_ARGUMENT, "bad mode");
+    if (d->width <= 0 || d->height <= 0 || (int64_t)d->width * d->height >= (1ll << 31))
+        return fail(c, GF_E_INVALID_ARGUMENT, "bad image size");
+    if (d->mode == GF_MODE_SCATTER && (d->max_depth < 1 || d->max_depth > 1024))
+        return fail(c, GF_E_INVALID_ARGUMENT, "max_depth must be in [1,1024]");
+    if (d->spp_count < 0 || d->spp_begin < 0) return fail(c, GF_E_INVALID_ARGUMENT, "bad spp range");
+    if (d->shard_kind < 0 || d->shard_kind > 2) return fail(c, GF_E_INVALID_ARGUMENT, "bad shard kind");
+    if (d->shard_kind != GF_SHARD_NONE && (d->shard_world < 1 || d->shard_rank < 0 || d->shard_rank >= d->shard_world))
+        return fail(c, GF_E_INVALID_ARGUMENT, "bad shard rank/world");
+    if (d->probe_pixels && (d->n_probe < 0 || d->shard_kind == GF_SHARD_TILES))
+        return fail(c, GF_E_INVALID_ARGUMENT, "probe mode: n_probe >= 0 and no tile sharding");
+    if (!(d->hg_g > -1.0f && d->hg_g < 1.0f)) return fail(c, GF_E_INVALID_ARGUMENT, "hg_g must be in (-1,1)");
+    return GF_OK;
+}
+
+gf_status gf_render_scratch_bytes(gf_ctx* c, const gf_render_desc* d, size_t* bytes) {
+    if (!c || !bytes) return GF_E_INVALID_ARGUMENT;
+    if (gf_status s = check_desc(c, d)) return s;
+    *bytes = gf_render_state_bytes(std::max<int64_t>(render_paths(d), 1), nullptr, nullptr);
+    return GF_OK;
+}
+
+gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scratch, size_t scratch_bytes,
+                    uint64_t* ray_counts, gf_stream stream) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (gf_status s = check_desc(c, d)) return s;
+    if (!c->loaded || !c->built) return fail(c, GF_E_STATE, "render before gf_load_primitives / gf_build_bvh");
+    const int64_t np = render_paths(d);
+    size_t need = gf_render_state_bytes(std::max<int64_t>(np, 1), nullptr, nullptr);
+    if (scratch_bytes < need || !scratch) return fail(c, GF_E_OUT_OF_MEMORY, "render scratch too small");
+    if (!accum && np > 0) return fail(c, GF_E_INVALID_ARGUMENT, "accum required");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    RenderDev R{};
+    gf_render_state_bytes(std::max<int64_t>(np, 1), (char*)scratch, &R);
+    R.nodes = c->nodes;
+    R.n_nodes = c->n_nodes;
+    R.prims = c->sorted;
+    R.ext = c->dext;
+    R.nee = c->dnee;
+    R.sc = c->sc;
+    for (int k = 0; k < 3; ++k) {
+        R.cam.pos[k] = d->cam_pos[k]; R.cam.fwd[k] = d->cam_fwd[k];
+        R.cam.right[k] = d->cam_right[k]; R.cam.up[k] = d->cam_up[k];
+    }
+    R.cam.W = d->width;
+    R.cam.H = d->height;
+    R.root_lo = make_float4(c->root[0], c->root[1], c->root[2], 0.0f);
+    R.root_hi = make_float4(c->root[3], c->root[4], c->root[5], 0.0f);
+    R.mode = d->mode;
+    R.max_depth = d->mode == GF_MODE_SCATTER ? d->max_depth : 1;
+    R.jitter = d->jitter;
+    R.albedo = d->albedo; R.hg_g = d->hg_g; R.sun_E = d->sun_E; R.env_L = d->env_L;
+    R.sun = make_float3(d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]);
+    R.seed = d->seed;
+    R.n_paths = np;
+    R.shard_kind = d->shard_kind;
+    R.shard_rank = d->shard_rank;
+    R.shard_world = std::max(1, d->shard_world);
+    R.tiles_x = (d->width + 31) / 32;
+    R.tiles_y = (d->height + 31) / 32;
+    R.probe = d->probe_pixels;
+    R.spp_count = d->spp_count;
+    R.rays = ray_counts ? (unsigned long long*)ray_counts : c->d_rays;
+    R.accum = accum;
+    R.work = (c->prof & GF_PROFILE_WORK) ? c->d_work : nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int32_t k = 0; k < d->spp_count; ++k) {
+        const int32_t s = d->spp_begin + k;
+        if (d->shard_kind == GF_SHARD_SAMPLES && (s % R.shard_world) != d->shard_rank) continue;
+        GF_CUDA(c, gf_launch_render_pass(R, s, k, st, c->timer), "render pass");
+    }
+    if (c->timer.recs.size() > 4096) harvest(c);  // bound the event pool
+    return GF_OK;
+}
+
+gf_status gf_set_profiling(gf_ctx* c, uint32_t flags) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (flags & ~(GF_PROFILE_TIMING | GF_PROFILE_WORK)) return fail(c, GF_E_INVALID_ARGUMENT, "bad flags");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    c->prof = flags;
+    c->timer.on = (flags & GF_PROFILE_TIMING) != 0;
+    return GF_OK;
+}
+
+gf_status gf_get_stats(gf_ctx* c, gf_stats* out, int32_t reset) {
+    if (!c || !out) return GF_E_INVALID_ARGUMENT;
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    GF_CUDA(c, cudaDeviceSynchronize(), "sync");
+    harvest(c);
+    std::memset(out, 0, sizeof(*out));
+    out->launches = c->timer.launches;
+    for (int s = 0; s < N_STAGES; ++s) {
+        out->stage_launches[s] = c->timer.stage_launches[s];
+        out->stage_ms[s] = c->stage_ms[s];
+    }
+    unsigned long long w[8 * kWorkSlots];
+    GF_CUDA(c, cudaMemcpy(w, c->d_work, sizeof(w), cudaMemcpyDeviceToHost), "memcpy");
+    for (int i = 0; i < 8 * kWorkSlots; ++i) out->work[i / kWorkSlots][i % kWorkSlots] = w[i];
+    if (reset) {
+        c->timer.launches = 0;
+        for (int s = 0; s < N_STAGES; ++s) { c->timer.stage_launches[s] = 0; c->stage_ms[s] = 0.0; }
+        GF_CUDA(c, cudaMemset(c->d_work, 0, sizeof(w)), "memset");
+    }
+    return GF_OK;
+}
+
+int32_t gf_shard_pixel_owner(int32_t px, int32_t py, int32_t width, int32_t height, int32_t world) {
+    if (px < 0 || py < 0 || px >= width || py >= height || world < 1) return -1;
+    const int32_t tx = (width + 31) / 32;
+    const int64_t tile = (int64_t)(py / 32) * tx + (px / 32);
+    return (int32_t)(tile % world);
+}
+
+int32_t gf_shard_sample_owner(int32_t s, int32_t world) {
+    if (s < 0 || world < 1) return -1;
+    return s % world;
+}
+
+}  // extern "C"

@@ -1,0 +1,377 @@
+// gf_build.cu -- a1 primitive ingest and a2 LBVH build.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "gf_device.cuh"
+#include "gf_internal.h"
+
+namespace gfk {
+
+// error bits reported by the load kernel
+enum : uint32_t { ERR_SCALE = 1u, ERR_EXTENT = 2u, ERR_ASSIGN = 4u, ERR_QUAT = 8u, ERR_VALUE = 16u };
+
+// Orientation bin (reading C11): argmax_k |d . o_k|, d = R S^-1 (1,1,1)^T, ties -> lower k,
+// in fp32 with correctly rounded ops in the same expression order as the decision rule of
+// DESIGN.md §3 C11 (an integer decided by floating point: same precision on both sides).
+__device__ int derive_bin(const float* q, const float* sc, int K, const float* axes) {
+    float x = q[0], y = q[1], z = q[2], w = q[3];
+    float nn = __fsqrt_rn(__fmaf_rn(x, x, __fmaf_rn(y, y, __fmaf_rn(z, z, __fmul_rn(w, w)))));
+    x = __fdiv_rn(x, nn); y = __fdiv_rn(y, nn); z = __fdiv_rn(z, nn); w = __fdiv_rn(w, nn);
+    float R[9];
+    R[0] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fmaf_rn(y, y, __fmul_rn(z, z))));
+    R[1] = __fmul_rn(2.0f, __fmaf_rn(x, y, -__fmul_rn(w, z)));
+    R[2] = __fmul_rn(2.0f, __fmaf_rn(x, z, __fmul_rn(w, y)));
+    R[3] = __fmul_rn(2.0f, __fmaf_rn(x, y, __fmul_rn(w, z)));
+    R[4] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fmaf_rn(x, x, __fmul_rn(z, z))));
+    R[5] = __fmul_rn(2.0f, __fmaf_rn(y, z, -__fmul_rn(w, x)));
+    R[6] = __fmul_rn(2.0f, __fmaf_rn(x, z, -__fmul_rn(w, y)));
+    R[7] = __fmul_rn(2.0f, __fmaf_rn(y, z, __fmul_rn(w, x)));
+    R[8] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fmaf_rn(x, x, __fmul_rn(y, y))));
+    float i0 = __fdiv_rn(1.0f, sc[0]), i1 = __fdiv_rn(1.0f, sc[1]), i2 = __fdiv_rn(1.0f, sc[2]);
+    float d[3];
+    for (int r = 0; r < 3; ++r) d[r] = __fmaf_rn(R[3 * r], i0, __fmaf_rn(R[3 * r + 1], i1, __fmul_rn(R[3 * r + 2], i2)));
+    int best = 0;
+    float bestv = -1.0f;
+    for (int k = 0; k < K; ++k) {
+        float a = fabsf(__fmaf_rn(d[0], axes[3 * k], __fmaf_rn(d[1], axes[3 * k + 1], __fmul_rn(d[2], axes[3 * k + 2]))));
+        if (a > bestv) { bestv = a; best = k; }
+    }
+    return best;
+}
+
+__global__ void k_load_prims(LoadArgs A, GPrim* out, uint32_t* err) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const float* q = A.quat + 4 * i;
+    const float* sc = A.scale + 3 * i;
+    uint32_t e = 0;
+    float qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (!(fabsf(qn - 1.0f) <= 1e-5f)) e |= ERR_QUAT;
+    float smin = fminf(sc[0], fminf(sc[1], sc[2])), smax = fmaxf(sc[0], fmaxf(sc[1], sc[2]));
+    if (!(smin > 0.0f) || !isfinite(smax) || !(smax <= 1e6f * smin)) e |= ERR_SCALE;
+    float E = A.extent ? A.extent[i] : 3.0f;
+    if (!(E > 0.0f) || !isfinite(E)) e |= ERR_EXTENT;
+    float alpha = A.alpha[i], om = A.omega[i];
+    float mx = A.mu[3 * i], my = A.mu[3 * i + 1], mz = A.mu[3 * i + 2];
+    if (!(alpha >= 0.0f) || !isfinite(alpha) || !(om >= 0.0f) || !isfinite(om) || !isfinite(mx) || !isfinite(my) ||
+        !isfinite(mz))
+        e |= ERR_VALUE;
+    int lev;
+    if (A.level) {
+        lev = A.level[i];
+        if (lev >= A.P) e |= ERR_ASSIGN;
+    } else if (om == 0.0f) {
+        lev = 0;
+    } else {  // reading C10: f0 = omega |S^-1 (1,1,1)| against ascending cutoffs, last level open
+        float f0 = om * sqrtf(1.0f / (sc[0] * sc[0]) + 1.0f / (sc[1] * sc[1]) + 1.0f / (sc[2] * sc[2]));
+        lev = 1;
+        for (int c = 0; c < A.P - 2; ++c) if (f0 >= A.cutoffs[c]) lev = c + 2;
+        if (lev > A.P - 1) lev = A.P - 1;
+    }
+    int bin;
+    if (A.bin && A.bin[i] != 255) {
+        bin = A.bin[i];
+        if (bin >= A.K) e |= ERR_ASSIGN;
+    } else {
+        bin = (lev == 0) ? 0 : derive_bin(q, sc, A.K, A.axes);
+    }
+    if (e) {
+        atomicOr(err, e);
+        atomicMin(err + 1, (uint32_t)i);
+        return;
+    }
+    lev = min(lev, A.P - 1);
+    bin = min(bin, A.K - 1);
+    int group = lev == 0 ? 0 : 1 + (lev - 1) * A.K + bin;
+    // R from the normalised quaternion, W = S^-1 R^T: row k of W = (column k of R) / s_k
+    float x = q[0] / qn, y = q[1] / qn, z = q[2] / qn, w = q[3] / qn;
+    float R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                  2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                  2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    float is0 = 1.0f / sc[0], is1 = 1.0f / sc[1], is2 = 1.0f / sc[2];
+    double coef = (double)alpha / (2.0 * 3.14159265358979323846 * (double)sc[0] * (double)sc[1] * (double)sc[2]);
+    GPrim P;
+    P.a = make_float4(mx, my, mz, (float)coef);
+    P.b = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, om);
+    P.c = make_float4(R[1] * is1, R[4] * is1, R[7] * is1, E * E);
+    P.d = make_float4(R[2] * is2, R[5] * is2, R[8] * is2, __uint_as_float(((uint32_t)i << 5) | (uint32_t)group));
+    out[i] = P;
+}
+
+// ---------------------------------------------------------------------------------- build
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// conservative world AABB of the ellipsoid {mu + R S u : |u| <= E}: half-width_j = E |row_j(R S)|
+__global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cbounds) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    GPrim P = prims[i];
+    // W = S^-1 R^T  ->  (R S)_{jk} = R_jk s_k ; W_kj = R_jk / s_k  ->  R_jk s_k = W_kj s_k^2
+    // s_k^2 = 1 / |row_k(W)|^2
+    float s0 = 1.0f / (P.b.x * P.b.x + P.b.y * P.b.y + P.b.z * P.b.z);
+    float s1 = 1.0f / (P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
+    float s2 = 1.0f / (P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
+    float E = sqrtf(P.c.w);
+    float hwx = E * sqrtf(P.b.x * P.b.x * s0 * s0 + P.c.x * P.c.x * s1 * s1 + P.d.x * P.d.x * s2 * s2);
+    float hwy = E * sqrtf(P.b.y * P.b.y * s0 * s0 + P.c.y * P.c.y * s1 * s1 + P.d.y * P.d.y * s2 * s2);
+    float hwz = E * sqrtf(P.b.z * P.b.z * s0 * s0 + P.c.z * P.c.z * s1 * s1 + P.d.z * P.d.z * s2 * s2);
+    // outward padding: relative 1e-4 of the half width + absolute term for the slab rounding
+    float padx = 1e-4f * hwx + 4e-6f * (1.0f + fabsf(P.a.x));
+    float pady = 1e-4f * hwy + 4e-6f * (1.0f + fabsf(P.a.y));
+    float padz = 1e-4f * hwz + 4e-6f * (1.0f + fabsf(P.a.z));
+    float* b = box + 6 * i;
+    b[0] = P.a.x - hwx - padx; b[1] = P.a.y - hwy - pady; b[2] = P.a.z - hwz - padz;
+    b[3] = P.a.x + hwx + padx; b[4] = P.a.y + hwy + pady; b[5] = P.a.z + hwz + padz;
+    atomicMin(cbounds + 0, f2ord(P.a.x)); atomicMin(cbounds + 1, f2ord(P.a.y)); atomicMin(cbounds + 2, f2ord(P.a.z));
+    atomicMax(cbounds + 3, f2ord(P.a.x)); atomicMax(cbounds + 4, f2ord(P.a.y)); atomicMax(cbounds + 5, f2ord(P.a.z));
+}
+
+__device__ __forceinline__ uint64_t expand3(uint32_t x) {
+    uint64_t v = x & 0x1fffffu;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+__global__ void k_keys(const GPrim* prims, int64_t n, const uint32_t* cbounds, uint64_t* keys, uint32_t* vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    GPrim P = prims[i];
+    float lo[3] = {ord2f(cbounds[0]), ord2f(cbounds[1]), ord2f(cbounds[2])};
+    float hi[3] = {ord2f(cbounds[3]), ord2f(cbounds[4]), ord2f(cbounds[5])};
+    float c[3] = {P.a.x, P.a.y, P.a.z};
+    uint32_t q[3];
+    for (int k = 0; k < 3; ++k) {
+        float ext = hi[k] - lo[k];
+        float t = ext > 0.0f ? (c[k] - lo[k]) / ext : 0.5f;
+        t = fminf(fmaxf(t, 0.0f), 1.0f);
+        q[k] = min((uint32_t)(t * 524288.0f), 524287u);  // 19 bits
+    }
+    uint32_t group = __float_as_uint(P.d.w) & 31u;
+    keys[i] = ((uint64_t)group << 57) | (expand3(q[0]) << 2) | (expand3(q[1]) << 1) | expand3(q[2]);
+    vals[i] = (uint32_t)i;
+}
+
+__device__ __forceinline__ int delta(const uint64_t* keys, int64_t n, int64_t i, int64_t j) {
+    if (j < 0 || j >= n) return -1;
+    uint64_t a = keys[i], b = keys[j];
+    if (a == b) return 64 + __clz((uint32_t)(i ^ j));
+    return __clzll(a ^ b);
+}
+
+// Karras 2012 radix tree: internal nodes 0..n-2, leaf k stored as n-1+k
+__global__ void k_karras(const uint64_t* keys, int64_t n, int32_t* left, int32_t* right, int32_t* parent,
+                         int32_t* rlo, int32_t* rhi) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
+    int dmin = delta(keys, n, i, i - d);
+    int64_t lmax = 2;
+    while (delta(keys, n, i, i + lmax * d) > dmin) lmax *= 2;
+    int64_t l = 0;
+    for (int64_t t = lmax / 2; t >= 1; t /= 2)
+        if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+    int64_t j = i + l * d;
+    int dnode = delta(keys, n, i, j);
+    int64_t s = 0;
+    int64_t t = l;
+    do {
+        t = (t + 1) / 2;
+        if (delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+    } while (t > 1);
+    int64_t gamma = i + s * d + (d < 0 ? -1 : 0);
+    int64_t lo = i < j ? i : j, hi = i < j ? j : i;
+    int32_t L = (lo == gamma) ? (int32_t)(n - 1 + gamma) : (int32_t)gamma;
+    int32_t Rr = (hi == gamma + 1) ? (int32_t)(n - 1 + gamma + 1) : (int32_t)(gamma + 1);
+    left[i] = L; right[i] = Rr;
+    parent[L] = (int32_t)i; parent[Rr] = (int32_t)i;
+    rlo[i] = (int32_t)lo; rhi[i] = (int32_t)hi;
+}
+
+struct RefitArgs {
+    int64_t n;
+    const int32_t *left, *right, *parent, *perm;
+    const float* pbox;     // per original prim, 6 floats
+    const GPrim* prims;    // original order
+    float* nbox;           // 2n-1 nodes x 6
+    uint32_t *nmask, *ncount, *nsize;
+    uint32_t* flags;
+};
+
+__device__ __forceinline__ bool collapsed(uint32_t count, uint32_t mask) {
+    return count <= (uint32_t)kLeafMax && __popc(mask) == 1;
+}
+
+__global__ void k_refit(RefitArgs A) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= A.n) return;
+    int64_t x = A.n - 1 + k;
+    int32_t pi = A.perm[k];
+    const float* pb = A.pbox + 6 * (int64_t)pi;
+    for (int c = 0; c < 6; ++c) A.nbox[6 * x + c] = pb[c];
+    A.nmask[x] = 1u << (__float_as_uint(A.prims[pi].d.w) & 31u);
+    A.ncount[x] = 1;
+    A.nsize[x] = 1;
+    __threadfence();
+    while (x != 0) {
+        int32_t p = A.parent[x];
+        if (atomicAdd(A.flags + p, 1u) == 0) return;  // first arrival: sibling not done yet
+        __threadfence();
+        int32_t L = A.left[p], R = A.right[p];
+        const volatile float* bl = A.nbox + 6 * (int64_t)L;
+        const volatile float* br = A.nbox + 6 * (int64_t)R;
+        for (int c = 0; c < 3; ++c) {
+            A.nbox[6 * (int64_t)p + c] = fminf(bl[c], br[c]);
+            A.nbox[6 * (int64_t)p + 3 + c] = fmaxf(bl[3 + c], br[3 + c]);
+        }
+        uint32_t m = ((volatile uint32_t*)A.nmask)[L] | ((volatile uint32_t*)A.nmask)[R];
+        uint32_t cnt = ((volatile uint32_t*)A.ncount)[L] + ((volatile uint32_t*)A.ncount)[R];
+        A.nmask[p] = m;
+        A.ncount[p] = cnt;
+        A.nsize[p] = collapsed(cnt, m) ? 1u : 1u + ((volatile uint32_t*)A.nsize)[L] + ((volatile uint32_t*)A.nsize)[R];
+        __threadfence();
+        x = p;
+    }
+}
+
+struct LayoutArgs {
+    int64_t n;
+    const int32_t *left, *right, *parent, *rlo;
+    const float* nbox;
+    const uint32_t *nmask, *ncount, *nsize;
+    GNode* out;
+    uint32_t total;
+};
+
+__global__ void k_layout(LayoutArgs A) {
+    int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nn = 2 * A.n - 1;
+    if (x >= nn) return;
+    int64_t root = 0;
+    if (x != root) {
+        int32_t p = A.parent[x];
+        if (collapsed(A.ncount[p], A.nmask[p])) return;  // inside a collapsed leaf
+    }
+    // pre-order index: walk to the root
+    uint32_t idx = 0;
+    int64_t cur = x;
+    while (cur != root) {
+        int32_t p = A.parent[cur];
+        idx += 1;
+        if (A.right[p] == cur) idx += A.nsize[A.left[p]];
+        cur = p;
+    }
+    uint32_t cnt = A.ncount[x], m = A.nmask[x];
+    bool leaf = collapsed(cnt, m);
+    uint32_t skip = idx + A.nsize[x];
+    uint32_t info;
+    if (leaf) {
+        uint32_t first = (x >= A.n - 1) ? (uint32_t)(x - (A.n - 1)) : (uint32_t)A.rlo[x];
+        info = (first << 8) | (cnt << 5) | (uint32_t)(__ffs(m) - 1);
+    } else {
+        info = m;
+    }
+    const float* b = A.nbox + 6 * x;
+    GNode N;
+    N.lo = make_float4(b[0], b[1], b[2], __uint_as_float(skip | (leaf ? kLeafBit : 0u)));
+    N.hi = make_float4(b[3], b[4], b[5], __uint_as_float(info));
+    A.out[idx] = N;
+}
+
+__global__ void k_gather(const GPrim* in, const int32_t* perm, int64_t n, GPrim* out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    out[k] = in[perm[k]];
+}
+
+}  // namespace gfk
+
+// ------------------------------------------------------------------------------ host side
+using namespace gfk;
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint32_t* err, cudaStream_t st) {
+    if (A.n == 0) return cudaSuccess;
+    k_load_prims<<<nblk(A.n, 256), 256, 0, st>>>(A, (GPrim*)out, err);
+    return cudaGetLastError();
+}
+
+size_t gf_sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    if (n <= 0) return 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64);
+    return bytes;
+}
+
+BuildScratch gf_scratch_layout(int64_t n, char* base) {
+    BuildScratch s;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += (bytes + 255) & ~(size_t)255; return p; };
+    int64_t nn = n > 0 ? 2 * n - 1 : 1;
+    s.pbox = (float*)take(sizeof(float) * 6 * (n > 0 ? n : 1));
+    s.cbounds = (uint32_t*)take(sizeof(uint32_t) * 8);
+    s.keys_in = (uint64_t*)take(sizeof(uint64_t) * (n > 0 ? n : 1));
+    s.keys_out = (uint64_t*)take(sizeof(uint64_t) * (n > 0 ? n : 1));
+    s.vals_in = (uint32_t*)take(sizeof(uint32_t) * (n > 0 ? n : 1));
+    s.vals_out = (uint32_t*)take(sizeof(uint32_t) * (n > 0 ? n : 1));
+    s.left = (int32_t*)take(sizeof(int32_t) * (n > 0 ? n : 1));
+    s.right = (int32_t*)take(sizeof(int32_t) * (n > 0 ? n : 1));
+    s.parent = (int32_t*)take(sizeof(int32_t) * nn);
+    s.rlo = (int32_t*)take(sizeof(int32_t) * (n > 0 ? n : 1));
+    s.rhi = (int32_t*)take(sizeof(int32_t) * (n > 0 ? n : 1));
+    s.nbox = (float*)take(sizeof(float) * 6 * nn);
+    s.nmask = (uint32_t*)take(sizeof(uint32_t) * nn);
+    s.ncount = (uint32_t*)take(sizeof(uint32_t) * nn);
+    s.nsize = (uint32_t*)take(sizeof(uint32_t) * nn);
+    s.flags = (uint32_t*)take(sizeof(uint32_t) * (n > 0 ? n : 1));
+    s.sort_temp_bytes = gf_sort_temp_bytes(n);
+    s.sort_temp = take(s.sort_temp_bytes + 256);
+    s.total_bytes = off;
+    return s;
+}
+
+// builds into nodes/sorted; returns node count via *n_nodes (host, after sync)
+cudaError_t gf_launch_build(const void* prims_v, int64_t n, const BuildScratch& S, void* nodes_v, void* sorted_v,
+                            uint32_t* n_nodes, float* root_box, cudaStream_t st) {
+    const GPrim* prims = (const GPrim*)prims_v;
+    GNode* nodes = (GNode*)nodes_v;
+    cudaError_t e;
+    *n_nodes = 0;
+    if (n == 0) return cudaSuccess;
+    uint32_t init[8] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u, 0u};
+    if ((e = cudaMemcpyAsync(S.cbounds, init, sizeof(init), cudaMemcpyHostToDevice, st))) return e;
+    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.cbounds, S.keys_in, S.vals_in);
+    size_t tb = S.sort_temp_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
+                                             0, 64, st)))
+        return e;
+    if (n > 1) {
+        k_karras<<<nblk(n - 1, 256), 256, 0, st>>>(S.keys_out, n, S.left, S.right, S.parent, S.rlo, S.rhi);
+        if ((e = cudaMemsetAsync(S.flags, 0, sizeof(uint32_t) * n, st))) return e;
+    }
+    RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, prims, S.nbox, S.nmask, S.ncount,
+                S.nsize, S.flags};
+    k_refit<<<nblk(n, 256), 256, 0, st>>>(R);
+    // root (node 0 = internal root, or leaf 0 when n == 1 stored at n-1+0 = 0)
+    uint32_t total = 0;
+    if ((e = cudaMemcpyAsync(&total, S.nsize, sizeof(uint32_t), cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaStreamSynchronize(st))) return e;
+    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, total};
+    k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
+    k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v);
+    if ((e = cudaMemcpyAsync(root_box, S.nbox, sizeof(float) * 6, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaStreamSynchronize(st))) return e;
+    *n_nodes = total;
+    return cudaGetLastError();
+}

@@ -1,0 +1,451 @@
+// gf_device.cuh -- device-side building blocks of the Gabor Fields hot path (sm_100a).
+//
+// Data layout in HBM:
+//   GPrim  64 B  = 4 x float4 : (mu.xyz, c) (W row0, omega) (W row1, E^2) (W row2, idx<<5|group)
+//          with W = S^-1 R^T (PCA whitening, reading C1), c = alpha / (2 pi s1 s2 s3),
+//          k_W = (omega, omega, omega) implicit (reading C2).
+//   GNode  32 B  = 2 x float4 : (lo.xyz, skip | leaf<<31) (hi.xyz, info)
+//          depth-first layout, hit -> i+1, miss -> skip; info = group mask (internal) or
+//          first<<8 | count<<5 | group (leaf).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gfk {
+
+constexpr int kMaxGroups = 32;
+constexpr int kMaxLevels = 8;
+constexpr int kLeafMax = 4;
+constexpr uint32_t kLeafBit = 0x80000000u;
+
+struct __align__(16) GPrim {
+    float4 a, b, c, d;
+};
+struct __align__(16) GNode {
+    float4 lo, hi;
+};
+
+// ------------------------------------------------------------------ policy (Tables B1/B2)
+struct PolicyDev {
+    uint32_t static_mask;
+    int32_t ls, os;
+    float delta;
+    double th[kMaxLevels + 1];    // (j/P)^(1-beta), j = 0..P      (B1 power law buckets)
+    double psi[kMaxLevels + 1];   // (k/(P-1))^(1-beta), k = 0..P-1 (B1 PL + CV buckets, C13)
+    float w_pl[kMaxLevels];       // 1/(th[j+1]-th[j])
+    float w_plcv[kMaxLevels];     // 1/(psi[k+1]-psi[k])
+    float w_acc[kMaxLevels];      // 1/(1-th[j])                   (C14)
+};
+
+struct SceneDev {
+    int32_t P, K, G;
+    float axes[3 * 16];
+    float f0[kMaxGroups];
+};
+
+// ------------------------------------------------------------------ Philox4x32-10
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+enum { ST_EXT = 0, ST_NEE = 1, ST_SCAT = 2, ST_CAM = 3 };
+// 4 uniforms k0..k0+3 of a stream (k0 multiple of 4) -- one Philox call
+__device__ __forceinline__ uint4 stream_block(uint64_t seed, uint32_t pix, uint32_t smp, uint32_t d, uint32_t st,
+                                              uint32_t k0) {
+    return philox4x32_10(make_uint4(pix, smp, d, (st << 16) | (k0 >> 2)),
+                         make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+__device__ __forceinline__ float u01(uint32_t x) { return (float)(x >> 8) * (1.0f / 16777216.0f); }
+__device__ __forceinline__ uint32_t word(const uint4& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+// uniform k of a stream (k < 16)
+__device__ __forceinline__ float stream_u(uint64_t seed, uint32_t pix, uint32_t smp, uint32_t d, uint32_t st,
+                                          uint32_t k) {
+    uint4 b = stream_block(seed, pix, smp, d, st, k & ~3u);
+    return u01(word(b, k & 3));
+}
+
+// Evaluate a LOD policy for one ray segment (same decisions as the oracle: integer draws,
+// fp64 threshold compares, fp32 orientation arithmetic with explicitly rounded ops).
+// ul: level uniform; uo[l-1]: orientation uniform of Gabor level l. Writes weights for
+// selected groups into w[] (others untouched) and returns the mask.
+__device__ inline uint32_t policy_eval(const PolicyDev& pol, const SceneDev& sc, float3 dir, float ul,
+                                       const float* uo, float* w) {
+    const int P = sc.P, K = sc.K;
+    float lw[kMaxLevels];
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) lw[l] = 0.0f;
+    const uint32_t m24 = (uint32_t)(ul * 16777216.0f);
+    const double ud = (double)ul;
+    switch (pol.ls) {
+    case 1: { int j = (int)(((uint64_t)m24 * (uint64_t)P) >> 24); lw[j] = (float)P; break; }
+    case 2: {
+        int j = 0;
+        for (int k = 1; k < P; ++k) if (ud >= pol.th[k]) j = k;
+        lw[j] = pol.w_pl[j];
+        break;
+    }
+    case 3: {
+        lw[0] = 1.0f;
+        if (P > 1) { int j = 1 + (int)(((uint64_t)m24 * (uint64_t)(P - 1)) >> 24); lw[j] = (float)(P - 1); }
+        break;
+    }
+    case 4: {
+        lw[0] = 1.0f;
+        if (P > 1) {
+            int k = 0;
+            for (int q = 1; q < P - 1; ++q) if (ud >= pol.psi[q]) k = q;
+            lw[1 + k] = pol.w_plcv[k];
+        }
+        break;
+    }
+    case 5: {
+        int kk = 0;
+        for (int q = 1; q < P; ++q) if (ud >= pol.th[q]) kk = q;
+        for (int j = 0; j <= kk; ++j) lw[j] = pol.w_acc[j];
+        break;
+    }
+    default:
+        for (int l = 0; l < P; ++l) lw[l] = 1.0f;
+    }
+    uint32_t mask = 0;
+    if (lw[0] != 0.0f) { mask |= 1u; w[0] = lw[0]; }
+    for (int l = 1; l < P; ++l) {
+        if (lw[l] == 0.0f) continue;
+        float a[16], bw[16];
+        for (int b = 0; b < K; ++b) {
+            bw[b] = 0.0f;
+            a[b] = fabsf(__fmaf_rn(dir.x, sc.axes[3 * b], __fmaf_rn(dir.y, sc.axes[3 * b + 1],
+                                                                   __fmul_rn(dir.z, sc.axes[3 * b + 2]))));
+        }
+        const float u = uo[l - 1];
+        const uint32_t mu24 = (uint32_t)(u * 16777216.0f);
+        switch (pol.os) {
+        case 1:
+            for (int b = 0; b < K; ++b) if (a[b] <= pol.delta) bw[b] = 1.0f;
+            break;
+        case 2: { int b = (int)(((uint64_t)mu24 * (uint64_t)K) >> 24); bw[b] = (float)K; break; }
+        case 3: {
+            float wi[16], W = 0.0f;
+            for (int b = 0; b < K; ++b) {
+                float x = __fmul_rn(sc.f0[1 + (l - 1) * K + b], a[b]);
+                wi[b] = expf(__fmul_rn(-0.5f, __fmul_rn(x, x)));
+                W = __fadd_rn(W, wi[b]);
+            }
+            if (!(W > 0.0f) || !isfinite(W)) {
+                int b = (int)(((uint64_t)mu24 * (uint64_t)K) >> 24);
+                bw[b] = (float)K;
+            } else {
+                float t = __fmul_rn(u, W), c = 0.0f;
+                int pick = K - 1;
+                for (int b = 0; b < K; ++b) { c = __fadd_rn(c, wi[b]); if (t < c) { pick = b; break; } }
+                bw[pick] = __fdiv_rn(W, wi[pick]);
+            }
+            break;
+        }
+        case 4: {
+            int nab = 0;
+            for (int b = 0; b < K; ++b) { if (a[b] <= pol.delta) bw[b] = 1.0f; else ++nab; }
+            if (nab > 0) {
+                int pickn = (int)(((uint64_t)mu24 * (uint64_t)nab) >> 24), c = 0;
+                for (int b = 0; b < K; ++b)
+                    if (!(a[b] <= pol.delta)) { if (c == pickn) { bw[b] = (float)nab; break; } ++c; }
+            }
+            break;
+        }
+        default:
+            for (int b = 0; b < K; ++b) bw[b] = 1.0f;
+        }
+        for (int b = 0; b < K; ++b) {
+            if (bw[b] == 0.0f) continue;
+            int g = 1 + (l - 1) * K + b;
+            mask |= 1u << g;
+            w[g] = lw[l] * bw[b];
+        }
+    }
+    return mask & pol.static_mask;
+}
+
+// policy for segment (pix, smp, d) of stream st; level uniform at k_level, orientation at k_level+l
+__device__ inline uint32_t policy_for(const PolicyDev& pol, const SceneDev& sc, float3 dir, uint64_t seed,
+                                      uint32_t pix, uint32_t smp, uint32_t d, uint32_t st, uint32_t k_level,
+                                      float* w) {
+    if (pol.ls == 0 && pol.os == 0) return pol.static_mask;  // static: weights stay 1
+    float u[12];
+    uint4 b0 = stream_block(seed, pix, smp, d, st, 0);
+    uint4 b1 = stream_block(seed, pix, smp, d, st, 4);
+    uint4 b2 = stream_block(seed, pix, smp, d, st, 8);
+    u[0] = u01(b0.x); u[1] = u01(b0.y); u[2] = u01(b0.z); u[3] = u01(b0.w);
+    u[4] = u01(b1.x); u[5] = u01(b1.y); u[6] = u01(b1.z); u[7] = u01(b1.w);
+    u[8] = u01(b2.x); u[9] = u01(b2.y); u[10] = u01(b2.z); u[11] = u01(b2.w);
+    return policy_eval(pol, sc, dir, u[k_level], u + k_level + 1, w);
+}
+
+// ------------------------------------------------------------------ camera (fp32, correctly rounded ops)
+struct CamDev {
+    float pos[3], fwd[3], right[3], up[3];
+    int32_t W, H;
+};
+__device__ __forceinline__ void camera_ray(const CamDev& c, int px, int py, float jx, float jy, float3& o,
+                                           float3& v) {
+    float fx = __fadd_rn((float)px, jx), fy = __fadd_rn((float)py, jy);
+    float iw2 = __fdiv_rn(2.0f, (float)c.W), ih2 = __fdiv_rn(2.0f, (float)c.H);
+    float sx = __fmaf_rn(fx, iw2, -1.0f), sy = __fmaf_rn(-fy, ih2, 1.0f);
+    float r0 = __fmaf_rn(sy, c.up[0], __fmaf_rn(sx, c.right[0], c.fwd[0]));
+    float r1 = __fmaf_rn(sy, c.up[1], __fmaf_rn(sx, c.right[1], c.fwd[1]));
+    float r2 = __fmaf_rn(sy, c.up[2], __fmaf_rn(sx, c.right[2], c.fwd[2]));
+    float len = __fsqrt_rn(__fmaf_rn(r0, r0, __fmaf_rn(r1, r1, __fmul_rn(r2, r2))));
+    v = make_float3(__fdiv_rn(r0, len), __fdiv_rn(r1, len), __fdiv_rn(r2, len));
+    o = make_float3(c.pos[0], c.pos[1], c.pos[2]);
+}
+
+// ------------------------------------------------------------------ Henyey-Greenstein (C19)
+__device__ __forceinline__ float hg_eval(float g, float cost) {
+    float den = 1.0f + g * g - 2.0f * g * cost;
+    return (1.0f - g * g) / (4.0f * 3.14159265358979f * den * sqrtf(den));
+}
+__device__ inline float3 hg_sample(float g, float3 v, float u1, float u2) {
+    float cost;
+    if (fabsf(g) < 1e-3f) cost = 1.0f - 2.0f * u1;
+    else { float q = (1.0f - g * g) / (1.0f - g + 2.0f * g * u1); cost = (1.0f + g * g - q * q) / (2.0f * g); }
+    cost = fminf(1.0f, fmaxf(-1.0f, cost));
+    float sint = sqrtf(fmaxf(0.0f, 1.0f - cost * cost));
+    float sp, cp;
+    sincospif(2.0f * u2, &sp, &cp);
+    float sgn = v.z >= 0.0f ? 1.0f : -1.0f;
+    float a = -1.0f / (sgn + v.z), b = v.x * v.y * a;
+    float3 t1 = make_float3(1.0f + sgn * v.x * v.x * a, sgn * b, -sgn * v.x);
+    float3 t2 = make_float3(b, sgn + v.y * v.y * a, -v.y);
+    float3 o = make_float3(sint * cp * t1.x + sint * sp * t2.x + cost * v.x,
+                           sint * cp * t1.y + sint * sp * t2.y + cost * v.y,
+                           sint * cp * t1.z + sint * sp * t2.z + cost * v.z);
+    float n = rsqrtf(o.x * o.x + o.y * o.y + o.z * o.z);
+    return make_float3(o.x * n, o.y * n, o.z * n);
+}
+
+// ------------------------------------------------------------------ ray / box
+struct RayDev {
+    float3 o, d, inv, oinv;
+    float tmin, tmax;
+};
+__device__ __forceinline__ float safe_inv(float x) {
+    return 1.0f / (fabsf(x) > 1e-20f ? x : copysignf(1e-20f, x));
+}
+__device__ __forceinline__ RayDev make_ray(float3 o, float3 d, float tmin, float tmax) {
+    RayDev r;
+    r.o = o; r.d = d; r.tmin = tmin; r.tmax = tmax;
+    r.inv = make_float3(safe_inv(d.x), safe_inv(d.y), safe_inv(d.z));
+    r.oinv = make_float3(o.x * r.inv.x, o.y * r.inv.y, o.z * r.inv.z);
+    return r;
+}
+// slab test against [t0,t1]; boxes are padded at build time to absorb the rounding here
+__device__ __forceinline__ bool slab(const RayDev& r, float4 lo, float4 hi, float t0, float t1) {
+    float ax = fmaf(lo.x, r.inv.x, -r.oinv.x), bx = fmaf(hi.x, r.inv.x, -r.oinv.x);
+    float ay = fmaf(lo.y, r.inv.y, -r.oinv.y), by = fmaf(hi.y, r.inv.y, -r.oinv.y);
+    float az = fmaf(lo.z, r.inv.z, -r.oinv.z), bz = fmaf(hi.z, r.inv.z, -r.oinv.z);
+    float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), t0));
+    float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), t1));
+    return tn <= tf;
+}
+__device__ __forceinline__ bool slab_range(const RayDev& r, float4 lo, float4 hi, float t0, float t1, float& tn,
+                                           float& tf) {
+    float ax = fmaf(lo.x, r.inv.x, -r.oinv.x), bx = fmaf(hi.x, r.inv.x, -r.oinv.x);
+    float ay = fmaf(lo.y, r.inv.y, -r.oinv.y), by = fmaf(hi.y, r.inv.y, -r.oinv.y);
+    float az = fmaf(lo.z, r.inv.z, -r.oinv.z), bz = fmaf(hi.z, r.inv.z, -r.oinv.z);
+    tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), t0));
+    tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), t1));
+    return tn <= tf;
+}
+
+// ------------------------------------------------------------------ a5: whitened setup + predicate
+// Per (ray, primitive): world offset re-centred at the ray's closest approach to mu with an
+// error-free TwoSum (o - mu = hi + lo), so that far origins (|o-mu|/s up to 3000) keep fp32
+// precision in the whitened closest point p_c (SURVEY §0 finding 7).
+struct Setup {
+    float r2;    // |p_c|^2, squared whitened perpendicular distance (c - b^2)
+    float h;     // whitened half chord sqrt(E^2 - r2)
+    float bp;    // whitened arc parameter of the re-centred point: u(t) = bp + j (t - tc)
+    float j;     // |W v|  (P:L223 Jacobian)
+    float ij;    // 1/|W v|
+    float tc;    // re-centring parameter (world t)
+    float Om;    // Omega = k_W . v_W = omega (vWx+vWy+vWz)    (C2)
+    float phi0;  // phase at the closest point = k_W . p_c = d - Omega b
+    float u0, u1;  // whitened chord clipped to [tmin, tmax]
+};
+
+__device__ __forceinline__ bool prim_setup(const GPrim& P, const RayDev& r, float tmin, float tmax, Setup& s) {
+    // TwoSum(o, -mu): hi + lo == o - mu exactly
+    float hx = __fsub_rn(r.o.x, P.a.x), hy = __fsub_rn(r.o.y, P.a.y), hz = __fsub_rn(r.o.z, P.a.z);
+    float bx = __fsub_rn(hx, r.o.x), by = __fsub_rn(hy, r.o.y), bz = __fsub_rn(hz, r.o.z);
+    float lx = __fadd_rn(__fsub_rn(r.o.x, __fsub_rn(hx, bx)), __fsub_rn(-P.a.x, bx));
+    float ly = __fadd_rn(__fsub_rn(r.o.y, __fsub_rn(hy, by)), __fsub_rn(-P.a.y, by));
+    float lz = __fadd_rn(__fsub_rn(r.o.z, __fsub_rn(hz, bz)), __fsub_rn(-P.a.z, bz));
+    float tc = -fmaf(hx, r.d.x, fmaf(hy, r.d.y, hz * r.d.z));
+    float Dx = __fadd_rn(__fmaf_rn(tc, r.d.x, hx), lx);
+    float Dy = __fadd_rn(__fmaf_rn(tc, r.d.y, hy), ly);
+    float Dz = __fadd_rn(__fmaf_rn(tc, r.d.z, hz), lz);
+    // whitened offset and direction (W rows in b,c,d .xyz)
+    float px = fmaf(P.b.x, Dx, fmaf(P.b.y, Dy, P.b.z * Dz));
+    float py = fmaf(P.c.x, Dx, fmaf(P.c.y, Dy, P.c.z * Dz));
+    float pz = fmaf(P.d.x, Dx, fmaf(P.d.y, Dy, P.d.z * Dz));
+    float wx = fmaf(P.b.x, r.d.x, fmaf(P.b.y, r.d.y, P.b.z * r.d.z));
+    float wy = fmaf(P.c.x, r.d.x, fmaf(P.c.y, r.d.y, P.c.z * r.d.z));
+    float wz = fmaf(P.d.x, r.d.x, fmaf(P.d.y, r.d.y, P.d.z * r.d.z));
+    float jj = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
+    float ij = rsqrtf(jj);
+    float vx = wx * ij, vy = wy * ij, vz = wz * ij;
+    float bp = fmaf(px, vx, fmaf(py, vy, pz * vz));
+    float cx = fmaf(-bp, vx, px), cy = fmaf(-bp, vy, py), cz = fmaf(-bp, vz, pz);
+    float r2 = fmaf(cx, cx, fmaf(cy, cy, cz * cz));
+    const float E2 = P.c.w;
+    if (!(r2 < E2)) return false;
+    float h = sqrtf(E2 - r2);
+    float j = jj * ij;
+    float ut0 = fmaf(j, tmin - tc, bp);
+    float ut1 = (tmax == INFINITY) ? INFINITY : fmaf(j, tmax - tc, bp);
+    float u0 = fmaxf(-h, ut0), u1 = fminf(h, ut1);
+    if (!(u1 > u0)) return false;
+    const float om = P.b.w;
+    s.r2 = r2; s.h = h; s.bp = bp; s.j = j; s.ij = ij; s.tc = tc;
+    s.Om = om * (vx + vy + vz);
+    s.phi0 = om * (cx + cy + cz);
+    s.u0 = u0; s.u1 = u1;
+    return true;
+}
+
+// ------------------------------------------------------------------ a6: complex erf, Eq. 13 series
+// erf(z) = 2/sqrt(pi) z sum_n a_n (z^2)^n, a_n = (-1)^n / (n! (2n+1)), evaluated by Horner in
+// fp32 with N = 30 terms (reading C5: the paper's 16 terms miss the 1e-4 target near the
+// ellipsoid bound; 28-32 terms reach 2.3e-7 absolute over |u| <= 3, Omega <= 2.6).
+__constant__ float kErfA[32] = {
+    1.000000000e+00f, -3.333333333e-01f, 1.000000000e-01f, -2.380952381e-02f, 4.629629630e-03f,
+    -7.575757576e-04f, 1.068376068e-04f, -1.322751323e-05f, 1.458916900e-06f, -1.450385222e-07f,
+    1.312253296e-08f, -1.089222104e-09f, 8.350702795e-11f, -5.947794014e-12f, 3.955429516e-13f,
+    -2.466827010e-14f, 1.448326464e-15f, -8.032735012e-17f, 4.221407289e-18f, -2.107855191e-19f,
+    1.002516493e-20f, -4.551846759e-22f, 1.977064754e-23f, -8.230149299e-25f, 3.289260349e-26f,
+    -1.264107899e-27f, 4.678483516e-29f, -1.669761793e-30f, 5.754191644e-32f, -1.916942862e-33f,
+    6.180307588e-35f, -1.930357209e-36f};
+constexpr int kErfTerms = 30;
+constexpr float kRsqrt2 = 0.70710678118654752f;
+constexpr float kTwoOverSqrtPi = 1.12837916709551257f;
+constexpr float kInvSqrt2Pi = 0.39894228040143268f;
+constexpr float kWMaxSeries = 9.0f;  // |z^2| beyond this -> Gauss-Legendre fallback
+
+// F(u) = erf((u - i Omega)/sqrt2).  Omega == 0 (every Gaussian, omega = 0, and Gabors integrated
+// exactly along their modulation plane) reduces to the real erf: erff, 2 ulp.
+__device__ __forceinline__ float2 erf_shift(float u, float Om) {
+    if (Om == 0.0f) return make_float2(erff(u * kRsqrt2), 0.0f);
+    float zr = u * kRsqrt2, zi = -Om * kRsqrt2;
+    float wr = fmaf(zr, zr, -zi * zi), wi = 2.0f * zr * zi;
+    float sr = kErfA[kErfTerms - 1], si = 0.0f;
+#pragma unroll
+    for (int n = kErfTerms - 2; n >= 0; --n) {
+        float tr = fmaf(sr, wr, fmaf(-si, wi, kErfA[n]));
+        float ti = fmaf(sr, wi, si * wr);
+        sr = tr; si = ti;
+    }
+    return make_float2(kTwoOverSqrtPi * fmaf(zr, sr, -zi * si), kTwoOverSqrtPi * fmaf(zr, si, zi * sr));
+}
+
+__constant__ float kGLx[12] = {6.40568928626056300e-02f, 1.91118867473616311e-01f, 3.15042679696163397e-01f,
+                               4.33793507626045127e-01f, 5.45421471388839563e-01f, 6.48093651936975546e-01f,
+                               7.40124191578554358e-01f, 8.20001985973902947e-01f, 8.86415527004401071e-01f,
+                               9.38274552002732798e-01f, 9.74728555971309474e-01f, 9.95187219997021311e-01f};
+__constant__ float kGLw[12] = {1.27938195346752021e-01f, 1.25837456346828247e-01f, 1.21670472927803294e-01f,
+                               1.15505668053725516e-01f, 1.07444270115965565e-01f, 9.76186521041139260e-02f,
+                               8.61901615319532050e-02f, 7.33464814110801611e-02f, 5.92985849154363601e-02f,
+                               4.42774388174194122e-02f, 2.85313886289335593e-02f, 1.23412297999886903e-02f};
+
+// reduce phase to [-pi, pi] then fast sincos (|x| <= 8 in practice)
+__device__ __forceinline__ void sincos_red(float x, float* s, float* c) {
+    float k = rintf(x * 0.15915494309189535f);
+    float r = fmaf(-k, 6.28318548202514648f, x);
+    r = fmaf(-k, -1.7484555e-7f, r);
+    __sincosf(r, s, c);
+}
+
+// work counters (gf_stats.work, per stage), flushed with warp-aggregated atomics
+constexpr int kWorkSlots = 12;
+enum { W_NODES = 0, W_TESTS = 1, W_HITS = 2, W_ERFC = 3, W_ERFR = 4, W_GL = 5, W_OVERFLOW = 6, W_ROOT = 7,
+       W_PATHS = 8 };
+struct Work {
+    uint32_t nodes = 0, tests = 0, hits = 0, erfc = 0, erfr = 0, gl = 0, overflow = 0, root = 0, paths = 0;
+    __device__ __forceinline__ void erf(float Om, uint32_t k) {
+        if (Om == 0.0f) erfr += k; else erfc += k;
+    }
+};
+__device__ __forceinline__ void flush_work(unsigned long long* w, const Work& k) {
+    const unsigned long long v[9] = {k.nodes, k.tests, k.hits, k.erfc, k.erfr, k.gl, k.overflow, k.root, k.paths};
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        unsigned long long x = v[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicAdd(w + i, x);
+    }
+}
+// per-thread variant (partial warps allowed)
+__device__ __forceinline__ void flush_work_thread(unsigned long long* w, const Work& k) {
+    const unsigned long long v[9] = {k.nodes, k.tests, k.hits, k.erfc, k.erfr, k.gl, k.overflow, k.root, k.paths};
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+        if (v[i]) atomicAdd(w + i, v[i]);
+}
+
+// Segment integral of primitive with setup s over whitened [ua, ub] (alpha, W-Jacobian and
+// group weight NOT applied):  Jw = 1/2 e^{-(r2+Om^2)/2} Re{e^{i phi0}[F(ub) - F(ua)]}
+//   = e^{-r2/2} (2 pi)^-1/2 int_ua^ub e^{-u^2/2} cos(phi0 + Om u) du      (App. A, reading C3).
+// The caller multiplies by c / j (P:L223 K).  Symmetric full chords use one endpoint:
+// F(h) - F(-h) = 2 Re F(h) (the "symmetries in the pair of erf terms").
+__device__ inline float seg_J(const Setup& s, float ua, float ub, Work& wk) {
+    const float L = ub - ua;
+    float sp, cp;
+    if (L < 1e-4f) {  // midpoint rule: whitened segment below 1e-4
+        float um = 0.5f * (ua + ub);
+        sincos_red(fmaf(s.Om, um, s.phi0), &sp, &cp);
+        return kInvSqrt2Pi * __expf(-0.5f * (s.r2 + um * um)) * cp * L;
+    }
+    sincos_red(s.phi0, &sp, &cp);
+    const float wmax = 0.5f * (fmaxf(ua * ua, ub * ub) + s.Om * s.Om);
+    if (wmax > kWMaxSeries && s.Om != 0.0f) {  // outside the series domain: 24-node Gauss-Legendre
+        ++wk.gl;
+        float hm = 0.5f * L, c = 0.5f * (ua + ub), acc = 0.0f;
+#pragma unroll 4
+        for (int k = 0; k < 12; ++k) {
+            float x = hm * kGLx[k];
+            float s1, c1, s2, c2;
+            sincos_red(fmaf(s.Om, c + x, s.phi0), &s1, &c1);
+            sincos_red(fmaf(s.Om, c - x, s.phi0), &s2, &c2);
+            acc = fmaf(kGLw[k], __expf(-0.5f * (c + x) * (c + x)) * c1 + __expf(-0.5f * (c - x) * (c - x)) * c2, acc);
+        }
+        return kInvSqrt2Pi * __expf(-0.5f * s.r2) * hm * acc;
+    }
+    const float amp = 0.5f * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+    if (ua == -s.h && ub == s.h) {
+        wk.erf(s.Om, 1);
+        float2 F = erf_shift(ub, s.Om);
+        return 2.0f * amp * cp * F.x;
+    }
+    wk.erf(s.Om, 2);
+    float2 Fb = erf_shift(ub, s.Om), Fa = erf_shift(ua, s.Om);
+    return amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y));
+}
+
+// contribution of a hit over its clipped chord: c/j * Jw
+__device__ __forceinline__ float hit_tau(const GPrim& P, const Setup& s, Work& wk) {
+    return P.a.w * s.ij * seg_J(s, s.u0, s.u1, wk);
+}
+
+__device__ __forceinline__ uint32_t node_mask(uint32_t skipw, uint32_t info) {
+    return (skipw & kLeafBit) ? (1u << (info & 31u)) : info;
+}
+
+}  // namespace gfk

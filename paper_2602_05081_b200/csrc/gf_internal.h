@@ -1,0 +1,108 @@
+// gf_internal.h -- host-side declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "gf_device.cuh"
+
+struct LoadArgs {
+    int64_t n;
+    const float *mu, *quat, *scale, *alpha, *omega, *extent;
+    const uint8_t *level, *bin;
+    int32_t P, K;
+    float cutoffs[8];
+    float axes[48];
+};
+
+struct BuildScratch {
+    float* pbox;
+    uint32_t* cbounds;
+    uint64_t *keys_in, *keys_out;
+    uint32_t *vals_in, *vals_out;
+    int32_t *left, *right, *parent, *rlo, *rhi;
+    float* nbox;
+    uint32_t *nmask, *ncount, *nsize, *flags;
+    void* sort_temp;
+    size_t sort_temp_bytes;
+    size_t total_bytes;
+};
+
+struct TraceArgs {
+    const gfk::GNode* nodes;
+    uint32_t n_nodes;
+    const gfk::GPrim* prims;  // BVH order (sorted) or input order (brute force)
+    int64_t n_prims;
+    gfk::PolicyDev pol;
+    gfk::SceneDev sc;
+    uint64_t seed;
+    const float* rays;
+    int64_t n;
+    float* tau;
+    float* T;
+    uint32_t* counters;
+    int32_t* cand_ids;
+    int32_t cand_cap;
+    int32_t* cand_count;
+    unsigned long long* work;  // gf_stats work counters or null
+};
+
+// Stage timing with CUDA events recorded on the launching stream (gf_set_profiling).
+enum { STAGE_GEN = 0, STAGE_FFA = 1, STAGE_FFB = 2, STAGE_NEE = 3, STAGE_FINISH = 4, STAGE_TOMO = 5,
+       STAGE_TRACE = 6, STAGE_BUILD = 7, N_STAGES = 8 };
+struct StageTimer {
+    bool on = false;  // record events around every launch
+    unsigned long long launches = 0;
+    unsigned long long stage_launches[N_STAGES] = {};
+    struct Rec { int stage; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+    cudaEvent_t ev();
+    void pre(int stage, cudaStream_t st, cudaEvent_t& a);   // before a kernel launch
+    void post(int stage, cudaStream_t st, cudaEvent_t a);   // after it
+};
+
+// render launch state (see gf_render.cu)
+struct RenderDev {
+    const gfk::GNode* nodes;
+    uint32_t n_nodes;
+    const gfk::GPrim* prims;
+    gfk::PolicyDev ext, nee;
+    gfk::SceneDev sc;
+    gfk::CamDev cam;
+    float4 root_lo, root_hi;
+    int32_t mode, max_depth, jitter;
+    float albedo, hg_g, sun_E, env_L;
+    float3 sun;
+    uint64_t seed;
+    // work decomposition
+    int64_t n_paths;           // paths per sample pass
+    int32_t shard_kind, shard_rank, shard_world;
+    int32_t tiles_x, tiles_y;  // 32x32 tiles
+    const int32_t* probe;      // probe pixels or null
+    int32_t spp_count;
+    // per-path state (SoA, n_paths each)
+    float *ox, *oy, *oz, *dx, *dy, *dz, *beta, *L;
+    double* cum;  // 3 n: tau before the bracketing bin, tau*, tau in the bin
+    int32_t* bin;
+    uint32_t* pix;
+    // queues
+    uint32_t *qA, *qB, *qNext;
+    uint32_t* qcount;  // [4]: A, B, next, overflow
+    unsigned long long* rays;  // [2]
+    float* accum;
+    unsigned long long* work;  // gf_stats work counters (counting variant) or null
+};
+
+cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint32_t* err, cudaStream_t st);
+size_t gf_sort_temp_bytes(int64_t n);
+BuildScratch gf_scratch_layout(int64_t n, char* base);
+cudaError_t gf_launch_build(const void* prims, int64_t n, const BuildScratch& S, void* nodes, void* sorted,
+                            uint32_t* n_nodes, float* root_box, cudaStream_t st);
+cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
+cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
+size_t gf_render_state_bytes(int64_t n_paths, char* base, RenderDev* R);
+cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t sample_slot, cudaStream_t st,
+                                  StageTimer& T);

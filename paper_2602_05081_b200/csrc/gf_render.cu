@@ -1,0 +1,551 @@
+// gf_render.cu -- a8 free-flight distance sampling, a9 scatter loop, a10 accumulation
+// (Eq. 4-5, bisection/root finding P:L254, pipeline P:L352-L365).
+//
+// Wavefront over the paths of one sample pass: gen -> [ffA -> ffB -> nee] x max_depth -> finish.
+//  ffA: one traversal of the ray's scene interval accumulating tau into kBins t-bins
+//       (tau_total gives the escape test, the bins bracket the root);
+//  ffB: one traversal restricted to the bracketing bin gathers its active primitives, then a
+//       safeguarded Newton/bisection on tau(t) = tau* (derivative = kappa(t), analytic);
+//  nee: shadow ray towards the directional light (analytic T), HG phase, next direction.
+// Queues are warp-aggregated; work is fetched dynamically 32 paths at a time.
+#include <algorithm>
+
+#include "gf_device.cuh"
+#include "gf_internal.h"
+
+namespace gfk {
+
+constexpr int kBins = 32;
+constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6;
+
+template <bool COUNT, class F>
+__device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint32_t n_nodes,
+                                           const GPrim* __restrict__ prims, const RayDev& r, float t0, float t1,
+                                           uint32_t mask, Work& wk, F&& f) {
+    uint32_t i = 0;
+    while (i < n_nodes) {
+        const float4 lo = __ldg(&nodes[i].lo);
+        const float4 hi = __ldg(&nodes[i].hi);
+        const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+        if (COUNT) ++wk.nodes;
+        const bool hit = (node_mask(sk, info) & mask) && slab(r, lo, hi, t0, t1);
+        if (hit && (sk & kLeafBit)) {
+            const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, g = info & 31u;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const GPrim* p = prims + first + k;
+                GPrim P;
+                P.a = __ldg(&p->a); P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
+                if (COUNT) ++wk.tests;
+                f(P, g);
+            }
+            i = sk & ~kLeafBit;
+        } else if (hit) {
+            i = i + 1;
+        } else {
+            i = sk & ~kLeafBit;
+        }
+    }
+}
+
+// pixel of path p in this pass (-1 if p maps outside the image / shard)
+__device__ __forceinline__ int32_t path_pixel(const RenderDev& R, int64_t p) {
+    if (R.probe) return p < R.n_paths ? R.probe[p] : -1;
+    int64_t tile = p >> 10;
+    if (R.shard_kind == 1) tile = R.shard_rank + tile * R.shard_world;
+    if (tile >= (int64_t)R.tiles_x * R.tiles_y) return -1;
+    const int local = (int)(p & 1023), blk = local >> 5, lane = local & 31;
+    const int px = (int)(tile % R.tiles_x) * 32 + (blk & 3) * 8 + (lane & 7);
+    const int py = (int)(tile / R.tiles_x) * 32 + (blk >> 2) * 4 + (lane >> 3);
+    if (px >= R.cam.W || py >= R.cam.H) return -1;
+    return py * R.cam.W + px;
+}
+
+// warp-aggregated queue push (called by all 32 lanes of the warp)
+__device__ __forceinline__ void push(uint32_t* q, uint32_t* cnt, bool pred, uint32_t val) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    if (pred) q[base + __popc(m & ((1u << lane) - 1u))] = val;
+}
+
+// dynamic fetch of 32 work items per warp (all lanes call it)
+__device__ __forceinline__ bool fetch(uint32_t* work, uint32_t count, uint32_t& base) {
+    uint32_t b = 0;
+    if ((threadIdx.x & 31) == 0) b = atomicAdd(work, 32u);
+    base = __shfl_sync(0xFFFFFFFFu, b, 0);
+    return base < count;
+}
+
+__device__ __forceinline__ void count_rays(unsigned long long* c, bool active) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, active);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(c, (unsigned long long)__popc(m));
+}
+
+__device__ __forceinline__ float3 ld3(const float* x, const float* y, const float* z, uint32_t p) {
+    return make_float3(x[p], y[p], z[p]);
+}
+
+// tau of a ray through the masked, weighted field (NEE, tomography, ffB overflow)
+template <bool STOCH, bool COUNT>
+__device__ __forceinline__ double trace_tau(const RenderDev& R, const RayDev& r, float t0, float t1, uint32_t mask,
+                                            const float* w, Work& wk) {
+    double tau = 0.0;
+    traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, t0, t1, mask, wk, [&](const GPrim& P, uint32_t g) {
+        Setup s;
+        if (!prim_setup(P, r, t0, t1, s)) return;
+        if (COUNT) ++wk.hits;
+        float c = hit_tau(P, s, wk);
+        if (STOCH) c *= w[g];
+        tau += (double)c;
+    });
+    return tau;
+}
+
+__global__ void __launch_bounds__(128) k_gen(RenderDev R, int32_t sample) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // grid covers whole warps
+    const int32_t pix = p < R.n_paths ? path_pixel(R, p) : -1;
+    const bool ok = pix >= 0;
+    if (ok) {
+        float jx = 0.5f, jy = 0.5f;
+        if (R.jitter) {
+            uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
+            jx = u01(b.x); jy = u01(b.y);
+        }
+        float3 o, d;
+        camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+        R.ox[p] = o.x; R.oy[p] = o.y; R.oz[p] = o.z;
+        R.dx[p] = d.x; R.dy[p] = d.y; R.dz[p] = d.z;
+        R.beta[p] = 1.0f;
+        R.L[p] = 0.0f;
+        R.pix[p] = (uint32_t)pix;
+    }
+    push(R.qA, R.qcount + 0, ok, (uint32_t)p);
+}
+
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t pix = p < R.n_paths ? path_pixel(R, p) : -1;
+    Work wk;
+    if (pix >= 0) {
+        float jx = 0.5f, jy = 0.5f;
+        if (R.jitter) {
+            uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
+            jx = u01(b.x); jy = u01(b.y);
+        }
+        float3 o, d;
+        camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+        float w[kMaxGroups];
+        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_EXT,
+                                                 1, w)
+                                    : R.ext.static_mask;
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        R.L[p] = (float)trace_tau<STOCH, COUNT>(R, r, 0.0f, INFINITY, mask, w, wk);
+        wk.paths = 1;
+    }
+    count_rays(R.rays + 0, pix >= 0);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
+}
+
+// ---------------------------------------------------------------- binned tau over [t0, t1]
+// Adds each hit's partial integrals into NB equal t-bins (one erf evaluation per bin boundary
+// inside the chord, the chord ends shared) and counts the primitives overlapping each bin.
+template <int NB, bool STOCH, bool COUNT>
+__device__ __forceinline__ void bin_pass(const RenderDev& R, const RayDev& r, uint32_t mask, const float* w,
+                                         float t0, float t1, double* bins, uint16_t* cnts, Work& wk) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) { bins[k] = 0.0; cnts[k] = 0; }
+    const float bw = (t1 - t0) * (1.0f / NB), ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
+    traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, t0, t1, mask, wk, [&](const GPrim& P, uint32_t g) {
+        Setup s;
+        if (!prim_setup(P, r, t0, t1, s)) return;
+        if (COUNT) ++wk.hits;
+        float cj = P.a.w * s.ij;
+        if (STOCH) cj *= w[g];
+        const float ta = fmaf(s.u0 - s.bp, s.ij, s.tc), tb = fmaf(s.u1 - s.bp, s.ij, s.tc);
+        const int ka = min(NB - 1, max(0, (int)((ta - t0) * ibw)));
+        const int kb = min(NB - 1, max(0, (int)((tb - t0) * ibw)));
+        for (int m = ka; m <= kb; ++m) cnts[m] = (uint16_t)min(65535, cnts[m] + 1);
+        if (ka == kb) {
+            bins[ka] += (double)(cj * seg_J(s, s.u0, s.u1, wk));
+            return;
+        }
+        const float wmax = 0.5f * (fmaxf(s.u0 * s.u0, s.u1 * s.u1) + s.Om * s.Om);
+        float ua = s.u0;
+        if (wmax > kWMaxSeries || s.u1 - s.u0 < 1e-4f) {  // per-piece generic path
+            for (int m = ka + 1; m <= kb; ++m) {
+                float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
+                bins[m - 1] += (double)(cj * seg_J(s, ua, ub, wk));
+                ua = ub;
+            }
+            bins[kb] += (double)(cj * seg_J(s, ua, s.u1, wk));
+            return;
+        }
+        // shared endpoints: one erf evaluation per bin boundary inside the chord
+        float sp, cp;
+        sincos_red(s.phi0, &sp, &cp);
+        const float amp = cj * 0.5f * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+        float2 Fa = erf_shift(ua, s.Om);
+        for (int m = ka + 1; m <= kb; ++m) {
+            float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
+            float2 Fb = erf_shift(ub, s.Om);
+            bins[m - 1] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
+            Fa = Fb;
+            ua = ub;
+        }
+        float2 Fb = erf_shift(s.u1, s.Om);
+        bins[kb] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
+        if (COUNT) wk.erf(s.Om, (uint32_t)(kb - ka + 2));
+    });
+}
+
+// ---------------------------------------------------------------- ffA: binned tau over the ray
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_t depth) {
+    const uint32_t count = R.qcount[0];
+    uint32_t base;
+    Work wk;
+    while (fetch(R.qcount + kWorkA, count, base)) {
+        const uint32_t idx = base + (threadIdx.x & 31);
+        const bool active = idx < count;
+        uint32_t p = active ? R.qA[idx] : 0;
+        bool collide = false;
+        if (active) {
+            if (COUNT) ++wk.paths;
+            const uint32_t pix = R.pix[p];
+            const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+            float w[kMaxGroups];
+            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                     ST_EXT, 1, w)
+                                        : R.ext.static_mask;
+            const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
+            const double tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
+            const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+            float tlo, thi;
+            int32_t bin = -2;  // -2 escape, -1 collide at t_min, >= 0 bracketing bin
+            double cum_before = 0.0, bin_tau = 0.0;
+            int32_t nact = 0;
+            if (tstar <= 0.0) {
+                bin = -1;
+            } else if (R.n_nodes > 0 && slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
+                double bins[kBins];
+                uint16_t cnts[kBins];
+                bin_pass<kBins, STOCH, COUNT>(R, r, mask, w, tlo, thi, bins, cnts, wk);
+                double cum = 0.0;
+                for (int k = 0; k < kBins; ++k) {
+                    const double c2 = cum + bins[k];
+                    if (c2 >= tstar) { bin = k; cum_before = cum; bin_tau = bins[k]; nact = cnts[k]; break; }
+                    cum = c2;
+                }
+            }
+            if (bin == -2) {
+                R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+            } else {
+                R.bin[p] = bin < 0 ? bin : (bin | (nact << 16));
+                R.cum[p] = cum_before;               // tau before the bracketing bin
+                R.cum[p + R.n_paths] = tstar;        // tau*
+                R.cum[p + 2 * R.n_paths] = bin_tau;  // tau inside the bin
+                collide = true;
+            }
+        }
+        push(R.qB, R.qcount + 1, active && collide, p);
+        count_rays(R.rays + 0, active);
+    }
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+}
+
+// ---------------------------------------------------------------- ffB: root in the bracketing bin
+// Active primitives of the bracket, split into Gaussians (Omega == 0: real erf, 8 floats) and
+// Gabors (complex erf, 13 floats); kept in local memory.  Inside the bunny-like scenes the
+// overlap depth of the level-0 Gaussians is ~150, hence the large Gaussian list.
+constexpr int kCapG = 224, kCapB = 64;
+struct ActG {
+    float amp, kap0, j, tc, bp, u0, u1, F0;
+};
+struct ActB {
+    float amp, kap0, Om, phi0, cp, sp, j, tc, bp, u0, u1, F0r, F0i;
+};
+
+__device__ __forceinline__ double actg_tau(const ActG& a, float t, double& kap, Work& wk) {
+    float u = fmaf(a.j, t - a.tc, a.bp);
+    if (!(u > a.u0)) return 0.0;
+    if (u < a.u1) kap += (double)(a.kap0 * __expf(-0.5f * u * u));
+    else u = a.u1;
+    ++wk.erfr;
+    return (double)(a.amp * (erff(u * kRsqrt2) - a.F0));
+}
+
+__device__ __forceinline__ double actb_tau(const ActB& a, float t, double& kap, Work& wk) {
+    float u = fmaf(a.j, t - a.tc, a.bp);
+    if (!(u > a.u0)) return 0.0;
+    if (u < a.u1) {
+        float sp, cp;
+        sincos_red(fmaf(a.Om, u, a.phi0), &sp, &cp);
+        kap += (double)(a.kap0 * __expf(-0.5f * u * u) * cp);
+    } else {
+        u = a.u1;
+    }
+    const float wmax = 0.5f * (fmaxf(a.u0 * a.u0, u * u) + a.Om * a.Om);
+    if (wmax > kWMaxSeries || u - a.u0 < 1e-4f) {  // generic path (GL / midpoint): cj*J from scratch
+        Setup s;
+        s.r2 = 0.0f; s.h = INFINITY; s.bp = a.bp; s.j = a.j; s.ij = 1.0f / a.j; s.tc = a.tc; s.Om = a.Om;
+        s.phi0 = a.phi0; s.u0 = a.u0; s.u1 = u;
+        // amp = cj e^{-r2/2} e^{-Om^2/2} / 2 ; seg_J with r2 = 0 carries e^{-Om^2/2}/2 only for the series,
+        // so rescale from kap0 = cj j e^{-r2/2} / sqrt(2 pi)
+        return (double)(a.kap0 * s.ij * 2.5066282746310002f * seg_J(s, a.u0, u, wk));
+    }
+    wk.erf(a.Om, 1);
+    const float2 F = erf_shift(u, a.Om);
+    return (double)(a.amp * fmaf(a.cp, F.x - a.F0r, -a.sp * (F.y - a.F0i)));
+}
+
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_t depth) {
+    const uint32_t count = R.qcount[1];
+    uint32_t base;
+    Work wk;
+    while (fetch(R.qcount + kWorkB, count, base)) {
+        const uint32_t idx = base + (threadIdx.x & 31);
+        if (idx >= count) continue;
+        const uint32_t p = R.qB[idx];
+        const int32_t binw = R.bin[p];
+        const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+        float tres = 0.0f;
+        if (binw >= 0) {
+            const int32_t bin = binw & 0xFFFF;
+            const uint32_t pix = R.pix[p];
+            float w[kMaxGroups];
+            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                     ST_EXT, 1, w)
+                                        : R.ext.static_mask;
+            const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+            float tlo, thi;
+            slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi);
+            const float bw = (thi - tlo) * (1.0f / kBins);
+            const float ta = tlo + bin * bw;
+            const float tb = (bin == kBins - 1) ? thi : tlo + (bin + 1) * bw;
+            const double tstar = R.cum[p + R.n_paths];
+            const double cum0 = R.cum[p], span = R.cum[p + 2 * R.n_paths];
+            ActG ag[kCapG];
+            ActB ab[kCapB];
+            int ng = 0, nb = 0;
+            traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, ta, tb, mask, wk, [&](const GPrim& P, uint32_t g) {
+                Setup s;
+                if (!prim_setup(P, r, ta, tb, s)) return;
+                if (COUNT) ++wk.hits;
+                float cj = P.a.w * s.ij;
+                if (STOCH) cj *= w[g];
+                const float kap0 = cj * s.j * kInvSqrt2Pi * __expf(-0.5f * s.r2);
+                if (s.Om == 0.0f) {
+                    if (ng < kCapG) {
+                        ActG& a = ag[ng];
+                        a.amp = 0.5f * cj * __expf(-0.5f * s.r2); a.kap0 = kap0; a.j = s.j; a.tc = s.tc; a.bp = s.bp;
+                        a.u0 = s.u0; a.u1 = s.u1; a.F0 = erff(s.u0 * kRsqrt2);
+                        if (COUNT) ++wk.erfr;
+                    }
+                    ++ng;
+                } else {
+                    if (nb < kCapB) {
+                        ActB& a = ab[nb];
+                        a.amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om)); a.kap0 = kap0;
+                        a.Om = s.Om; a.phi0 = s.phi0; a.j = s.j; a.tc = s.tc; a.bp = s.bp; a.u0 = s.u0; a.u1 = s.u1;
+                        sincos_red(s.phi0, &a.sp, &a.cp);
+                        const float2 F0 = erf_shift(s.u0, s.Om);
+                        if (COUNT) wk.erf(s.Om, 1);
+                        a.F0r = F0.x; a.F0i = F0.y;
+                    }
+                    ++nb;
+                }
+            });
+            const bool overflow = ng > kCapG || nb > kCapB;
+            if (COUNT && overflow) ++wk.overflow;
+            auto eval = [&](float t, double& kap) -> double {
+                kap = 0.0;
+                double acc = cum0 - tstar;
+                if (COUNT) ++wk.root;
+                if (!overflow) {
+                    for (int k = 0; k < ng; ++k) acc += actg_tau(ag[k], t, kap, wk);
+                    for (int k = 0; k < nb; ++k) acc += actb_tau(ab[k], t, kap, wk);
+                } else {  // overflow: re-traverse [ta, t]; bisection only
+                    acc += trace_tau<STOCH, COUNT>(R, r, ta, t, mask, w, wk);
+                    kap = 0.0;
+                }
+                return acc;
+            };
+            float lo = ta, hi = tb;
+            // initial guess: linear in the bin's own tau (from ffA)
+            const double need = tstar - cum0;
+            float t = ta + 0.5f * (tb - ta);
+            if (span > 0.0 && need >= 0.0) t = ta + (float)(need / span) * (tb - ta);
+            t = fminf(fmaxf(t, lo), hi);
+            for (int it = 0; it < 48; ++it) {
+                double kap;
+                const double f = eval(t, kap);
+                if (f >= 0.0) hi = t; else lo = t;
+                if (!(hi - lo > 1e-6f * bw)) break;
+                float tn = (kap > 0.0) ? (float)((double)t - f / kap) : 0.5f * (lo + hi);
+                if (!(tn > lo && tn < hi)) tn = 0.5f * (lo + hi);
+                if (fabsf(tn - t) <= 1e-7f * bw) { t = tn; break; }
+                t = tn;
+            }
+            tres = t;
+        }
+        // collision point becomes the new origin
+        R.ox[p] = fmaf(tres, d.x, o.x);
+        R.oy[p] = fmaf(tres, d.y, o.y);
+        R.oz[p] = fmaf(tres, d.z, o.z);
+    }
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFB, wk);
+}
+
+// ---------------------------------------------------------------- NEE + phase sampling
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_nee(RenderDev R, int32_t sample, int32_t depth) {
+    const uint32_t count = R.qcount[1];
+    uint32_t base;
+    Work wk;
+    while (fetch(R.qcount + kWorkN, count, base)) {
+        const uint32_t idx = base + (threadIdx.x & 31);
+        const bool active = idx < count;
+        uint32_t p = active ? R.qB[idx] : 0;
+        bool cont = false;
+        if (active) {
+            const uint32_t pix = R.pix[p];
+            const float3 x = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+            float w[kMaxGroups];
+            const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample,
+                                                     (uint32_t)depth, ST_NEE, 0, w)
+                                        : R.nee.static_mask;
+            const RayDev r = make_ray(x, R.sun, 0.0f, INFINITY);
+            const double tau = trace_tau<STOCH, COUNT>(R, r, 0.0f, INFINITY, mask, w, wk);
+            const float beta = R.beta[p];
+            const float cost = d.x * R.sun.x + d.y * R.sun.y + d.z * R.sun.z;
+            R.L[p] += beta * R.albedo * hg_eval(R.hg_g, cost) * (float)exp(-tau) * R.sun_E;
+            if (depth + 1 < R.max_depth) {
+                uint4 b = stream_block(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_SCAT, 0);
+                float3 nd = hg_sample(R.hg_g, d, u01(b.x), u01(b.y));
+                R.dx[p] = nd.x; R.dy[p] = nd.y; R.dz[p] = nd.z;
+                R.beta[p] = beta * R.albedo;
+                cont = true;
+            }
+        }
+        push(R.qNext, R.qcount + 2, active && cont, p);
+        count_rays(R.rays + 1, active);
+    }
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
+}
+
+__global__ void k_rotate(uint32_t* qc) {
+    qc[0] = qc[2];
+    qc[1] = 0; qc[2] = 0;
+    qc[kWorkA] = 0; qc[kWorkB] = 0; qc[kWorkN] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_finish(RenderDev R, int32_t slot) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= R.n_paths) return;
+    const int32_t pix = path_pixel(R, p);
+    if (pix < 0) return;
+    const float v = R.L[p];
+    if (R.probe) {
+        R.accum[p * R.spp_count + slot] = v;
+    } else {
+        R.accum[2 * (int64_t)pix] += v;
+        R.accum[2 * (int64_t)pix + 1] += v * v;
+    }
+}
+
+}  // namespace gfk
+
+using namespace gfk;
+
+size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += (bytes + 255) & ~(size_t)255; return p; };
+    const size_t nf = sizeof(float) * (size_t)n, nu = sizeof(uint32_t) * (size_t)n;
+    float* ox = (float*)take(nf); float* oy = (float*)take(nf); float* oz = (float*)take(nf);
+    float* dx = (float*)take(nf); float* dy = (float*)take(nf); float* dz = (float*)take(nf);
+    float* beta = (float*)take(nf); float* L = (float*)take(nf);
+    double* cum = (double*)take(sizeof(double) * 3 * (size_t)n);
+    int32_t* bin = (int32_t*)take(nu); uint32_t* pix = (uint32_t*)take(nu);
+    uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
+    uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
+    if (R) {
+        R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
+        R->cum = cum; R->bin = bin; R->pix = pix;
+        R->qA = qA; R->qB = qB; R->qNext = qN; R->qcount = qc;
+    }
+    return off;
+}
+
+static int g_persist_blocks = 0;
+
+template <bool S, bool C>
+static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, cudaStream_t st, StageTimer& T,
+                         bool stoch_nee) {
+    cudaEvent_t e;
+    T.pre(STAGE_FFA, st, e);
+    k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    T.post(STAGE_FFA, st, e);
+    T.pre(STAGE_FFB, st, e);
+    k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    T.post(STAGE_FFB, st, e);
+    T.pre(STAGE_NEE, st, e);
+    if (stoch_nee) k_nee<true, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    else k_nee<false, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    T.post(STAGE_NEE, st, e);
+}
+
+cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cudaStream_t st, StageTimer& T) {
+    cudaError_t e;
+    if (R.n_paths == 0) return cudaSuccess;
+    if (!g_persist_blocks) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g_persist_blocks = sms * 16;
+    }
+    const bool cnt = R.work != nullptr;
+    const bool stoch_ext = !(R.ext.ls == 0 && R.ext.os == 0);
+    const bool stoch_nee = !(R.nee.ls == 0 && R.nee.os == 0);
+    const unsigned grid = (unsigned)((R.n_paths + 127) / 128);
+    const unsigned pgrid = (unsigned)std::min<int64_t>((int64_t)g_persist_blocks, (R.n_paths + 127) / 128);
+    if ((e = cudaMemsetAsync(R.qcount, 0, sizeof(uint32_t) * 16, st))) return e;
+    cudaEvent_t ev;
+    if (R.mode == 0) {
+        T.pre(STAGE_TOMO, st, ev);
+        if (stoch_ext) {
+            if (cnt) k_tomo<true, true><<<grid, 128, 0, st>>>(R, sample);
+            else k_tomo<true, false><<<grid, 128, 0, st>>>(R, sample);
+        } else {
+            if (cnt) k_tomo<false, true><<<grid, 128, 0, st>>>(R, sample);
+            else k_tomo<false, false><<<grid, 128, 0, st>>>(R, sample);
+        }
+        T.post(STAGE_TOMO, st, ev);
+    } else {
+        T.pre(STAGE_GEN, st, ev);
+        k_gen<<<grid, 128, 0, st>>>(R, sample);
+        T.post(STAGE_GEN, st, ev);
+        for (int d = 0; d < R.max_depth; ++d) {
+            if (stoch_ext) {
+                if (cnt) launch_depth<true, true>(R, sample, d, pgrid, st, T, stoch_nee);
+                else launch_depth<true, false>(R, sample, d, pgrid, st, T, stoch_nee);
+            } else {
+                if (cnt) launch_depth<false, true>(R, sample, d, pgrid, st, T, stoch_nee);
+                else launch_depth<false, false>(R, sample, d, pgrid, st, T, stoch_nee);
+            }
+            T.pre(STAGE_FINISH, st, ev);
+            k_rotate<<<1, 1, 0, st>>>(R.qcount);
+            T.post(STAGE_FINISH, st, ev);
+            std::swap(R.qA, R.qNext);
+        }
+    }
+    T.pre(STAGE_FINISH, st, ev);
+    k_finish<<<(unsigned)((R.n_paths + 255) / 256), 256, 0, st>>>(R, slot);
+    T.post(STAGE_FINISH, st, ev);
+    return cudaGetLastError();
+}

@@ -1,0 +1,140 @@
+// gf_trace.cu -- a4 masked all-hits traversal + a5 ellipsoid clip + a6 fused line integral
+// + a7 transmittance (Eq. 2-3; masks P:L344-L350).
+#include "gf_device.cuh"
+#include "gf_internal.h"
+
+namespace gfk {
+
+// Stackless depth-first traversal with escape links over all nodes whose box meets [t0,t1]
+// and whose group mask meets the ray mask; calls f(prim, group) for every primitive of every
+// visited leaf.  No early exit: tau needs every overlap.
+template <bool COUNT, class F>
+__device__ __forceinline__ void traverse(const GNode* __restrict__ nodes, uint32_t n_nodes,
+                                         const GPrim* __restrict__ prims, const RayDev& r, float t0, float t1,
+                                         uint32_t mask, uint32_t& nvis, F&& f) {
+    uint32_t i = 0;
+    while (i < n_nodes) {
+        const float4 lo = __ldg(&nodes[i].lo);
+        const float4 hi = __ldg(&nodes[i].hi);
+        const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+        if (COUNT) ++nvis;
+        const bool hit = (node_mask(sk, info) & mask) && slab(r, lo, hi, t0, t1);
+        if (hit && (sk & kLeafBit)) {
+            const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, g = info & 31u;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const GPrim* p = prims + first + k;
+                GPrim P;
+                P.a = __ldg(&p->a); P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
+                f(P, g);
+            }
+            i = sk & ~kLeafBit;
+        } else if (hit) {
+            i = i + 1;
+        } else {
+            i = sk & ~kLeafBit;
+        }
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void brute(const GPrim* __restrict__ prims, int64_t n, uint32_t mask, F&& f) {
+    for (int64_t k = 0; k < n; ++k) {
+        const GPrim* p = prims + k;
+        GPrim P;
+        P.d = __ldg(&p->d);
+        uint32_t g = __float_as_uint(P.d.w) & 31u;
+        if (!((mask >> g) & 1u)) continue;
+        P.a = __ldg(&p->a); P.b = __ldg(&p->b); P.c = __ldg(&p->c);
+        f(P, g);
+    }
+}
+
+template <bool BRUTE, bool COUNT, bool STOCH>
+__global__ void __launch_bounds__(128) k_trace(TraceArgs A) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const float4 r0 = __ldg((const float4*)A.rays + 2 * i);
+    const float4 r1 = __ldg((const float4*)A.rays + 2 * i + 1);
+    const float3 o = make_float3(r0.x, r0.y, r0.z), d = make_float3(r1.x, r1.y, r1.z);
+    const RayDev r = make_ray(o, d, r0.w, r1.w);
+    float w[kMaxGroups];
+    uint32_t mask;
+    if (STOCH) mask = policy_for(A.pol, A.sc, d, A.seed, (uint32_t)i, 0, 0, ST_EXT, 1, w);
+    else mask = A.pol.static_mask;
+    double tau = 0.0;
+    uint32_t nvis = 0, ntest = 0, nhit = 0;
+    Work wk;
+    auto on_prim = [&](const GPrim& P, uint32_t g) {
+        if (COUNT) ++ntest;
+        Setup s;
+        if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
+        if (COUNT) ++nhit;
+        float c = hit_tau(P, s, wk);
+        if (STOCH) c *= w[g];
+        tau += (double)c;
+    };
+    if (BRUTE) brute(A.prims, A.n_prims, mask, on_prim);
+    else traverse<COUNT>(A.nodes, A.n_nodes, A.prims, r, r.tmin, r.tmax, mask, nvis, on_prim);
+    A.tau[i] = (float)tau;
+    if (A.T) A.T[i] = (float)exp(-tau);
+    if (COUNT && A.counters) {
+        A.counters[3 * i] = nvis;
+        A.counters[3 * i + 1] = ntest;
+        A.counters[3 * i + 2] = nhit;
+    }
+    if (COUNT && A.work) {
+        wk.nodes = nvis; wk.tests = ntest; wk.hits = nhit; wk.paths = 1;
+        flush_work_thread(A.work + kWorkSlots * STAGE_TRACE, wk);
+    }
+}
+
+template <bool BRUTE>
+__global__ void __launch_bounds__(128) k_candidates(TraceArgs A) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const float4 r0 = __ldg((const float4*)A.rays + 2 * i);
+    const float4 r1 = __ldg((const float4*)A.rays + 2 * i + 1);
+    const RayDev r = make_ray(make_float3(r0.x, r0.y, r0.z), make_float3(r1.x, r1.y, r1.z), r0.w, r1.w);
+    const uint32_t mask = A.pol.static_mask;
+    int32_t cnt = 0;
+    uint32_t nvis = 0;
+    int32_t* out = A.cand_ids + i * (int64_t)A.cand_cap;
+    auto on_prim = [&](const GPrim& P, uint32_t) {
+        Setup s;
+        if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
+        if (cnt < A.cand_cap) out[cnt] = (int32_t)(__float_as_uint(P.d.w) >> 5);
+        ++cnt;
+    };
+    if (BRUTE) brute(A.prims, A.n_prims, mask, on_prim);
+    else traverse<false>(A.nodes, A.n_nodes, A.prims, r, r.tmin, r.tmax, mask, nvis, on_prim);
+    A.cand_count[i] = cnt;
+}
+
+}  // namespace gfk
+
+using namespace gfk;
+
+cudaError_t gf_launch_trace(const TraceArgs& A, bool brute_force, bool count, cudaStream_t st) {
+    if (A.n == 0) return cudaSuccess;
+    count = count || A.work != nullptr;
+    const unsigned grid = (unsigned)((A.n + 127) / 128);
+    const bool stoch = !(A.pol.ls == 0 && A.pol.os == 0);
+#define GF_T(B, C, S) k_trace<B, C, S><<<grid, 128, 0, st>>>(A)
+    if (brute_force) {
+        if (count) { if (stoch) GF_T(true, true, true); else GF_T(true, true, false); }
+        else { if (stoch) GF_T(true, false, true); else GF_T(true, false, false); }
+    } else {
+        if (count) { if (stoch) GF_T(false, true, true); else GF_T(false, true, false); }
+        else { if (stoch) GF_T(false, false, true); else GF_T(false, false, false); }
+    }
+#undef GF_T
+    return cudaGetLastError();
+}
+
+cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute_force, cudaStream_t st) {
+    if (A.n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((A.n + 127) / 128);
+    if (brute_force) k_candidates<true><<<grid, 128, 0, st>>>(A);
+    else k_candidates<false><<<grid, 128, 0, st>>>(A);
+    return cudaGetLastError();
+}

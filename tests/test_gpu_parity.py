@@ -1,0 +1,311 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (DESIGN.md §3 C20/C21, north star): deterministic tau within
+|tau_gpu - tau_or| <= 1e-4 |tau_or| + 1e-6 A_or + 1e-7 (A = sum |tau_i|) and T within 1e-4
+relative; candidate sets bit-exact between the BVH and brute-force kernels, equal to the
+oracle's up to grazing pairs; stochastic estimates with identical Philox streams agree in
+per-pixel mean within 3 standard errors.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2602_05081_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def gfm():
+    from paper_2602_05081_b200 import build as B
+    B.build()
+    from paper_2602_05081_b200 import gf
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return gf
+
+
+def field(gfm, scene, **kw):
+    f = gfm.GaborField(0)
+    f.load_primitives(scene, **kw)
+    f.build_bvh()
+    return f
+
+
+def assert_tau_parity(tau_g, tau_o, A_o, T_g=None, what=""):
+    tau_g = np.asarray(tau_g, np.float64)
+    err = np.abs(tau_g - tau_o)
+    tol = 1e-4 * np.abs(tau_o) + 1e-6 * A_o + 1e-7
+    bad = np.nonzero(err > tol)[0]
+    assert bad.size == 0, f"{what}: {bad.size} rays out of tolerance, worst {err[bad].max():.3e} e.g. ray {bad[0]}: " \
+                          f"gpu {tau_g[bad[0]]} oracle {tau_o[bad[0]]} A {A_o[bad[0]]}"
+    if T_g is not None:
+        T_o = np.exp(-tau_o)
+        assert np.all(np.abs(np.asarray(T_g, np.float64) - T_o) <= 1e-4 * T_o + 1e-7), what
+
+
+def camera_rays(desc, n=None, seed=0):
+    W, H = desc["width"], desc["height"]
+    if n is None:
+        idx = np.arange(W * H)
+    else:
+        idx = np.random.default_rng(seed).integers(0, W * H, n)
+    o, d = I.camera_rays_f64(desc, idx % W, idx // W)
+    return I.pack_rays(o, d)
+
+
+# ------------------------------------------------------------------------------ a1
+def test_load_groups_match_oracle(gfm, orc):
+    sc = I.scene_cfg1()
+    f = field(gfm, sc)
+    rec = f.prim_ws[: 64 * sc["n"]].view(torch.int32).view(sc["n"], 16).cpu().numpy()
+    g_gpu = rec[:, 15] & 31
+    idx = rec[:, 15] >> 5
+    assert np.array_equal(idx, np.arange(sc["n"]))
+    g_or, _ = orc.Scene(sc).groups()
+    assert np.array_equal(g_gpu, g_or)
+
+
+def test_invalid_inputs_rejected(gfm):
+    sc = I.scene_cfg1(n=50)
+    bad = dict(sc, scale=sc["scale"].copy())
+    bad["scale"][7, 1] = 0.0
+    f = gfm.GaborField(0)
+    with pytest.raises(gfm.GFError) as e:
+        f.load_primitives(bad)
+    assert e.value.status == 3  # GF_E_SINGULAR_COVARIANCE
+    bad = dict(sc, level=sc["level"].copy())
+    bad["level"][3] = 9
+    with pytest.raises(gfm.GFError) as e:
+        f.load_primitives(bad)
+    assert e.value.status == 8
+    with pytest.raises(gfm.GFError) as e:
+        f.trace_transmittance(np.zeros((1, 8), np.float32))
+    assert e.value.status == 2  # GF_E_STATE
+    with pytest.raises(gfm.GFError) as e:
+        f.set_lod_mask({"level_strategy": 2, "beta": 1.0})
+    assert e.value.status == 7
+
+
+# ------------------------------------------------------------------------------ a4-a7
+@pytest.mark.parametrize("brute", [False, True])
+def test_cfg1_camera_tau_parity(gfm, orc, brute):
+    sc = I.scene_cfg1()
+    desc = I.render_desc_cfg1()
+    rays = camera_rays(desc)
+    f = field(gfm, sc)
+    tau, T, _ = f.trace_transmittance(rays, brute_force=brute)
+    r = orc.Scene(sc).trace(rays)
+    assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), "cfg1 camera")
+
+
+def test_random_rays_and_ragged_sizes(gfm, orc):
+    sc = I.scene_cfg1(seed=77)
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    for n in (1, 31, 129, 1000):
+        rays = I.rays_through_box(n, n, tmin=0.0)
+        rays[::3, 3] = 2.5   # clipped starts
+        rays[::5, 7] = 4.7   # clipped ends
+        tau, T, _ = f.trace_transmittance(rays)
+        r = S.trace(rays)
+        assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), f"n={n}")
+
+
+def test_empty_scene_and_misses(gfm):
+    f = field(gfm, I.empty_scene())
+    tau, T, _ = f.trace_transmittance(I.rays_through_box(1, 64))
+    assert torch.all(tau == 0) and torch.all(T == 1)
+    f2 = field(gfm, I.scene_cfg1(n=100))
+    miss = I.pack_rays(np.tile([[10.0, 10.0, 10.0]], (8, 1)), np.tile([[1.0, 0, 0]], (8, 1)))
+    tau, T, _ = f2.trace_transmittance(miss)
+    assert torch.all(tau == 0)
+
+
+def test_candidate_sets_bvh_equal_brute_force(gfm, orc):
+    """C21: BVH candidate sets == brute-force kernel sets bit-exactly (same fp32 predicate), and ==
+    the double oracle's up to grazing pairs (|r^2/E^2 - 1| <= 1e-5)."""
+    for sc, masks in ((I.scene_cfg1(), (0xFFFFFFFF, I.level_mask([0, 2]), 1 << 5)),
+                      (I.scene_cfg2(), (0xFFFFFFFF, I.level_mask([0, 1]))),):
+        f = field(gfm, sc)
+        S = orc.Scene(sc)
+        desc = I.render_desc_cfg1() if sc["n"] == 1000 else I.render_desc_cfg2(3, 256, 256)
+        rays = camera_rays(desc, 300, seed=5)
+        rays[::4] = I.rays_through_box(9, len(rays[::4]))
+        for m in masks:
+            f.set_lod_mask({"static_mask": m})
+            ids_b, cnt_b = f.trace_candidates(rays, 4096)
+            ids_f, cnt_f = f.trace_candidates(rays, 4096, brute_force=True)
+            ids_b, cnt_b, ids_f, cnt_f = (t.cpu().numpy() for t in (ids_b, cnt_b, ids_f, cnt_f))
+            assert np.array_equal(cnt_b, cnt_f)
+            grazing = 0
+            for k in range(len(rays)):
+                sb = set(ids_b[k, :cnt_b[k]].tolist())
+                assert sb == set(ids_f[k, :cnt_f[k]].tolist())
+                so = set(S.candidates(rays[k], m)[0].tolist())
+                for i in sb ^ so:
+                    assert abs(S.r2_rel(i, rays[k]) - 1.0) <= 1e-5, (k, i)
+                    grazing += 1
+            assert grazing <= 2
+
+
+def test_static_masks_parity(gfm, orc):
+    sc = I.scene_cfg1()
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    rays = camera_rays(I.render_desc_cfg1(), 512, seed=3)
+    for levels in ([0], [0, 1], [0, 1, 2], [1, 3]):
+        m = I.level_mask(levels)
+        f.set_lod_mask({"static_mask": m})
+        tau, _, _ = f.trace_transmittance(rays)
+        r = S.trace(rays, mask=m)
+        assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], None, f"mask {levels}")
+
+
+@pytest.mark.parametrize("pol", [dict(level_strategy=5, beta=0.2, orient_strategy=3),
+                                 dict(level_strategy=1), dict(level_strategy=4, beta=0.5, orient_strategy=4,
+                                                              delta=0.5),
+                                 dict(orient_strategy=2), dict(level_strategy=3, orient_strategy=1, delta=0.7)])
+def test_stochastic_mask_parity(gfm, orc, pol):
+    """Per-ray stochastic policy with identical Philox uniforms: same mask and weights on both sides
+    (DESIGN.md §5), so tau-hat agrees per ray to the deterministic tolerance."""
+    sc = I.scene_cfg1()
+    f0 = I.group_f0(sc)
+    f = field(gfm, sc, group_f0=f0)
+    f.set_lod_mask(pol)
+    rays = camera_rays(I.render_desc_cfg1(), 256, seed=11)
+    seed = 0xABCDEF12345
+    tau, _, _ = f.trace_transmittance(rays, seed=seed)
+    S = orc.Scene(sc)
+    P = sc["P"]
+    tau_o, A_o = np.zeros(len(rays)), np.zeros(len(rays))
+    for i in range(len(rays)):
+        ul = orc.uniform(seed, i, 0, 0, 0, 1)
+        uo = [orc.uniform(seed, i, 0, 0, 0, 2 + l) for l in range(P - 1)]
+        m, w = S.policy_eval(dict(I.policy(), **pol), rays[i, 4:7], ul, uo, f0)
+        r = S.trace(rays[i:i + 1], mask=m, weights=w, nthreads=1)
+        tau_o[i], A_o[i] = r["tau"][0], r["A"][0]
+    assert_tau_parity(tau.cpu().numpy(), tau_o, A_o, None, str(pol))
+
+
+@pytest.mark.parametrize("ratio", [30.0, 300.0, 3000.0])
+def test_far_origin_stress(gfm, orc, ratio):
+    """rays starting |o-mu|/s in {30,300,3000} from primitives of s in [0.005,0.05]."""
+    fo = I.far_origin_pairs(int(ratio), 2000, ratio)
+    n = len(fo["rays"])
+    sc = {"n": n, "P": 4, "K": 3, "mu": fo["mu"].astype(np.float32), "quat": fo["quat"],
+          "scale": fo["scale"].astype(np.float32), "alpha": np.ones(n, np.float32),
+          "omega": fo["omega"].astype(np.float32), "extent": np.full(n, 3.0, np.float32),
+          "level": np.ones(n, np.uint8), "bin": np.zeros(n, np.uint8), "bin_axes": I.bin_axes(3)}
+    f = field(gfm, sc)
+    tau, _, _ = f.trace_transmittance(fo["rays"])
+    r = orc.Scene(sc).trace(fo["rays"])
+    assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], None, f"far origin {ratio}")
+
+
+def test_cfg2_sampled_rays(gfm, orc):
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    desc = I.render_desc_cfg2(3)
+    rays = camera_rays(desc, 600, seed=21)
+    S = orc.Scene(sc)
+    for li, levels in enumerate(I.CFG2_LOD_LEVELS):
+        m = I.level_mask(levels)
+        f.set_lod_mask({"static_mask": m})
+        tau, T, cnt = f.trace_transmittance(rays, counters=True)
+        r = S.trace(rays, mask=m)
+        assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), f"cfg2 mask {levels}")
+        assert np.array_equal(cnt.cpu().numpy()[:, 2], r["nhits"])
+
+
+# ------------------------------------------------------------------------------ render
+def test_render_tomography_cfg1_full_image(gfm, orc):
+    """Config 1 exactly as the bench runs it: 64x64, pixel centres, 1 spp, full LOD, gf_render."""
+    sc = I.scene_cfg1()
+    desc = I.render_desc_cfg1()
+    f = field(gfm, sc)
+    acc, rc = f.render(desc)
+    acc = acc.view(-1, 2).cpu().numpy()
+    S = orc.Scene(sc)
+    pix = np.arange(64 * 64)
+    vals, _ = S.render_probes(desc, pix, 0, 1)
+    r = S.trace(camera_rays(desc))
+    assert_tau_parity(acc[:, 0], vals[:, 0], r["A"], None, "cfg1 tomo")
+    assert int(rc[0]) == 64 * 64
+
+
+def _probe_compare(gfm, orc, sc, desc, probes, spp, what, frac_tol=0.02, f0=None):
+    f = field(gfm, sc, group_f0=f0)
+    if f0 is not None:
+        desc = dict(desc, group_f0=f0)
+    vg, rc = f.render(desc, 0, spp, probes=probes)
+    vg = vg.view(len(probes), spp).cpu().numpy().astype(np.float64)
+    vo, nr = orc.Scene(sc).render_probes(desc, probes, 0, spp)
+    diff = np.abs(vg - vo)
+    flips = np.mean(diff > 1e-3 * (np.abs(vo) + 1e-2))
+    se = vo.std() / math.sqrt(vo.size)
+    assert abs(vg.mean() - vo.mean()) <= 3 * se + 1e-6, (what, vg.mean(), vo.mean(), se)
+    assert flips <= frac_tol, (what, flips)
+    per_pix_se = vo.std(1) / math.sqrt(spp) + 1e-9
+    assert np.mean(np.abs(vg.mean(1) - vo.mean(1)) <= 3 * per_pix_se + 1e-6) >= 0.98
+    return vg, vo, int(rc.sum())
+
+
+def test_render_single_scatter_probes_paired(gfm, orc):
+    sc = I.scene_cfg1p()
+    desc = I.render_desc_cfg2(3, 64, 64)
+    desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 64, 64))
+    desc["ext"] = desc["nee"] = I.policy()
+    probes = np.random.default_rng(1).integers(0, 64 * 64, 48)
+    _probe_compare(gfm, orc, sc, desc, probes, 16, "single scatter cfg1p")
+
+
+def test_render_multi_scatter_probes(gfm, orc):
+    sc = I.scene_cfg1p()
+    desc = I.render_desc_cfg2(3, 32, 32)
+    desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 32, 32))
+    desc.update(max_depth=6, albedo=0.95, hg_g=0.6, ext=I.policy(), nee=I.policy())
+    probes = np.random.default_rng(2).integers(0, 32 * 32, 24)
+    _probe_compare(gfm, orc, sc, desc, probes, 16, "multi scatter", frac_tol=0.05)
+
+
+def test_render_stochastic_masks_probes(gfm, orc):
+    """Config-4 style policies: PL+CV(Accum.) beta=0.2 x orientation Importance on extension
+    rays, Zero NEE, multiple scattering, identical Philox streams."""
+    sc = I.scene_cfg1()
+    desc = I.render_desc_cfg2(3, 32, 32)
+    desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 32, 32))
+    desc.update(max_depth=4, albedo=0.9, ext=I.policy(level_strategy=5, beta=0.2, orient_strategy=3),
+                nee=I.policy(static_mask=1))
+    probes = np.random.default_rng(3).integers(0, 32 * 32, 24)
+    _probe_compare(gfm, orc, sc, desc, probes, 16, "stochastic", frac_tol=0.05, f0=I.group_f0(sc))
+
+
+def test_render_tomography_stochastic_probes(gfm, orc):
+    sc = I.scene_cfg1()
+    desc = I.render_desc_cfg1(32, 32)
+    desc.update(jitter=1, ext=I.policy(level_strategy=2, beta=0.5, orient_strategy=2))
+    probes = np.random.default_rng(4).integers(0, 32 * 32, 32)
+    vg, vo, _ = _probe_compare(gfm, orc, sc, desc, probes, 32, "stochastic tomography", frac_tol=0.0)
+
+
+def test_cfg2_bench_configuration_sampled(gfm, orc):
+    """Config 2 at full size in the launch configuration bench.py times (1024^2, 1 spp per LOD
+    mask, single scattering): sampled pixels of the full-image render vs the oracle's paths."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    rng = np.random.default_rng(5)
+    for mi in (0, 3):
+        desc = I.render_desc_cfg2(mi)
+        acc, rc = f.render(desc)
+        acc = acc.view(-1, 2).cpu().numpy()
+        pix = rng.integers(0, 1024 * 1024, 96)
+        vo, _ = S.render_probes(desc, pix, 0, 1)
+        vg = acc[pix, 0].astype(np.float64)
+        flips = np.mean(np.abs(vg - vo[:, 0]) > 1e-3 * (np.abs(vo[:, 0]) + 1e-2))
+        assert flips <= 0.03, (mi, flips)
+        assert int(rc[0]) == 1024 * 1024
