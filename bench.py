@@ -32,6 +32,7 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # hit setup, and one complex-erf endpoint (Horner, kErfTerms complex terms, 4 FFMA = 8 FLOP each).
 ERF_TERMS = 30
 FLOP_NODE, FLOP_TEST, FLOP_HIT, FLOP_ERF = 24, 45, 40, 8 * ERF_TERMS
+FLOP_ERF_REAL = 20  # real erf (Omega = 0): erff, ~10 FFMA
 FLOP_ROOT_EVAL = 20  # per root-finder evaluation (kappa term, excluding its erf endpoints)
 
 
@@ -236,8 +237,8 @@ def main():
     dom = max(stage_ms, key=stage_ms.get)
     launches = st["stage_launches"][dom]
     w = sw["work"][dom]
-    flops = (FLOP_NODE * w["nodes"] + FLOP_TEST * w["tests"] + FLOP_HIT * w["hits"] + FLOP_ERF * w["erf"]
-             + FLOP_ROOT_EVAL * w["root_evals"])
+    flops = (FLOP_NODE * w["nodes"] + FLOP_TEST * w["tests"] + FLOP_HIT * w["hits"] + FLOP_ERF * w["erf_complex"]
+             + FLOP_ERF_REAL * w["erf_real"] + FLOP_ROOT_EVAL * w["root_evals"])
     per_launch_flop = flops / max(1, sw["stage_launches"][dom])
     avg_ms = stage_ms[dom] / max(1, launches)
     achieved = per_launch_flop / (avg_ms * 1e-3) / 1e12

@@ -21,9 +21,11 @@ struct gf_ctx {
     bool loaded = false, built = false;
     int64_t n = 0;
     SceneDev sc{};
-    GPrim* prims = nullptr;  // input order (prim_ws)
-    GNode* nodes = nullptr;  // bvh_ws
+    GPrim* prims = nullptr;    // input order (prim_ws)
+    uint8_t* group = nullptr;  // input-order group ids (prim_ws, after the records)
+    GNode* nodes = nullptr;    // bvh_ws
     GPrim* sorted = nullptr;
+    int32_t* perm = nullptr;   // sorted -> input index (bvh_ws, after the nodes)
     uint32_t n_nodes = 0;
     float root[6] = {0, 0, 0, 0, 0, 0};
     // policies
@@ -179,10 +181,10 @@ const char* gf_last_error(const gf_ctx* c) { return c ? c->err.c_str() : "null c
 
 gf_status gf_query_workspace(int64_t n, size_t* prim_bytes, size_t* bvh_bytes, size_t* scratch_bytes) {
     if (n < 0 || n >= (1 << 24)) return GF_E_INVALID_ARGUMENT;
-    if (prim_bytes) *prim_bytes = align256(sizeof(GPrim) * (size_t)std::max<int64_t>(n, 1));
+    const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+    if (prim_bytes) *prim_bytes = align256(sizeof(GPrim) * n1) + align256(n1);
     if (bvh_bytes)
-        *bvh_bytes = align256(sizeof(GPrim) * (size_t)std::max<int64_t>(n, 1)) +
-                     align256(sizeof(GNode) * (size_t)std::max<int64_t>(2 * n, 1));
+        *bvh_bytes = align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1) + align256(sizeof(int32_t) * n1);
     if (scratch_bytes) {
         if (n > 0) {
             int ndev = 0;
@@ -220,7 +222,8 @@ gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_p
     for (int i = 0; i < 3 * K; ++i) A.axes[i] = pyr->bin_axes[i];
     uint32_t init[4] = {0u, 0xFFFFFFFFu, 0u, 0u};
     GF_CUDA(c, cudaMemcpyAsync(c->d_err, init, sizeof(init), cudaMemcpyHostToDevice, st), "memcpy");
-    GF_CUDA(c, gf_launch_load(A, prim_ws, c->d_err, st), "k_load_prims");
+    uint8_t* gptr = (uint8_t*)prim_ws + align256(sizeof(GPrim) * (size_t)std::max<int64_t>(n, 1));
+    GF_CUDA(c, gf_launch_load(A, prim_ws, gptr, c->d_err, st), "k_load_prims");
     uint32_t herr[4];
     GF_CUDA(c, cudaMemcpyAsync(herr, c->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st), "memcpy");
     GF_CUDA(c, cudaStreamSynchronize(st), "load sync");
@@ -237,6 +240,7 @@ gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_p
     for (int i = 0; i < 3 * K; ++i) c->sc.axes[i] = pyr->bin_axes[i];
     for (int g = 0; g < kMaxGroups; ++g) c->sc.f0[g] = (pyr->group_f0 && g < c->sc.G) ? pyr->group_f0[g] : 0.0f;
     c->prims = (GPrim*)prim_ws;
+    c->group = gptr;
     c->dext = make_policy_dev(c->ext, P);
     c->dnee = make_policy_dev(c->nee, P);
     c->loaded = true;
@@ -255,11 +259,14 @@ gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch,
     if (gf_status s = check_sticky(c)) return s;
     cudaStream_t st = (cudaStream_t)stream;
     char* base = (char*)bvh_ws;
+    const size_t n1 = (size_t)std::max<int64_t>(c->n, 1);
     c->sorted = (GPrim*)base;
-    c->nodes = (GNode*)(base + align256(sizeof(GPrim) * (size_t)std::max<int64_t>(c->n, 1)));
+    c->nodes = (GNode*)(base + align256(sizeof(GPrim) * n1));
+    c->perm = (int32_t*)(base + align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1));
     BuildScratch S = gf_scratch_layout(c->n, (char*)scratch);
     uint32_t nn = 0;
-    GF_CUDA(c, gf_launch_build(c->prims, c->n, S, c->nodes, c->sorted, &nn, c->root, st), "gf_build_bvh");
+    GF_CUDA(c, gf_launch_build(c->prims, c->group, c->n, S, c->nodes, c->sorted, c->perm, &nn, c->root, st),
+            "gf_build_bvh");
     c->n_nodes = nn;
     c->built = true;
     return GF_OK;
@@ -291,6 +298,8 @@ static gf_status trace_common(gf_ctx* c, const float* rays, int64_t n, TraceArgs
     A.nodes = c->nodes;
     A.n_nodes = c->built ? c->n_nodes : 0;
     A.prims = brute ? c->prims : c->sorted;
+    A.group = c->group;
+    A.perm = c->perm;
     A.n_prims = c->n;
     A.pol = c->dext;
     A.sc = c->sc;

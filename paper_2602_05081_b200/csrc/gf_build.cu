@@ -38,7 +38,7 @@ __device__ int derive_bin(const float* q, const float* sc, int K, const float* a
     return best;
 }
 
-__global__ void k_load_prims(LoadArgs A, GPrim* out, uint32_t* err) {
+__global__ void k_load_prims(LoadArgs A, GPrim* out, uint8_t* gout, uint32_t* err) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.n) return;
     const float* q = A.quat + 4 * i;
@@ -89,12 +89,14 @@ __global__ void k_load_prims(LoadArgs A, GPrim* out, uint32_t* err) {
                   2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
     float is0 = 1.0f / sc[0], is1 = 1.0f / sc[1], is2 = 1.0f / sc[2];
     double coef = (double)alpha / (2.0 * 3.14159265358979323846 * (double)sc[0] * (double)sc[1] * (double)sc[2]);
+    const float Rs = E * smax * 1.00001f + 1e-7f;  // world bounding sphere of the ellipsoid
     GPrim P;
-    P.a = make_float4(mx, my, mz, (float)coef);
+    P.a = make_float4(mx, my, mz, Rs * Rs);
     P.b = make_float4(R[0] * is0, R[3] * is0, R[6] * is0, om);
     P.c = make_float4(R[1] * is1, R[4] * is1, R[7] * is1, E * E);
-    P.d = make_float4(R[2] * is2, R[5] * is2, R[8] * is2, __uint_as_float(((uint32_t)i << 5) | (uint32_t)group));
+    P.d = make_float4(R[2] * is2, R[5] * is2, R[8] * is2, (float)coef);
     out[i] = P;
+    gout[i] = (uint8_t)group;
 }
 
 // ---------------------------------------------------------------------------------- build
@@ -141,7 +143,8 @@ __device__ __forceinline__ uint64_t expand3(uint32_t x) {
     return v;
 }
 
-__global__ void k_keys(const GPrim* prims, int64_t n, const uint32_t* cbounds, uint64_t* keys, uint32_t* vals) {
+__global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, const uint32_t* cbounds, uint64_t* keys,
+                       uint32_t* vals) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     GPrim P = prims[i];
@@ -155,7 +158,7 @@ __global__ void k_keys(const GPrim* prims, int64_t n, const uint32_t* cbounds, u
         t = fminf(fmaxf(t, 0.0f), 1.0f);
         q[k] = min((uint32_t)(t * 524288.0f), 524287u);  // 19 bits
     }
-    uint32_t group = __float_as_uint(P.d.w) & 31u;
+    uint32_t group = groups[i];
     keys[i] = ((uint64_t)group << 57) | (expand3(q[0]) << 2) | (expand3(q[1]) << 1) | expand3(q[2]);
     vals[i] = (uint32_t)i;
 }
@@ -200,7 +203,7 @@ struct RefitArgs {
     int64_t n;
     const int32_t *left, *right, *parent, *perm;
     const float* pbox;     // per original prim, 6 floats
-    const GPrim* prims;    // original order
+    const uint8_t* group;  // original order
     float* nbox;           // 2n-1 nodes x 6
     uint32_t *nmask, *ncount, *nsize;
     uint32_t* flags;
@@ -217,7 +220,7 @@ __global__ void k_refit(RefitArgs A) {
     int32_t pi = A.perm[k];
     const float* pb = A.pbox + 6 * (int64_t)pi;
     for (int c = 0; c < 6; ++c) A.nbox[6 * x + c] = pb[c];
-    A.nmask[x] = 1u << (__float_as_uint(A.prims[pi].d.w) & 31u);
+    A.nmask[x] = 1u << A.group[pi];
     A.ncount[x] = 1;
     A.nsize[x] = 1;
     __threadfence();
@@ -286,10 +289,11 @@ __global__ void k_layout(LayoutArgs A) {
     A.out[idx] = N;
 }
 
-__global__ void k_gather(const GPrim* in, const int32_t* perm, int64_t n, GPrim* out) {
+__global__ void k_gather(const GPrim* in, const int32_t* perm, int64_t n, GPrim* out, int32_t* perm_out) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     out[k] = in[perm[k]];
+    perm_out[k] = perm[k];
 }
 
 }  // namespace gfk
@@ -299,9 +303,9 @@ using namespace gfk;
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint32_t* err, cudaStream_t st) {
+cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, cudaStream_t st) {
     if (A.n == 0) return cudaSuccess;
-    k_load_prims<<<nblk(A.n, 256), 256, 0, st>>>(A, (GPrim*)out, err);
+    k_load_prims<<<nblk(A.n, 256), 256, 0, st>>>(A, (GPrim*)out, group, err);
     return cudaGetLastError();
 }
 
@@ -341,8 +345,8 @@ BuildScratch gf_scratch_layout(int64_t n, char* base) {
 }
 
 // builds into nodes/sorted; returns node count via *n_nodes (host, after sync)
-cudaError_t gf_launch_build(const void* prims_v, int64_t n, const BuildScratch& S, void* nodes_v, void* sorted_v,
-                            uint32_t* n_nodes, float* root_box, cudaStream_t st) {
+cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes_v,
+                            void* sorted_v, int32_t* perm, uint32_t* n_nodes, float* root_box, cudaStream_t st) {
     const GPrim* prims = (const GPrim*)prims_v;
     GNode* nodes = (GNode*)nodes_v;
     cudaError_t e;
@@ -351,7 +355,7 @@ cudaError_t gf_launch_build(const void* prims_v, int64_t n, const BuildScratch& 
     uint32_t init[8] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u, 0u};
     if ((e = cudaMemcpyAsync(S.cbounds, init, sizeof(init), cudaMemcpyHostToDevice, st))) return e;
     k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds);
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.cbounds, S.keys_in, S.vals_in);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in);
     size_t tb = S.sort_temp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
                                              0, 64, st)))
@@ -360,7 +364,7 @@ cudaError_t gf_launch_build(const void* prims_v, int64_t n, const BuildScratch& 
         k_karras<<<nblk(n - 1, 256), 256, 0, st>>>(S.keys_out, n, S.left, S.right, S.parent, S.rlo, S.rhi);
         if ((e = cudaMemsetAsync(S.flags, 0, sizeof(uint32_t) * n, st))) return e;
     }
-    RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, prims, S.nbox, S.nmask, S.ncount,
+    RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, group, S.nbox, S.nmask, S.ncount,
                 S.nsize, S.flags};
     k_refit<<<nblk(n, 256), 256, 0, st>>>(R);
     // root (node 0 = internal root, or leaf 0 when n == 1 stored at n-1+0 = 0)
@@ -369,7 +373,7 @@ cudaError_t gf_launch_build(const void* prims_v, int64_t n, const BuildScratch& 
     if ((e = cudaStreamSynchronize(st))) return e;
     LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, total};
     k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
-    k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v);
+    k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
     if ((e = cudaMemcpyAsync(root_box, S.nbox, sizeof(float) * 6, cudaMemcpyDeviceToHost, st))) return e;
     if ((e = cudaStreamSynchronize(st))) return e;
     *n_nodes = total;

@@ -1,9 +1,10 @@
 // gf_device.cuh -- device-side building blocks of the Gabor Fields hot path (sm_100a).
 //
 // Data layout in HBM:
-//   GPrim  64 B  = 4 x float4 : (mu.xyz, c) (W row0, omega) (W row1, E^2) (W row2, idx<<5|group)
+//   GPrim  64 B  = 4 x float4 : (mu.xyz, Rs^2) (W row0, omega) (W row1, E^2) (W row2, c)
 //          with W = S^-1 R^T (PCA whitening, reading C1), c = alpha / (2 pi s1 s2 s3),
-//          k_W = (omega, omega, omega) implicit (reading C2).
+//          k_W = (omega, omega, omega) implicit (reading C2), Rs = E s_max the world bounding
+//          sphere (one 16-byte load pre-test); the group lives in the leaf (and a side array).
 //   GNode  32 B  = 2 x float4 : (lo.xyz, skip | leaf<<31) (hi.xyz, info)
 //          depth-first layout, hit -> i+1, miss -> skip; info = group mask (internal) or
 //          first<<8 | count<<5 | group (leaf).
@@ -265,6 +266,21 @@ __device__ __forceinline__ bool slab_range(const RayDev& r, float4 lo, float4 hi
     return tn <= tf;
 }
 
+// ------------------------------------------------------------------ a5: bounding-sphere pre-test
+// Conservative world-space test of the ray against the primitive's bounding sphere (mu, Rs):
+// one 16-byte load rejects most leaf candidates before the whitened setup.  Margins cover the
+// fp32 rounding of |D|^2 - (D.d)^2 so that no primitive accepted by prim_setup is rejected.
+__device__ __forceinline__ bool sphere_pretest(float4 a, const RayDev& r, float t0, float t1) {
+    const float dx = r.o.x - a.x, dy = r.o.y - a.y, dz = r.o.z - a.z;
+    const float b = fmaf(dx, r.d.x, fmaf(dy, r.d.y, dz * r.d.z));
+    const float c = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float perp2 = fmaf(-b, b, c);
+    const float slack = 1e-4f * a.w + 1e-6f * c;
+    if (perp2 > a.w + slack) return false;
+    const float h = sqrtf(fmaxf(a.w + slack - perp2, 0.0f)) * 1.0001f + 1e-6f * fabsf(b);
+    return (-b - h <= t1) && (-b + h >= t0);
+}
+
 // ------------------------------------------------------------------ a5: whitened setup + predicate
 // Per (ray, primitive): world offset re-centred at the ray's closest approach to mu with an
 // error-free TwoSum (o - mu = hi + lo), so that far origins (|o-mu|/s up to 3000) keep fp32
@@ -441,11 +457,133 @@ __device__ inline float seg_J(const Setup& s, float ua, float ub, Work& wk) {
 
 // contribution of a hit over its clipped chord: c/j * Jw
 __device__ __forceinline__ float hit_tau(const GPrim& P, const Setup& s, Work& wk) {
-    return P.a.w * s.ij * seg_J(s, s.u0, s.u1, wk);
+    return P.d.w * s.ij * seg_J(s, s.u0, s.u1, wk);
 }
 
 __device__ __forceinline__ uint32_t node_mask(uint32_t skipw, uint32_t info) {
     return (skipw & kLeafBit) ? (1u << (info & 31u)) : info;
+}
+
+// ------------------------------------------------------------------ flat warp traversal engine
+// One traversal step = one node test or one primitive test (a4 + a5).  State of a ray's
+// stackless depth-first traversal: next node i, leaf cursor [lk, le) and the leaf's group g.
+// A second (postponed) leaf slot lets a lane keep taking node steps while it still has an
+// unprocessed leaf, so node steps and primitive tests each run with most lanes of the warp.
+struct Trav {
+    RayDev r;
+    float t0, t1;
+    uint32_t mask, i, lk, le, g, lk2, le2, g2;
+};
+__device__ __forceinline__ void trav_begin(Trav& T, const RayDev& r, float t0, float t1, uint32_t mask) {
+    T.r = r; T.t0 = t0; T.t1 = t1; T.mask = mask; T.i = 0; T.lk = 0; T.le = 0; T.g = 0;
+    T.lk2 = 0; T.le2 = 0; T.g2 = 0;
+}
+__device__ __forceinline__ bool trav_done(const Trav& T, uint32_t n_nodes) {
+    return T.lk >= T.le && T.lk2 >= T.le2 && T.i >= n_nodes;
+}
+
+// Persistent warp loop over `count` work items (all 32 lanes call it).  Each lane owns one ray;
+// a lane whose ray is finished fetches the next item at once (lane-level refill).  Every
+// iteration the warp executes ONE uniform operation for the lanes eligible for it:
+//   NODE  lanes with no unprocessed leaf: one node test (a4);
+//   PRIM  lanes inside a leaf without a pending hit: one primitive test (a5);
+//   HIT   lanes with a pending accepted primitive: its fused integral (a6), batched so that the
+//         expensive erf work runs once BATCH lanes have one (or nothing else can advance).
+// The op with the most eligible lanes wins, so node/prim/integral code never diverge against
+// each other.  Callbacks (lane-local): begin(idx) -> bool (false: item needs no traversal);
+// hit(setup, coef, group, sorted prim index); end().  sync() is called by all lanes once per iteration.
+template <bool COUNT, int BATCH, class Begin, class Hit, class End, class Sync>
+__device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const GNode* __restrict__ nodes,
+                                          uint32_t n_nodes, const GPrim* __restrict__ prims, Trav& T, Work& wk,
+                                          Begin&& begin, Hit&& hit, End&& end, Sync&& sync) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    bool active = false, pend = false, exhausted = false;
+    Setup s;
+    float coef = 0.0f;
+    uint32_t pg = 0, pidx = 0;
+    while (true) {
+        // finish + refill
+        if (active && !pend && trav_done(T, n_nodes)) {
+            end();
+            active = false;
+        }
+        if (!exhausted) {
+            const unsigned need = __ballot_sync(FULL, !active);
+            if (need) {
+                const int leader = __ffs(need) - 1;
+                uint32_t base = 0;
+                if (lane == leader) base = atomicAdd(work, (uint32_t)__popc(need));
+                base = __shfl_sync(FULL, base, leader);
+                if (!active) {
+                    const uint32_t idx = base + __popc(need & ((1u << lane) - 1u));
+                    if (idx < count) active = begin(idx);
+                }
+                if (base + (uint32_t)__popc(need) >= count) exhausted = true;
+            }
+        }
+        sync();
+        if (!__any_sync(FULL, active)) {
+            if (exhausted) break;
+            continue;
+        }
+        // inner loop of uniform operations until some lane finishes its ray
+        while (true) {
+            const bool in_leaf = active && T.lk < T.le;
+            const bool e_node = active && T.i < n_nodes && (!in_leaf || T.lk2 >= T.le2);
+            const bool e_prim = in_leaf && !pend;
+            const unsigned m_hit = __ballot_sync(FULL, pend);
+            const unsigned m_node = __ballot_sync(FULL, e_node);
+            const unsigned m_prim = __ballot_sync(FULL, e_prim);
+            const int n_hit = __popc(m_hit), n_node = __popc(m_node), n_prim = __popc(m_prim);
+            if (n_hit > 0 && (n_hit >= BATCH || n_hit >= n_node + n_prim)) {
+                if (pend) {
+                    hit(s, coef, pg, pidx);
+                    pend = false;
+                }
+            } else if (n_prim > 0 && n_prim >= n_node) {
+                if (e_prim) {
+                    const uint32_t k = T.lk, g = T.g;
+                    const GPrim* q = prims + k;
+                    ++T.lk;
+                    if (T.lk >= T.le && T.lk2 < T.le2) {  // promote the postponed leaf
+                        T.lk = T.lk2; T.le = T.le2; T.g = T.g2; T.lk2 = T.le2 = 0;
+                    }
+                    GPrim P;
+                    P.a = __ldg(&q->a);
+                    if (COUNT) ++wk.tests;
+                    if (sphere_pretest(P.a, T.r, T.t0, T.t1)) {
+                        P.b = __ldg(&q->b); P.c = __ldg(&q->c); P.d = __ldg(&q->d);
+                        if (prim_setup(P, T.r, T.t0, T.t1, s)) {
+                            if (COUNT) ++wk.hits;
+                            coef = P.d.w;
+                            pg = g;
+                            pidx = k;
+                            pend = true;
+                        }
+                    }
+                }
+            } else if (n_node > 0) {
+                if (e_node) {
+                    const uint32_t i = T.i;
+                    const float4 lo = __ldg(&nodes[i].lo), hi = __ldg(&nodes[i].hi);
+                    const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+                    if (COUNT) ++wk.nodes;
+                    const bool h = (node_mask(sk, info) & T.mask) && slab(T.r, lo, hi, T.t0, T.t1);
+                    if (h && (sk & kLeafBit)) {
+                        const uint32_t lk = info >> 8, le = lk + ((info >> 5) & 7u), g = info & 31u;
+                        if (T.lk >= T.le) { T.lk = lk; T.le = le; T.g = g; }
+                        else { T.lk2 = lk; T.le2 = le; T.g2 = g; }
+                        T.i = sk & ~kLeafBit;
+                    } else {
+                        T.i = h ? i + 1 : (sk & ~kLeafBit);
+                    }
+                }
+            }
+            // leave the inner loop when a lane can be finished (its slot is refilled)
+            if (__any_sync(FULL, active && !pend && trav_done(T, n_nodes))) break;
+        }
+    }
 }
 
 }  // namespace gfk

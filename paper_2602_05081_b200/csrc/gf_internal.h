@@ -33,6 +33,8 @@ struct TraceArgs {
     const gfk::GNode* nodes;
     uint32_t n_nodes;
     const gfk::GPrim* prims;  // BVH order (sorted) or input order (brute force)
+    const uint8_t* group;     // input-order group ids (brute force)
+    const int32_t* perm;      // sorted -> input index (candidates)
     int64_t n_prims;
     gfk::PolicyDev pol;
     gfk::SceneDev sc;
@@ -88,6 +90,9 @@ struct RenderDev {
     double* cum;  // 3 n: tau before the bracketing bin, tau*, tau in the bin
     int32_t* bin;
     uint32_t* pix;
+    uint32_t* nhit;  // hits recorded by ffA
+    uint2* hits;     // [hit_cap][n_paths]: sorted prim index | group << 24, bin span ka | kb << 8
+    int32_t hit_cap;
     // queues
     uint32_t *qA, *qB, *qNext;
     uint32_t* qcount;  // [4]: A, B, next, overflow
@@ -96,11 +101,11 @@ struct RenderDev {
     unsigned long long* work;  // gf_stats work counters (counting variant) or null
 };
 
-cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint32_t* err, cudaStream_t st);
+cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, cudaStream_t st);
 size_t gf_sort_temp_bytes(int64_t n);
 BuildScratch gf_scratch_layout(int64_t n, char* base);
-cudaError_t gf_launch_build(const void* prims, int64_t n, const BuildScratch& S, void* nodes, void* sorted,
-                            uint32_t* n_nodes, float* root_box, cudaStream_t st);
+cudaError_t gf_launch_build(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes,
+                            void* sorted, int32_t* perm, uint32_t* n_nodes, float* root_box, cudaStream_t st);
 cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
 cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
 size_t gf_render_state_bytes(int64_t n_paths, char* base, RenderDev* R);

@@ -16,7 +16,8 @@
 namespace gfk {
 
 constexpr int kBins = 32;
-constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6;
+constexpr int kHitCap = 1024;  // hits recorded per path by ffA for ffB (overflow -> traversal gather)
+constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6, kWorkT = 7;
 
 template <bool COUNT, class F>
 __device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint32_t n_nodes,
@@ -34,8 +35,10 @@ __device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint
             for (uint32_t k = 0; k < cnt; ++k) {
                 const GPrim* p = prims + first + k;
                 GPrim P;
-                P.a = __ldg(&p->a); P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
+                P.a = __ldg(&p->a);
                 if (COUNT) ++wk.tests;
+                if (!sphere_pretest(P.a, r, t0, t1)) continue;
+                P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
                 f(P, g);
             }
             i = sk & ~kLeafBit;
@@ -126,34 +129,52 @@ __global__ void __launch_bounds__(128) k_gen(RenderDev R, int32_t sample) {
     push(R.qA, R.qcount + 0, ok, (uint32_t)p);
 }
 
-template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int32_t pix = p < R.n_paths ? path_pixel(R, p) : -1;
-    Work wk;
-    if (pix >= 0) {
-        float jx = 0.5f, jy = 0.5f;
-        if (R.jitter) {
-            uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
-            jx = u01(b.x); jy = u01(b.y);
-        }
-        float3 o, d;
-        camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
-        float w[kMaxGroups];
-        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_EXT,
-                                                 1, w)
-                                    : R.ext.static_mask;
-        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
-        R.L[p] = (float)trace_tau<STOCH, COUNT>(R, r, 0.0f, INFINITY, mask, w, wk);
-        wk.paths = 1;
+// ---------------------------------------------------------------- binned tau over [t0, t1]
+// Adds one hit's partial integrals into NB equal t-bins (one erf evaluation per bin boundary
+// inside the chord, the chord ends shared) and counts the primitives overlapping each bin.
+// Returns the bin span ka | kb << 8 of the chord.
+template <int NB, bool COUNT>
+__device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, float bw, float ibw, double* bins,
+                                            uint16_t* cnts, Work& wk) {
+    const float ta = fmaf(s.u0 - s.bp, s.ij, s.tc), tb = fmaf(s.u1 - s.bp, s.ij, s.tc);
+    const int ka = min(NB - 1, max(0, (int)((ta - t0) * ibw)));
+    const int kb = min(NB - 1, max(0, (int)((tb - t0) * ibw)));
+    const uint32_t span = (uint32_t)ka | ((uint32_t)kb << 8);
+    for (int m = ka; m <= kb; ++m) cnts[m] = (uint16_t)min(65535, cnts[m] + 1);
+    if (ka == kb) {
+        bins[ka] += (double)(cj * seg_J(s, s.u0, s.u1, wk));
+        return span;
     }
-    count_rays(R.rays + 0, pix >= 0);
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
+    const float wmax = 0.5f * (fmaxf(s.u0 * s.u0, s.u1 * s.u1) + s.Om * s.Om);
+    float ua = s.u0;
+    if ((wmax > kWMaxSeries && s.Om != 0.0f) || s.u1 - s.u0 < 1e-4f) {  // per-piece generic path
+        for (int m = ka + 1; m <= kb; ++m) {
+            float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
+            bins[m - 1] += (double)(cj * seg_J(s, ua, ub, wk));
+            ua = ub;
+        }
+        bins[kb] += (double)(cj * seg_J(s, ua, s.u1, wk));
+        return span;
+    }
+    // shared endpoints: one erf evaluation per bin boundary inside the chord
+    float sp, cp;
+    sincos_red(s.phi0, &sp, &cp);
+    const float amp = cj * 0.5f * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+    float2 Fa = erf_shift(ua, s.Om);
+    for (int m = ka + 1; m <= kb; ++m) {
+        float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
+        float2 Fb = erf_shift(ub, s.Om);
+        bins[m - 1] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
+        Fa = Fb;
+        ua = ub;
+    }
+    float2 Fb = erf_shift(s.u1, s.Om);
+    bins[kb] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
+    if (COUNT) wk.erf(s.Om, (uint32_t)(kb - ka + 2));
+    return span;
 }
 
-// ---------------------------------------------------------------- binned tau over [t0, t1]
-// Adds each hit's partial integrals into NB equal t-bins (one erf evaluation per bin boundary
-// inside the chord, the chord ends shared) and counts the primitives overlapping each bin.
+// full-ray binned pass (used by the ffB overflow fallback)
 template <int NB, bool STOCH, bool COUNT>
 __device__ __forceinline__ void bin_pass(const RenderDev& R, const RayDev& r, uint32_t mask, const float* w,
                                          float t0, float t1, double* bins, uint16_t* cnts, Work& wk) {
@@ -164,97 +185,133 @@ __device__ __forceinline__ void bin_pass(const RenderDev& R, const RayDev& r, ui
         Setup s;
         if (!prim_setup(P, r, t0, t1, s)) return;
         if (COUNT) ++wk.hits;
-        float cj = P.a.w * s.ij;
+        float cj = P.d.w * s.ij;
         if (STOCH) cj *= w[g];
-        const float ta = fmaf(s.u0 - s.bp, s.ij, s.tc), tb = fmaf(s.u1 - s.bp, s.ij, s.tc);
-        const int ka = min(NB - 1, max(0, (int)((ta - t0) * ibw)));
-        const int kb = min(NB - 1, max(0, (int)((tb - t0) * ibw)));
-        for (int m = ka; m <= kb; ++m) cnts[m] = (uint16_t)min(65535, cnts[m] + 1);
-        if (ka == kb) {
-            bins[ka] += (double)(cj * seg_J(s, s.u0, s.u1, wk));
-            return;
-        }
-        const float wmax = 0.5f * (fmaxf(s.u0 * s.u0, s.u1 * s.u1) + s.Om * s.Om);
-        float ua = s.u0;
-        if (wmax > kWMaxSeries || s.u1 - s.u0 < 1e-4f) {  // per-piece generic path
-            for (int m = ka + 1; m <= kb; ++m) {
-                float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
-                bins[m - 1] += (double)(cj * seg_J(s, ua, ub, wk));
-                ua = ub;
-            }
-            bins[kb] += (double)(cj * seg_J(s, ua, s.u1, wk));
-            return;
-        }
-        // shared endpoints: one erf evaluation per bin boundary inside the chord
-        float sp, cp;
-        sincos_red(s.phi0, &sp, &cp);
-        const float amp = cj * 0.5f * __expf(-0.5f * (s.r2 + s.Om * s.Om));
-        float2 Fa = erf_shift(ua, s.Om);
-        for (int m = ka + 1; m <= kb; ++m) {
-            float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
-            float2 Fb = erf_shift(ub, s.Om);
-            bins[m - 1] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
-            Fa = Fb;
-            ua = ub;
-        }
-        float2 Fb = erf_shift(s.u1, s.Om);
-        bins[kb] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
-        if (COUNT) wk.erf(s.Om, (uint32_t)(kb - ka + 2));
+        bin_add<NB, COUNT>(s, cj, t0, bw, ibw, bins, cnts, wk);
     });
+}
+
+constexpr int kBatch = 24;  // integrate pending hits once this many lanes (or most blocked lanes) have one
+
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
+    Work wk;
+    Trav T;
+    uint32_t p = 0;
+    double tau = 0.0;
+    float w[kMaxGroups];
+    bool began = false;
+    flat_loop<COUNT, kBatch>(
+        R.qcount + kWorkT, (uint32_t)R.n_paths, R.nodes, R.n_nodes, R.prims, T, wk,
+        [&](uint32_t idx) -> bool {
+            p = idx;
+            const int32_t pix = path_pixel(R, p);
+            if (pix < 0) return false;
+            float jx = 0.5f, jy = 0.5f;
+            if (R.jitter) {
+                uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
+                jx = u01(b.x); jy = u01(b.y);
+            }
+            float3 o, d;
+            camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0,
+                                                     ST_EXT, 1, w)
+                                        : R.ext.static_mask;
+            trav_begin(T, make_ray(o, d, 0.0f, INFINITY), 0.0f, INFINITY, mask);
+            tau = 0.0;
+            began = true;
+            if (COUNT) ++wk.paths;
+            return true;
+        },
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
+            float c = coef * s.ij * seg_J(s, s.u0, s.u1, wk);
+            if (STOCH) c *= w[g];
+            tau += (double)c;
+        },
+        [&]() { R.L[p] = (float)tau; },
+        [&]() { count_rays(R.rays + 0, began); began = false; });
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
 }
 
 // ---------------------------------------------------------------- ffA: binned tau over the ray
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_t depth) {
-    const uint32_t count = R.qcount[0];
-    uint32_t base;
     Work wk;
-    while (fetch(R.qcount + kWorkA, count, base)) {
-        const uint32_t idx = base + (threadIdx.x & 31);
-        const bool active = idx < count;
-        uint32_t p = active ? R.qA[idx] : 0;
-        bool collide = false;
-        if (active) {
+    Trav T;
+    uint32_t p = 0;
+    double tstar = 0.0;
+    float tlo = 0.0f, bw = 0.0f, ibw = 0.0f;
+    double bins[kBins];
+    uint16_t cnts[kBins];
+    float w[kMaxGroups];
+    bool began = false, fin = false, collide = false;
+    uint32_t fin_p = 0, nh = 0;
+    auto finish = [&](int32_t bin, double cum_before, double bin_tau, int32_t nact) {
+        if (bin == -2) {
+            R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+            collide = false;
+        } else {
+            R.bin[p] = bin < 0 ? bin : (bin | (nact << 16));
+            R.cum[p] = cum_before;               // tau before the bracketing bin
+            R.cum[p + R.n_paths] = tstar;        // tau*
+            R.cum[p + 2 * R.n_paths] = bin_tau;  // tau inside the bin
+            R.nhit[p] = nh;
+            collide = true;
+        }
+        fin = true;
+        fin_p = p;
+    };
+    flat_loop<COUNT, kBatch>(
+        R.qcount + kWorkA, R.qcount[0], R.nodes, R.n_nodes, R.prims, T, wk,
+        [&](uint32_t idx) -> bool {
+            p = R.qA[idx];
+            began = true;
             if (COUNT) ++wk.paths;
             const uint32_t pix = R.pix[p];
             const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
-            float w[kMaxGroups];
             const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                      ST_EXT, 1, w)
                                         : R.ext.static_mask;
             const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
-            const double tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
+            tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
+            if (tstar <= 0.0) { finish(-1, 0.0, 0.0, 0); return false; }
             const RayDev r = make_ray(o, d, 0.0f, INFINITY);
-            float tlo, thi;
-            int32_t bin = -2;  // -2 escape, -1 collide at t_min, >= 0 bracketing bin
-            double cum_before = 0.0, bin_tau = 0.0;
-            int32_t nact = 0;
-            if (tstar <= 0.0) {
-                bin = -1;
-            } else if (R.n_nodes > 0 && slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
-                double bins[kBins];
-                uint16_t cnts[kBins];
-                bin_pass<kBins, STOCH, COUNT>(R, r, mask, w, tlo, thi, bins, cnts, wk);
-                double cum = 0.0;
-                for (int k = 0; k < kBins; ++k) {
-                    const double c2 = cum + bins[k];
-                    if (c2 >= tstar) { bin = k; cum_before = cum; bin_tau = bins[k]; nact = cnts[k]; break; }
-                    cum = c2;
-                }
+            float thi;
+            if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
+                finish(-2, 0.0, 0.0, 0);
+                return false;
             }
-            if (bin == -2) {
-                R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
-            } else {
-                R.bin[p] = bin < 0 ? bin : (bin | (nact << 16));
-                R.cum[p] = cum_before;               // tau before the bracketing bin
-                R.cum[p + R.n_paths] = tstar;        // tau*
-                R.cum[p + 2 * R.n_paths] = bin_tau;  // tau inside the bin
-                collide = true;
+            bw = (thi - tlo) * (1.0f / kBins);
+            ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
+            nh = 0;
+#pragma unroll
+            for (int k = 0; k < kBins; ++k) { bins[k] = 0.0; cnts[k] = 0; }
+            trav_begin(T, r, tlo, thi, mask);
+            return true;
+        },
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
+            float cj = coef * s.ij;
+            if (STOCH) cj *= w[g];
+            const uint32_t span = bin_add<kBins, COUNT>(s, cj, tlo, bw, ibw, bins, cnts, wk);
+            // hit list for ffB: (sorted primitive index | group << 24, bin span), layout [k][path]
+            if (nh < (uint32_t)R.hit_cap) R.hits[(size_t)nh * R.n_paths + p] = make_uint2(k | (g << 24), span);
+            ++nh;
+        },
+        [&]() {
+            double cum = 0.0;
+            for (int k = 0; k < kBins; ++k) {
+                const double c2 = cum + bins[k];
+                if (c2 >= tstar) { finish(k, cum, bins[k], cnts[k]); return; }
+                cum = c2;
             }
-        }
-        push(R.qB, R.qcount + 1, active && collide, p);
-        count_rays(R.rays + 0, active);
-    }
+            finish(-2, 0.0, 0.0, 0);
+        },
+        [&]() {
+            push(R.qB, R.qcount + 1, fin && collide, fin_p);
+            count_rays(R.rays + 0, began);
+            fin = false;
+            began = false;
+        });
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
 }
 
@@ -262,7 +319,7 @@ __global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_
 // Active primitives of the bracket, split into Gaussians (Omega == 0: real erf, 8 floats) and
 // Gabors (complex erf, 13 floats); kept in local memory.  Inside the bunny-like scenes the
 // overlap depth of the level-0 Gaussians is ~150, hence the large Gaussian list.
-constexpr int kCapG = 224, kCapB = 64;
+constexpr int kCapG = 448, kCapB = 96;
 struct ActG {
     float amp, kap0, j, tc, bp, u0, u1, F0;
 };
@@ -333,11 +390,11 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
             ActG ag[kCapG];
             ActB ab[kCapB];
             int ng = 0, nb = 0;
-            traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, ta, tb, mask, wk, [&](const GPrim& P, uint32_t g) {
+            auto gather = [&](const GPrim& P, uint32_t g) {
                 Setup s;
                 if (!prim_setup(P, r, ta, tb, s)) return;
                 if (COUNT) ++wk.hits;
-                float cj = P.a.w * s.ij;
+                float cj = P.d.w * s.ij;
                 if (STOCH) cj *= w[g];
                 const float kap0 = cj * s.j * kInvSqrt2Pi * __expf(-0.5f * s.r2);
                 if (s.Om == 0.0f) {
@@ -360,7 +417,21 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
                     }
                     ++nb;
                 }
-            });
+            };
+            const uint32_t nh = R.nhit[p];
+            if (nh <= (uint32_t)R.hit_cap) {  // scan the path's hit list from ffA (no traversal)
+                for (uint32_t k = 0; k < nh; ++k) {
+                    const uint2 e = R.hits[(size_t)k * R.n_paths + p];
+                    if ((int)(e.y & 0xFFu) > bin || (int)(e.y >> 8) < bin) continue;
+                    const GPrim* q = R.prims + (e.x & 0xFFFFFFu);
+                    GPrim P;
+                    P.a = __ldg(&q->a); P.b = __ldg(&q->b); P.c = __ldg(&q->c); P.d = __ldg(&q->d);
+                    if (COUNT) ++wk.tests;
+                    gather(P, e.x >> 24);  // (hits already passed the predicate on the full ray)
+                }
+            } else {
+                traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, ta, tb, mask, wk, gather);
+            }
             const bool overflow = ng > kCapG || nb > kCapB;
             if (COUNT && overflow) ++wk.overflow;
             auto eval = [&](float t, double& kap) -> double {
@@ -370,9 +441,33 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
                 if (!overflow) {
                     for (int k = 0; k < ng; ++k) acc += actg_tau(ag[k], t, kap, wk);
                     for (int k = 0; k < nb; ++k) acc += actb_tau(ab[k], t, kap, wk);
-                } else {  // overflow: re-traverse [ta, t]; bisection only
-                    acc += trace_tau<STOCH, COUNT>(R, r, ta, t, mask, w, wk);
-                    kap = 0.0;
+                } else {  // list overflow: stream the bracket's primitives again (hit list or traversal)
+                    auto one = [&](const GPrim& P, uint32_t g) {
+                        Setup s;
+                        if (!prim_setup(P, r, ta, tb, s)) return;
+                        float cj = P.d.w * s.ij;
+                        if (STOCH) cj *= w[g];
+                        const float ut = fmaf(s.j, t - s.tc, s.bp);
+                        if (!(ut > s.u0)) return;
+                        if (ut < s.u1) {
+                            float sp, cp;
+                            sincos_red(fmaf(s.Om, ut, s.phi0), &sp, &cp);
+                            kap += (double)(cj * s.j * kInvSqrt2Pi * __expf(-0.5f * (s.r2 + ut * ut)) * cp);
+                        }
+                        acc += (double)(cj * seg_J(s, s.u0, fminf(ut, s.u1), wk));
+                    };
+                    if (nh <= (uint32_t)R.hit_cap) {
+                        for (uint32_t k = 0; k < nh; ++k) {
+                            const uint2 e = R.hits[(size_t)k * R.n_paths + p];
+                            if ((int)(e.y & 0xFFu) > bin || (int)(e.y >> 8) < bin) continue;
+                            const GPrim* q = R.prims + (e.x & 0xFFFFFFu);
+                            GPrim P;
+                            P.a = __ldg(&q->a); P.b = __ldg(&q->b); P.c = __ldg(&q->c); P.d = __ldg(&q->d);
+                            one(P, e.x >> 24);
+                        }
+                    } else {
+                        traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, ta, tb, mask, wk, one);
+                    }
                 }
                 return acc;
             };
@@ -387,10 +482,13 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
                 const double f = eval(t, kap);
                 if (f >= 0.0) hi = t; else lo = t;
                 if (!(hi - lo > 1e-6f * bw)) break;
+                if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
                 float tn = (kap > 0.0) ? (float)((double)t - f / kap) : 0.5f * (lo + hi);
-                if (!(tn > lo && tn < hi)) tn = 0.5f * (lo + hi);
-                if (fabsf(tn - t) <= 1e-7f * bw) { t = tn; break; }
+                const bool newton = tn > lo && tn < hi;
+                if (!newton) tn = 0.5f * (lo + hi);
+                const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
                 t = tn;
+                if (small) break;
             }
             tres = t;
         }
@@ -405,23 +503,35 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
 // ---------------------------------------------------------------- NEE + phase sampling
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128) k_nee(RenderDev R, int32_t sample, int32_t depth) {
-    const uint32_t count = R.qcount[1];
-    uint32_t base;
     Work wk;
-    while (fetch(R.qcount + kWorkN, count, base)) {
-        const uint32_t idx = base + (threadIdx.x & 31);
-        const bool active = idx < count;
-        uint32_t p = active ? R.qB[idx] : 0;
-        bool cont = false;
-        if (active) {
-            const uint32_t pix = R.pix[p];
-            const float3 x = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
-            float w[kMaxGroups];
+    Trav T;
+    uint32_t p = 0, pix = 0;
+    double tau = 0.0;
+    float w[kMaxGroups];
+    bool began = false, cont = false;
+    uint32_t fin_p = 0;
+    flat_loop<COUNT, kBatch>(
+        R.qcount + kWorkN, R.qcount[1], R.nodes, R.n_nodes, R.prims, T, wk,
+        [&](uint32_t idx) -> bool {
+            p = R.qB[idx];
+            pix = R.pix[p];
+            began = true;
+            if (COUNT) ++wk.paths;
+            const float3 x = ld3(R.ox, R.oy, R.oz, p);
             const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample,
                                                      (uint32_t)depth, ST_NEE, 0, w)
                                         : R.nee.static_mask;
-            const RayDev r = make_ray(x, R.sun, 0.0f, INFINITY);
-            const double tau = trace_tau<STOCH, COUNT>(R, r, 0.0f, INFINITY, mask, w, wk);
+            trav_begin(T, make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask);
+            tau = 0.0;
+            return true;
+        },
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
+            float c = coef * s.ij * seg_J(s, s.u0, s.u1, wk);
+            if (STOCH) c *= w[g];
+            tau += (double)c;
+        },
+        [&]() {
+            const float3 d = ld3(R.dx, R.dy, R.dz, p);
             const float beta = R.beta[p];
             const float cost = d.x * R.sun.x + d.y * R.sun.y + d.z * R.sun.z;
             R.L[p] += beta * R.albedo * hg_eval(R.hg_g, cost) * (float)exp(-tau) * R.sun_E;
@@ -431,11 +541,15 @@ __global__ void __launch_bounds__(128) k_nee(RenderDev R, int32_t sample, int32_
                 R.dx[p] = nd.x; R.dy[p] = nd.y; R.dz[p] = nd.z;
                 R.beta[p] = beta * R.albedo;
                 cont = true;
+                fin_p = p;
             }
-        }
-        push(R.qNext, R.qcount + 2, active && cont, p);
-        count_rays(R.rays + 1, active);
-    }
+        },
+        [&]() {
+            push(R.qNext, R.qcount + 2, cont, fin_p);
+            count_rays(R.rays + 1, began);
+            cont = false;
+            began = false;
+        });
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
 }
 
@@ -471,12 +585,13 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     float* dx = (float*)take(nf); float* dy = (float*)take(nf); float* dz = (float*)take(nf);
     float* beta = (float*)take(nf); float* L = (float*)take(nf);
     double* cum = (double*)take(sizeof(double) * 3 * (size_t)n);
-    int32_t* bin = (int32_t*)take(nu); uint32_t* pix = (uint32_t*)take(nu);
+    int32_t* bin = (int32_t*)take(nu); uint32_t* pix = (uint32_t*)take(nu); uint32_t* nhit = (uint32_t*)take(nu);
+    uint2* hits = (uint2*)take(sizeof(uint2) * (size_t)kHitCap * (size_t)n);
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
     uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
-        R->cum = cum; R->bin = bin; R->pix = pix;
+        R->cum = cum; R->bin = bin; R->pix = pix; R->nhit = nhit; R->hits = hits; R->hit_cap = kHitCap;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qcount = qc;
     }
     return off;
@@ -519,11 +634,11 @@ cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cu
     if (R.mode == 0) {
         T.pre(STAGE_TOMO, st, ev);
         if (stoch_ext) {
-            if (cnt) k_tomo<true, true><<<grid, 128, 0, st>>>(R, sample);
-            else k_tomo<true, false><<<grid, 128, 0, st>>>(R, sample);
+            if (cnt) k_tomo<true, true><<<pgrid, 128, 0, st>>>(R, sample);
+            else k_tomo<true, false><<<pgrid, 128, 0, st>>>(R, sample);
         } else {
-            if (cnt) k_tomo<false, true><<<grid, 128, 0, st>>>(R, sample);
-            else k_tomo<false, false><<<grid, 128, 0, st>>>(R, sample);
+            if (cnt) k_tomo<false, true><<<pgrid, 128, 0, st>>>(R, sample);
+            else k_tomo<false, false><<<pgrid, 128, 0, st>>>(R, sample);
         }
         T.post(STAGE_TOMO, st, ev);
     } else {

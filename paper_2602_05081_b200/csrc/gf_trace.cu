@@ -24,8 +24,10 @@ __device__ __forceinline__ void traverse(const GNode* __restrict__ nodes, uint32
             for (uint32_t k = 0; k < cnt; ++k) {
                 const GPrim* p = prims + first + k;
                 GPrim P;
-                P.a = __ldg(&p->a); P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
-                f(P, g);
+                P.a = __ldg(&p->a);
+                if (!sphere_pretest(P.a, r, t0, t1)) continue;
+                P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
+                f(P, g, first + k);
             }
             i = sk & ~kLeafBit;
         } else if (hit) {
@@ -36,16 +38,19 @@ __device__ __forceinline__ void traverse(const GNode* __restrict__ nodes, uint32
     }
 }
 
+// brute force over all primitives in input order (test path); same pre-test + predicate
 template <class F>
-__device__ __forceinline__ void brute(const GPrim* __restrict__ prims, int64_t n, uint32_t mask, F&& f) {
+__device__ __forceinline__ void brute(const GPrim* __restrict__ prims, const uint8_t* __restrict__ group, int64_t n,
+                                     const RayDev& r, float t0, float t1, uint32_t mask, F&& f) {
     for (int64_t k = 0; k < n; ++k) {
+        const uint32_t g = __ldg(group + k);
+        if (!((mask >> g) & 1u)) continue;
         const GPrim* p = prims + k;
         GPrim P;
-        P.d = __ldg(&p->d);
-        uint32_t g = __float_as_uint(P.d.w) & 31u;
-        if (!((mask >> g) & 1u)) continue;
-        P.a = __ldg(&p->a); P.b = __ldg(&p->b); P.c = __ldg(&p->c);
-        f(P, g);
+        P.a = __ldg(&p->a);
+        if (!sphere_pretest(P.a, r, t0, t1)) continue;
+        P.b = __ldg(&p->b); P.c = __ldg(&p->c); P.d = __ldg(&p->d);
+        f(P, g, (uint32_t)k);
     }
 }
 
@@ -64,7 +69,7 @@ __global__ void __launch_bounds__(128) k_trace(TraceArgs A) {
     double tau = 0.0;
     uint32_t nvis = 0, ntest = 0, nhit = 0;
     Work wk;
-    auto on_prim = [&](const GPrim& P, uint32_t g) {
+    auto on_prim = [&](const GPrim& P, uint32_t g, uint32_t) {
         if (COUNT) ++ntest;
         Setup s;
         if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
@@ -73,7 +78,7 @@ __global__ void __launch_bounds__(128) k_trace(TraceArgs A) {
         if (STOCH) c *= w[g];
         tau += (double)c;
     };
-    if (BRUTE) brute(A.prims, A.n_prims, mask, on_prim);
+    if (BRUTE) brute(A.prims, A.group, A.n_prims, r, r.tmin, r.tmax, mask, on_prim);
     else traverse<COUNT>(A.nodes, A.n_nodes, A.prims, r, r.tmin, r.tmax, mask, nvis, on_prim);
     A.tau[i] = (float)tau;
     if (A.T) A.T[i] = (float)exp(-tau);
@@ -99,13 +104,13 @@ __global__ void __launch_bounds__(128) k_candidates(TraceArgs A) {
     int32_t cnt = 0;
     uint32_t nvis = 0;
     int32_t* out = A.cand_ids + i * (int64_t)A.cand_cap;
-    auto on_prim = [&](const GPrim& P, uint32_t) {
+    auto on_prim = [&](const GPrim& P, uint32_t, uint32_t k) {
         Setup s;
         if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
-        if (cnt < A.cand_cap) out[cnt] = (int32_t)(__float_as_uint(P.d.w) >> 5);
+        if (cnt < A.cand_cap) out[cnt] = BRUTE ? (int32_t)k : A.perm[k];
         ++cnt;
     };
-    if (BRUTE) brute(A.prims, A.n_prims, mask, on_prim);
+    if (BRUTE) brute(A.prims, A.group, A.n_prims, r, r.tmin, r.tmax, mask, on_prim);
     else traverse<false>(A.nodes, A.n_nodes, A.prims, r, r.tmin, r.tmax, mask, nvis, on_prim);
     A.cand_count[i] = cnt;
 }

@@ -61,10 +61,9 @@ def camera_rays(desc, n=None, seed=0):
 def test_load_groups_match_oracle(gfm, orc):
     sc = I.scene_cfg1()
     f = field(gfm, sc)
-    rec = f.prim_ws[: 64 * sc["n"]].view(torch.int32).view(sc["n"], 16).cpu().numpy()
-    g_gpu = rec[:, 15] & 31
-    idx = rec[:, 15] >> 5
-    assert np.array_equal(idx, np.arange(sc["n"]))
+    # prim_ws layout: n x 64-byte records, then (256-aligned) n group ids
+    off = (64 * sc["n"] + 255) // 256 * 256
+    g_gpu = f.prim_ws[off: off + sc["n"]].cpu().numpy().astype(np.int64)
     g_or, _ = orc.Scene(sc).groups()
     assert np.array_equal(g_gpu, g_or)
 
