@@ -235,6 +235,11 @@ gf_status gf_get_stats(gf_ctx *ctx, gf_stats *out, int32_t reset);
 int32_t gf_shard_pixel_owner(int32_t px, int32_t py, int32_t width, int32_t height, int32_t world);
 /* Owner rank of sample s under sample-interleaved sharding (s mod world). */
 int32_t gf_shard_sample_owner(int32_t s, int32_t world);
+/* Number of paths of one sample pass of a shard (gf_render's work items), -1 on bad args. */
+int64_t gf_shard_paths(int32_t width, int32_t height, int32_t kind, int32_t rank, int32_t world);
+/* Pixel (y*W+x) rendered by path p of a shard's pass, -1 for padding paths: the exact map the
+ * kernels use (8x4-pixel warps inside 32x32 tiles). */
+int32_t gf_shard_path_pixel(int64_t p, int32_t width, int32_t height, int32_t kind, int32_t rank, int32_t world);
 
 #ifdef __cplusplus
 }

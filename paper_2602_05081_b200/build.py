@@ -26,29 +26,32 @@ def _deps():
     return max(os.path.getmtime(f) for f in files)
 
 
-def build(force=False, verbose=False):
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps():
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
+def build(force=False, verbose=False, defines=(), lib=None):
+    """Build libgf.so; `defines` (e.g. ["GF_BATCH=16"]) + `lib` build a tuning variant elsewhere."""
+    lib = lib or LIB
+    if not force and not defines and os.path.exists(lib) and os.path.getmtime(lib) >= _deps():
+        return lib
+    obj_dir = OBJ if not defines else OBJ + "_" + os.path.basename(lib).replace(".so", "")
+    os.makedirs(obj_dir, exist_ok=True)
 
     def comp(src):
-        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        with open(os.path.join(OBJ, src + ".ptxas.txt"), "w") as f:
+        with open(os.path.join(obj_dir, src + ".ptxas.txt"), "w") as f:
             f.write(r.stderr)
         return obj
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(comp, SOURCES))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", LIB] + objs
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", lib] + objs
     subprocess.check_call(cmd)
     if verbose:
         for s in SOURCES:
-            print(open(os.path.join(OBJ, s + ".ptxas.txt")).read())
-    return LIB
+            print(open(os.path.join(obj_dir, s + ".ptxas.txt")).read())
+    return lib
 
 
 if __name__ == "__main__":

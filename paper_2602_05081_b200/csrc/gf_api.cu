@@ -470,6 +470,18 @@ int32_t gf_shard_pixel_owner(int32_t px, int32_t py, int32_t width, int32_t heig
     return (int32_t)(tile % world);
 }
 
+int64_t gf_shard_paths(int32_t width, int32_t height, int32_t kind, int32_t rank, int32_t world) {
+    if (width <= 0 || height <= 0 || kind < 0 || kind > 2 || world < 1 || rank < 0 || rank >= world) return -1;
+    gf_render_desc d{};
+    d.width = width; d.height = height; d.shard_kind = kind; d.shard_rank = rank; d.shard_world = world;
+    return render_paths(&d);
+}
+
+int32_t gf_shard_path_pixel(int64_t p, int32_t width, int32_t height, int32_t kind, int32_t rank, int32_t world) {
+    if (width <= 0 || height <= 0 || world < 1 || rank < 0 || rank >= world) return -1;
+    return shard_path_pixel(p, width, height, kind, rank, world);
+}
+
 int32_t gf_shard_sample_owner(int32_t s, int32_t world) {
     if (s < 0 || world < 1) return -1;
     return s % world;

@@ -232,6 +232,23 @@ __device__ inline float3 hg_sample(float g, float3 v, float u1, float u2) {
     return make_float3(o.x * n, o.y * n, o.z * n);
 }
 
+// ------------------------------------------------------------------ work decomposition (§8(e))
+// Path p of a sample pass -> pixel.  Paths enumerate 32x32 tiles (1024 paths each) in 8x4-pixel
+// warps for coherence; under tile sharding (kind 1) rank r owns tiles r, r+N, r+2N, ...
+// (host + device: the C ABI exports it as gf_shard_path_pixel for the multi-process tests).
+__host__ __device__ inline int32_t shard_path_pixel(int64_t p, int32_t W, int32_t H, int32_t kind, int32_t rank,
+                                                    int32_t world) {
+    const int64_t tiles_x = (W + 31) / 32, tiles_y = (H + 31) / 32;
+    int64_t tile = p >> 10;
+    if (kind == 1) tile = rank + tile * world;
+    if (p < 0 || tile >= tiles_x * tiles_y) return -1;
+    const int local = (int)(p & 1023), blk = local >> 5, lane = local & 31;
+    const int px = (int)(tile % tiles_x) * 32 + (blk & 3) * 8 + (lane & 7);
+    const int py = (int)(tile / tiles_x) * 32 + (blk >> 2) * 4 + (lane >> 3);
+    if (px >= W || py >= H) return -1;
+    return py * W + px;
+}
+
 // ------------------------------------------------------------------ ray / box
 struct RayDev {
     float3 o, d, inv, oinv;
@@ -492,7 +509,7 @@ __device__ __forceinline__ bool trav_done(const Trav& T, uint32_t n_nodes) {
 // The op with the most eligible lanes wins, so node/prim/integral code never diverge against
 // each other.  Callbacks (lane-local): begin(idx) -> bool (false: item needs no traversal);
 // hit(setup, coef, group, sorted prim index); end().  sync() is called by all lanes once per iteration.
-template <bool COUNT, int BATCH, class Begin, class Hit, class End, class Sync>
+template <bool COUNT, int BATCH, bool SPLIT, class Begin, class Hit, class End, class Sync>
 __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const GNode* __restrict__ nodes,
                                           uint32_t n_nodes, const GPrim* __restrict__ prims, Trav& T, Work& wk,
                                           Begin&& begin, Hit&& hit, End&& end, Sync&& sync) {
@@ -537,7 +554,14 @@ __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const 
             const unsigned m_prim = __ballot_sync(FULL, e_prim);
             const int n_hit = __popc(m_hit), n_node = __popc(m_node), n_prim = __popc(m_prim);
             if (n_hit > 0 && (n_hit >= BATCH || n_hit >= n_node + n_prim)) {
-                if (pend) {
+                // run one erf type per op (real for Omega == 0, complex otherwise): no divergence
+                bool run = pend;
+                if (SPLIT) {
+                    const unsigned m_real = __ballot_sync(FULL, pend && s.Om == 0.0f);
+                    const bool real_op = 2 * __popc(m_real) >= n_hit;
+                    run = pend && ((s.Om == 0.0f) == real_op);
+                }
+                if (run) {
                     hit(s, coef, pg, pidx);
                     pend = false;
                 }

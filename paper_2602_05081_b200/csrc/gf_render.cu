@@ -53,14 +53,7 @@ __device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint
 // pixel of path p in this pass (-1 if p maps outside the image / shard)
 __device__ __forceinline__ int32_t path_pixel(const RenderDev& R, int64_t p) {
     if (R.probe) return p < R.n_paths ? R.probe[p] : -1;
-    int64_t tile = p >> 10;
-    if (R.shard_kind == 1) tile = R.shard_rank + tile * R.shard_world;
-    if (tile >= (int64_t)R.tiles_x * R.tiles_y) return -1;
-    const int local = (int)(p & 1023), blk = local >> 5, lane = local & 31;
-    const int px = (int)(tile % R.tiles_x) * 32 + (blk & 3) * 8 + (lane & 7);
-    const int py = (int)(tile / R.tiles_x) * 32 + (blk >> 2) * 4 + (lane >> 3);
-    if (px >= R.cam.W || py >= R.cam.H) return -1;
-    return py * R.cam.W + px;
+    return shard_path_pixel(p, R.cam.W, R.cam.H, R.shard_kind, R.shard_rank, R.shard_world);
 }
 
 // warp-aggregated queue push (called by all 32 lanes of the warp)
@@ -132,17 +125,18 @@ __global__ void __launch_bounds__(128) k_gen(RenderDev R, int32_t sample) {
 // ---------------------------------------------------------------- binned tau over [t0, t1]
 // Adds one hit's partial integrals into NB equal t-bins (one erf evaluation per bin boundary
 // inside the chord, the chord ends shared) and counts the primitives overlapping each bin.
-// Returns the bin span ka | kb << 8 of the chord.
+// Returns the bin span ka | kb << 8 of the chord.  bins/cnts are per-thread columns of shared
+// arrays (element k at [k * stride]).
 template <int NB, bool COUNT>
-__device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, float bw, float ibw, double* bins,
-                                            uint16_t* cnts, Work& wk) {
+__device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, float bw, float ibw, float* bins,
+                                            uint16_t* cnts, int stride, Work& wk) {
     const float ta = fmaf(s.u0 - s.bp, s.ij, s.tc), tb = fmaf(s.u1 - s.bp, s.ij, s.tc);
     const int ka = min(NB - 1, max(0, (int)((ta - t0) * ibw)));
     const int kb = min(NB - 1, max(0, (int)((tb - t0) * ibw)));
     const uint32_t span = (uint32_t)ka | ((uint32_t)kb << 8);
-    for (int m = ka; m <= kb; ++m) cnts[m] = (uint16_t)min(65535, cnts[m] + 1);
+    for (int m = ka; m <= kb; ++m) cnts[m * stride] = (uint16_t)min(65535, cnts[m * stride] + 1);
     if (ka == kb) {
-        bins[ka] += (double)(cj * seg_J(s, s.u0, s.u1, wk));
+        bins[ka * stride] += cj * seg_J(s, s.u0, s.u1, wk);
         return span;
     }
     const float wmax = 0.5f * (fmaxf(s.u0 * s.u0, s.u1 * s.u1) + s.Om * s.Om);
@@ -150,10 +144,10 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
     if ((wmax > kWMaxSeries && s.Om != 0.0f) || s.u1 - s.u0 < 1e-4f) {  // per-piece generic path
         for (int m = ka + 1; m <= kb; ++m) {
             float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
-            bins[m - 1] += (double)(cj * seg_J(s, ua, ub, wk));
+            bins[(m - 1) * stride] += cj * seg_J(s, ua, ub, wk);
             ua = ub;
         }
-        bins[kb] += (double)(cj * seg_J(s, ua, s.u1, wk));
+        bins[kb * stride] += cj * seg_J(s, ua, s.u1, wk);
         return span;
     }
     // shared endpoints: one erf evaluation per bin boundary inside the chord
@@ -164,34 +158,33 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
     for (int m = ka + 1; m <= kb; ++m) {
         float ub = fminf(fmaxf(fmaf(s.j, (t0 + m * bw) - s.tc, s.bp), ua), s.u1);
         float2 Fb = erf_shift(ub, s.Om);
-        bins[m - 1] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
+        bins[(m - 1) * stride] += amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y));
         Fa = Fb;
         ua = ub;
     }
     float2 Fb = erf_shift(s.u1, s.Om);
-    bins[kb] += (double)(amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y)));
+    bins[kb * stride] += amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y));
     if (COUNT) wk.erf(s.Om, (uint32_t)(kb - ka + 2));
     return span;
 }
 
-// full-ray binned pass (used by the ffB overflow fallback)
-template <int NB, bool STOCH, bool COUNT>
-__device__ __forceinline__ void bin_pass(const RenderDev& R, const RayDev& r, uint32_t mask, const float* w,
-                                         float t0, float t1, double* bins, uint16_t* cnts, Work& wk) {
-#pragma unroll
-    for (int k = 0; k < NB; ++k) { bins[k] = 0.0; cnts[k] = 0; }
-    const float bw = (t1 - t0) * (1.0f / NB), ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
-    traverse_r<COUNT>(R.nodes, R.n_nodes, R.prims, r, t0, t1, mask, wk, [&](const GPrim& P, uint32_t g) {
-        Setup s;
-        if (!prim_setup(P, r, t0, t1, s)) return;
-        if (COUNT) ++wk.hits;
-        float cj = P.d.w * s.ij;
-        if (STOCH) cj *= w[g];
-        bin_add<NB, COUNT>(s, cj, t0, bw, ibw, bins, cnts, wk);
-    });
-}
-
-constexpr int kBatch = 24;  // integrate pending hits once this many lanes (or most blocked lanes) have one
+// tuning knobs (compile-time; bench variants are built with -D overrides)
+#ifndef GF_BATCH
+#define GF_BATCH 24
+#endif
+#ifndef GF_MINB_FFA
+#define GF_MINB_FFA 1
+#endif
+#ifndef GF_MINB_NEE
+#define GF_MINB_NEE 1
+#endif
+#ifndef GF_SPLIT_FFA
+#define GF_SPLIT_FFA 0
+#endif
+#ifndef GF_SPLIT_NEE
+#define GF_SPLIT_NEE 0
+#endif
+constexpr int kBatch = GF_BATCH;  // integrate pending hits once this many lanes (or most blocked lanes) have one
 
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
@@ -201,7 +194,7 @@ __global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
     double tau = 0.0;
     float w[kMaxGroups];
     bool began = false;
-    flat_loop<COUNT, kBatch>(
+    flat_loop<COUNT, kBatch, GF_SPLIT_NEE>(
         R.qcount + kWorkT, (uint32_t)R.n_paths, R.nodes, R.n_nodes, R.prims, T, wk,
         [&](uint32_t idx) -> bool {
             p = idx;
@@ -235,14 +228,17 @@ __global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
 
 // ---------------------------------------------------------------- ffA: binned tau over the ray
 template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t sample, int32_t depth) {
     Work wk;
     Trav T;
     uint32_t p = 0;
     double tstar = 0.0;
     float tlo = 0.0f, bw = 0.0f, ibw = 0.0f;
-    double bins[kBins];
-    uint16_t cnts[kBins];
+    // per-thread bins in shared memory, [bin][thread] (conflict-free), fp32 (a bin sums tens of terms)
+    __shared__ float s_bins[kBins * 128];
+    __shared__ uint16_t s_cnts[kBins * 128];
+    float* bins = s_bins + threadIdx.x;
+    uint16_t* cnts = s_cnts + threadIdx.x;
     float w[kMaxGroups];
     bool began = false, fin = false, collide = false;
     uint32_t fin_p = 0, nh = 0;
@@ -261,7 +257,7 @@ __global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_
         fin = true;
         fin_p = p;
     };
-    flat_loop<COUNT, kBatch>(
+    flat_loop<COUNT, kBatch, GF_SPLIT_FFA>(
         R.qcount + kWorkA, R.qcount[0], R.nodes, R.n_nodes, R.prims, T, wk,
         [&](uint32_t idx) -> bool {
             p = R.qA[idx];
@@ -285,14 +281,14 @@ __global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_
             ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
             nh = 0;
 #pragma unroll
-            for (int k = 0; k < kBins; ++k) { bins[k] = 0.0; cnts[k] = 0; }
+            for (int k = 0; k < kBins; ++k) { bins[k * 128] = 0.0f; cnts[k * 128] = 0; }
             trav_begin(T, r, tlo, thi, mask);
             return true;
         },
         [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
             float cj = coef * s.ij;
             if (STOCH) cj *= w[g];
-            const uint32_t span = bin_add<kBins, COUNT>(s, cj, tlo, bw, ibw, bins, cnts, wk);
+            const uint32_t span = bin_add<kBins, COUNT>(s, cj, tlo, bw, ibw, bins, cnts, 128, wk);
             // hit list for ffB: (sorted primitive index | group << 24, bin span), layout [k][path]
             if (nh < (uint32_t)R.hit_cap) R.hits[(size_t)nh * R.n_paths + p] = make_uint2(k | (g << 24), span);
             ++nh;
@@ -300,8 +296,8 @@ __global__ void __launch_bounds__(128) k_ffA(RenderDev R, int32_t sample, int32_
         [&]() {
             double cum = 0.0;
             for (int k = 0; k < kBins; ++k) {
-                const double c2 = cum + bins[k];
-                if (c2 >= tstar) { finish(k, cum, bins[k], cnts[k]); return; }
+                const double c2 = cum + (double)bins[k * 128];
+                if (c2 >= tstar) { finish(k, cum, (double)bins[k * 128], cnts[k * 128]); return; }
                 cum = c2;
             }
             finish(-2, 0.0, 0.0, 0);
@@ -502,7 +498,7 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
 
 // ---------------------------------------------------------------- NEE + phase sampling
 template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128) k_nee(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t sample, int32_t depth) {
     Work wk;
     Trav T;
     uint32_t p = 0, pix = 0;
@@ -510,7 +506,7 @@ __global__ void __launch_bounds__(128) k_nee(RenderDev R, int32_t sample, int32_
     float w[kMaxGroups];
     bool began = false, cont = false;
     uint32_t fin_p = 0;
-    flat_loop<COUNT, kBatch>(
+    flat_loop<COUNT, kBatch, GF_SPLIT_NEE>(
         R.qcount + kWorkN, R.qcount[1], R.nodes, R.n_nodes, R.prims, T, wk,
         [&](uint32_t idx) -> bool {
             p = R.qB[idx];

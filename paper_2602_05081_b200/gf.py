@@ -12,7 +12,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgf.so")
+LIB_PATH = os.environ.get("GF_LIB", os.path.join(HERE, "libgf.so"))  # GF_LIB: tuning variants only
 HEADER = os.path.join(os.path.dirname(HERE), "include", "gf.h")
 _lib = None
 
@@ -102,6 +102,10 @@ def lib():
     L.gf_shard_pixel_owner.argtypes = [i32, i32, i32, i32, i32]
     L.gf_shard_sample_owner.restype = i32
     L.gf_shard_sample_owner.argtypes = [i32, i32]
+    L.gf_shard_paths.restype = i64
+    L.gf_shard_paths.argtypes = [i32, i32, i32, i32, i32]
+    L.gf_shard_path_pixel.restype = i32
+    L.gf_shard_path_pixel.argtypes = [i64, i32, i32, i32, i32, i32]
     _lib = L
     return L
 
@@ -286,3 +290,11 @@ def shard_pixel_owner(px, py, width, height, world):
 
 def shard_sample_owner(s, world):
     return lib().gf_shard_sample_owner(s, world)
+
+
+def shard_paths(width, height, kind, rank, world):
+    return lib().gf_shard_paths(width, height, kind, rank, world)
+
+
+def shard_path_pixel(p, width, height, kind, rank, world):
+    return lib().gf_shard_path_pixel(p, width, height, kind, rank, world)
