@@ -370,22 +370,28 @@ constexpr int kErfTerms = 30;
 constexpr float kRsqrt2 = 0.70710678118654752f;
 constexpr float kTwoOverSqrtPi = 1.12837916709551257f;
 constexpr float kInvSqrt2Pi = 0.39894228040143268f;
-constexpr float kWMaxSeries = 9.0f;  // |z^2| beyond this -> Gauss-Legendre fallback
+constexpr float kWMaxSeries = 8.0f;  // |z^2| beyond this -> Gauss-Legendre fallback (30 terms: 2.4e-7)
 
-// F(u) = erf((u - i Omega)/sqrt2).  Omega == 0 (every Gaussian, omega = 0, and Gabors integrated
-// exactly along their modulation plane) reduces to the real erf (P:L191, P:L271): erff, 2 ulp.
-__device__ __forceinline__ float2 erf_shift(float u, float Om) {
-    if (Om == 0.0f) return make_float2(erff(u * kRsqrt2), 0.0f);
-    float zr = u * kRsqrt2, zi = -Om * kRsqrt2;
-    float wr = fmaf(zr, zr, -zi * zi), wi = 2.0f * zr * zi;
-    float sr = kErfA[kErfTerms - 1], si = 0.0f;
+template <int N>
+__device__ __forceinline__ float2 erf_horner(float zr, float zi, float wr, float wi) {
+    float sr = kErfA[N - 1], si = 0.0f;
 #pragma unroll
-    for (int n = kErfTerms - 2; n >= 0; --n) {
+    for (int n = N - 2; n >= 0; --n) {
         float tr = fmaf(sr, wr, fmaf(-si, wi, kErfA[n]));
         float ti = fmaf(sr, wi, si * wr);
         sr = tr; si = ti;
     }
     return make_float2(kTwoOverSqrtPi * fmaf(zr, sr, -zi * si), kTwoOverSqrtPi * fmaf(zr, si, zi * sr));
+}
+
+// F(u) = erf((u - i Omega)/sqrt2).  Omega == 0 (every Gaussian, omega = 0, and Gabors integrated
+// exactly along their modulation plane) reduces to the real erf (P:L191, P:L271): erff, 2 ulp.
+// Otherwise the 30-term Horner series (a warp-uniform adaptive term count was measured slower:
+// four unrolled copies at every call site cost more in instruction fetch than they save).
+__device__ __forceinline__ float2 erf_shift(float u, float Om) {
+    if (Om == 0.0f) return make_float2(erff(u * kRsqrt2), 0.0f);
+    const float zr = u * kRsqrt2, zi = -Om * kRsqrt2;
+    return erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
 }
 
 __constant__ float kGLx[12] = {6.40568928626056300e-02f, 1.91118867473616311e-01f, 3.15042679696163397e-01f,
@@ -508,7 +514,7 @@ __device__ __forceinline__ bool trav_done(const Trav& T, uint32_t n_nodes) {
 //         expensive erf work runs once BATCH lanes have one (or nothing else can advance).
 // The op with the most eligible lanes wins, so node/prim/integral code never diverge against
 // each other.  Callbacks (lane-local): begin(idx) -> bool (false: item needs no traversal);
-// hit(setup, coef, group, sorted prim index); end().  sync() is called by all lanes once per iteration.
+// hit(setup, coef, group, sorted prim index) -> bool done (a hit may take several ops); end().  sync() is called by all lanes once per iteration.
 template <bool COUNT, int BATCH, bool SPLIT, class Begin, class Hit, class End, class Sync>
 __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const GNode* __restrict__ nodes,
                                           uint32_t n_nodes, const GPrim* __restrict__ prims, Trav& T, Work& wk,
@@ -561,10 +567,7 @@ __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const 
                     const bool real_op = 2 * __popc(m_real) >= n_hit;
                     run = pend && ((s.Om == 0.0f) == real_op);
                 }
-                if (run) {
-                    hit(s, coef, pg, pidx);
-                    pend = false;
-                }
+                if (run && hit(s, coef, pg, pidx)) pend = false;  // hit() may take several ops
             } else if (n_prim > 0 && n_prim >= n_node) {
                 if (e_prim) {
                     const uint32_t k = T.lk, g = T.g;

@@ -91,7 +91,7 @@ struct RenderDev {
     int32_t* bin;
     uint32_t* pix;
     uint32_t* nhit;  // hits recorded by ffA
-    uint2* hits;     // [hit_cap][n_paths]: sorted prim index | group << 24, bin span ka | kb << 8
+    uint2* hits;     // [n_paths][hit_cap]: sorted prim index | group << 24, bin span ka | kb << 8
     int32_t hit_cap;
     // queues
     uint32_t *qA, *qB, *qNext;

@@ -173,7 +173,7 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #define GF_BATCH 24
 #endif
 #ifndef GF_MINB_FFA
-#define GF_MINB_FFA 1
+#define GF_MINB_FFA 6
 #endif
 #ifndef GF_MINB_NEE
 #define GF_MINB_NEE 1
@@ -216,10 +216,11 @@ __global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
             if (COUNT) ++wk.paths;
             return true;
         },
-        [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
             float c = coef * s.ij * seg_J(s, s.u0, s.u1, wk);
             if (STOCH) c *= w[g];
             tau += (double)c;
+            return true;
         },
         [&]() { R.L[p] = (float)tau; },
         [&]() { count_rays(R.rays + 0, began); began = false; });
@@ -285,13 +286,14 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
             trav_begin(T, r, tlo, thi, mask);
             return true;
         },
-        [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
             float cj = coef * s.ij;
             if (STOCH) cj *= w[g];
             const uint32_t span = bin_add<kBins, COUNT>(s, cj, tlo, bw, ibw, bins, cnts, 128, wk);
-            // hit list for ffB: (sorted primitive index | group << 24, bin span), layout [k][path]
-            if (nh < (uint32_t)R.hit_cap) R.hits[(size_t)nh * R.n_paths + p] = make_uint2(k | (g << 24), span);
+            // hit list for ffB: (sorted primitive index | group << 24, bin span), layout [path][k]
+            if (nh < (uint32_t)R.hit_cap) R.hits[(size_t)p * R.hit_cap + nh] = make_uint2(k | (g << 24), span);
             ++nh;
+            return true;
         },
         [&]() {
             double cum = 0.0;
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
             const uint32_t nh = R.nhit[p];
             if (nh <= (uint32_t)R.hit_cap) {  // scan the path's hit list from ffA (no traversal)
                 for (uint32_t k = 0; k < nh; ++k) {
-                    const uint2 e = R.hits[(size_t)k * R.n_paths + p];
+                    const uint2 e = R.hits[(size_t)p * R.hit_cap + k];
                     if ((int)(e.y & 0xFFu) > bin || (int)(e.y >> 8) < bin) continue;
                     const GPrim* q = R.prims + (e.x & 0xFFFFFFu);
                     GPrim P;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
                     };
                     if (nh <= (uint32_t)R.hit_cap) {
                         for (uint32_t k = 0; k < nh; ++k) {
-                            const uint2 e = R.hits[(size_t)k * R.n_paths + p];
+                            const uint2 e = R.hits[(size_t)p * R.hit_cap + k];
                             if ((int)(e.y & 0xFFu) > bin || (int)(e.y >> 8) < bin) continue;
                             const GPrim* q = R.prims + (e.x & 0xFFFFFFu);
                             GPrim P;
@@ -521,10 +523,11 @@ __global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t s
             tau = 0.0;
             return true;
         },
-        [&](const Setup& s, float coef, uint32_t g, uint32_t k) {
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
             float c = coef * s.ij * seg_J(s, s.u0, s.u1, wk);
             if (STOCH) c *= w[g];
             tau += (double)c;
+            return true;
         },
         [&]() {
             const float3 d = ld3(R.dx, R.dy, R.dz, p);
