@@ -344,6 +344,8 @@ gf_status gf_trace_candidates(gf_ctx* c, const float* rays, int64_t n, uint32_t 
     return GF_OK;
 }
 
+static constexpr int64_t kRenderChunk = 1 << 20;  // paths per wavefront chunk (scratch ~9 GB)
+
 static int64_t render_paths(const gf_render_desc* d) {
     if (d->probe_pixels) return d->n_probe;
     const int64_t tx = (d->width + 31) / 32, ty = (d->height + 31) / 32, tiles = tx * ty;
@@ -374,7 +376,8 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
 gf_status gf_render_scratch_bytes(gf_ctx* c, const gf_render_desc* d, size_t* bytes) {
     if (!c || !bytes) return GF_E_INVALID_ARGUMENT;
     if (gf_status s = check_desc(c, d)) return s;
-    *bytes = gf_render_state_bytes(std::max<int64_t>(render_paths(d), 1), nullptr, nullptr);
+    *bytes = gf_render_state_bytes(std::min<int64_t>(std::max<int64_t>(render_paths(d), 1), kRenderChunk), nullptr,
+                                   nullptr);
     return GF_OK;
 }
 
@@ -384,13 +387,14 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     if (gf_status s = check_desc(c, d)) return s;
     if (!c->loaded || !c->built) return fail(c, GF_E_STATE, "render before gf_load_primitives / gf_build_bvh");
     const int64_t np = render_paths(d);
-    size_t need = gf_render_state_bytes(std::max<int64_t>(np, 1), nullptr, nullptr);
+    const int64_t chunk = std::min<int64_t>(std::max<int64_t>(np, 1), kRenderChunk);
+    size_t need = gf_render_state_bytes(chunk, nullptr, nullptr);
     if (scratch_bytes < need || !scratch) return fail(c, GF_E_OUT_OF_MEMORY, "render scratch too small");
     if (!accum && np > 0) return fail(c, GF_E_INVALID_ARGUMENT, "accum required");
     GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
     if (gf_status s = check_sticky(c)) return s;
     RenderDev R{};
-    gf_render_state_bytes(std::max<int64_t>(np, 1), (char*)scratch, &R);
+    gf_render_state_bytes(chunk, (char*)scratch, &R);
     R.nodes = c->nodes;
     R.n_nodes = c->n_nodes;
     R.prims = c->sorted;
@@ -411,7 +415,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.albedo = d->albedo; R.hg_g = d->hg_g; R.sun_E = d->sun_E; R.env_L = d->env_L;
     R.sun = make_float3(d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]);
     R.seed = d->seed;
-    R.n_paths = np;
+    R.n_total = np;
     R.shard_kind = d->shard_kind;
     R.shard_rank = d->shard_rank;
     R.shard_world = std::max(1, d->shard_world);
@@ -426,7 +430,11 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     for (int32_t k = 0; k < d->spp_count; ++k) {
         const int32_t s = d->spp_begin + k;
         if (d->shard_kind == GF_SHARD_SAMPLES && (s % R.shard_world) != d->shard_rank) continue;
-        GF_CUDA(c, gf_launch_render_pass(R, s, k, st, c->timer), "render pass");
+        for (int64_t base = 0; base < np; base += chunk) {  // bounded scratch: chunks of <= 1M paths
+            R.path_base = base;
+            R.n_paths = std::min<int64_t>(chunk, np - base);
+            GF_CUDA(c, gf_launch_render_pass(R, s, k, st, c->timer), "render pass");
+        }
     }
     if (c->timer.recs.size() > 4096) harvest(c);  // bound the event pool
     return GF_OK;

@@ -80,7 +80,9 @@ struct RenderDev {
     float3 sun;
     uint64_t seed;
     // work decomposition
-    int64_t n_paths;           // paths per sample pass
+    int64_t n_paths;           // paths of this chunk of the sample pass (state arrays are per chunk)
+    int64_t path_base;         // global index of the chunk's first path
+    int64_t n_total;           // paths of the whole pass
     int32_t shard_kind, shard_rank, shard_world;
     int32_t tiles_x, tiles_y;  // 32x32 tiles
     const int32_t* probe;      // probe pixels or null

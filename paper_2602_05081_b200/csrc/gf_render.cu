@@ -52,8 +52,9 @@ __device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint
 
 // pixel of path p in this pass (-1 if p maps outside the image / shard)
 __device__ __forceinline__ int32_t path_pixel(const RenderDev& R, int64_t p) {
-    if (R.probe) return p < R.n_paths ? R.probe[p] : -1;
-    return shard_path_pixel(p, R.cam.W, R.cam.H, R.shard_kind, R.shard_rank, R.shard_world);
+    const int64_t gp = R.path_base + p;
+    if (R.probe) return gp < R.n_total ? R.probe[gp] : -1;
+    return shard_path_pixel(gp, R.cam.W, R.cam.H, R.shard_kind, R.shard_rank, R.shard_world);
 }
 
 // warp-aggregated queue push (called by all 32 lanes of the warp)
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(256) k_finish(RenderDev R, int32_t slot) {
     if (pix < 0) return;
     const float v = R.L[p];
     if (R.probe) {
-        R.accum[p * R.spp_count + slot] = v;
+        R.accum[(R.path_base + p) * R.spp_count + slot] = v;
     } else {
         R.accum[2 * (int64_t)pix] += v;
         R.accum[2 * (int64_t)pix + 1] += v * v;

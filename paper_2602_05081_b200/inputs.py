@@ -166,6 +166,112 @@ def scene_cfg2(seed=SCENE_SEED + 2):
     return scene_bunny(seed=seed)
 
 
+def _maxwell(rng, a, n):
+    """Maxwell-distributed samples with scale a (norm of a 3D normal vector of std a)."""
+    return a * np.linalg.norm(rng.normal(size=(n, 3)), axis=1)
+
+
+def scene_cfg3(seed=SCENE_SEED + 3, n_clouds=100, depth=3, children=5, density=5.0):
+    """Config 3: procedural clouds (§6.3): each cloud is a chunk tree (depth 3, 5 children
+    per chunk -> 156 chunks); a chunk is one Gaussian core (sigma = r/3) plus 20 Gabors placed at a
+    random position inside each cell of a 4x5 latitude-longitude grid on its surface sphere, scales
+    Maxwell(r/12), omega ~ U[0.7,1.5], random orientation; child chunks sit uniformly at random on
+    the parent's surface with Maxwell(0.25 r_parent) radii.  100 clouds in [-20,20]x[0,6]x[-20,20].
+    Gabor levels by scale tertile (smaller -> higher level)."""
+    rng = np.random.default_rng(seed)
+    cores, core_r = [], []
+    for _ in range(n_clouds):
+        c0 = rng.uniform([-20, 0, -20], [20, 6, 20])
+        frontier = [(c0, rng.uniform(1.0, 2.0))]
+        for lvl in range(depth + 1):
+            nxt = []
+            for c, r in frontier:
+                cores.append(c)
+                core_r.append(r)
+                if lvl < depth:
+                    d = rng.normal(size=(children, 3))
+                    d /= np.linalg.norm(d, axis=1, keepdims=True)
+                    rc = np.maximum(_maxwell(rng, 0.25 * r / np.sqrt(3), children), 0.05 * r)
+                    nxt += [(c + r * d[k], rc[k]) for k in range(children)]
+            frontier = nxt
+    cores, core_r = np.array(cores), np.array(core_r)
+    nc = len(cores)
+    # 20 Gabors per chunk on a jittered 4 (lat) x 5 (lon) grid over the chunk's surface sphere
+    lat = (np.arange(4)[None, :, None] + rng.random((nc, 4, 5))) / 4.0  # cos(theta) cells
+    lon = (np.arange(5)[None, None, :] + rng.random((nc, 4, 5))) / 5.0
+    ct = 1 - 2 * lat
+    st = np.sqrt(1 - ct ** 2)
+    ph = 2 * np.pi * lon
+    dirs = np.stack([st * np.cos(ph), ct, st * np.sin(ph)], -1).reshape(nc, 20, 3)
+    gmu = (cores[:, None, :] + core_r[:, None, None] * dirs).reshape(-1, 3)
+    gr = np.repeat(core_r, 20)
+    gs = np.maximum(_maxwell(rng, gr / 12 / np.sqrt(3), len(gr)), 0.02 * gr)
+    gscale = gs[:, None] * np.exp(rng.normal(0, 0.15, (len(gs), 3)))
+    rel = gs / gr
+    q1, q2 = np.quantile(rel, [1 / 3, 2 / 3])
+    glevel = np.where(rel >= q2, 1, np.where(rel >= q1, 2, 3)).astype(np.uint8)
+    cscale = (core_r / 3.0)[:, None] * np.exp(rng.normal(0, 0.1, (nc, 3)))
+    mu = np.concatenate([cores, gmu])
+    scale = np.concatenate([cscale, gscale])
+    level = np.concatenate([np.zeros(nc, np.uint8), glevel])
+    omega = np.concatenate([np.zeros(nc), rng.uniform(0.7, 1.5, len(gmu))])
+    peak = density * np.concatenate([rng.uniform(0.5, 1.0, nc), np.array([0, 0.5, 0.35, 0.25])[glevel]])
+    n = len(mu)
+    return _finish(mu, random_quats(rng, n), scale, peak, omega, level, name="cfg3")
+
+
+def scene_cfg4(seed=SCENE_SEED + 4, counts=(12000, 48000, 192000, 748000), s_levels=(0.075, 0.025, 0.0125, 0.00625),
+               density=0.26):
+    """Config 4: 'dense asset' -- a volume-filling pyramid in the cube [-1,1]^3, levels 0..3 with
+    12k/48k/192k/748k primitives (N = 1,000,000) at scales 0.075/0.025/0.0125/0.00625."""
+    rng = np.random.default_rng(seed)
+    mus, scales, levels, peaks, omegas = [], [], [], [], []
+    for l, cnt in enumerate(counts):
+        mus.append(rng.uniform(-1, 1, (cnt, 3)))
+        scales.append(s_levels[l] * np.exp(rng.normal(0, 0.25, (cnt, 3))))
+        levels.append(np.full(cnt, l, np.uint8))
+        peaks.append(density * (rng.uniform(0.5, 1.0, cnt) if l == 0 else np.full(cnt, (0.5, 0.35, 0.25)[l - 1])))
+        omegas.append(np.zeros(cnt) if l == 0 else rng.uniform(0.7, 1.5, cnt))
+    n = sum(counts)
+    return _finish(np.concatenate(mus), random_quats(rng, n), np.concatenate(scales), np.concatenate(peaks),
+                   np.concatenate(omegas), np.concatenate(levels), name="cfg4")
+
+
+def scene_cfg5(seed=SCENE_SEED + 5, copies=120, grid=(12, 10), spacing=2.2):
+    """Config 5: 'army' -- 120 yawed, scaled copies of a 33,280-primitive bunny-like asset (config-2
+    generator at 500/3,494/9,318/19,968) on a 12 x 10 ground grid: N = 3,993,600."""
+    base = scene_bunny(seed=seed, counts=(500, 3494, 9318, 19968), name="cfg5-asset")
+    rng = np.random.default_rng(seed + 1)
+    nb = base["n"]
+    out = {k: [] for k in ("mu", "quat", "scale", "alpha")}
+    for c in range(copies):
+        gx, gz = c % grid[0], c // grid[0]
+        yaw = rng.uniform(0, 2 * np.pi)
+        sc = rng.uniform(0.8, 1.2)
+        cy, sy = np.cos(yaw), np.sin(yaw)
+        Ry = np.array([[cy, 0, sy], [0, 1, 0], [-sy, 0, cy]])
+        off = np.array([(gx - (grid[0] - 1) / 2) * spacing, 0.0, (gz - (grid[1] - 1) / 2) * spacing])
+        out["mu"].append(base["mu"].astype(np.float64) @ Ry.T * sc + off)
+        qy = np.array([0.0, np.sin(yaw / 2), 0.0, np.cos(yaw / 2)])  # (x,y,z,w)
+        q = base["quat"].astype(np.float64)
+        x1, y1, z1, w1 = qy
+        x2, y2, z2, w2 = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+        out["quat"].append(np.stack([w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2, w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2,
+                                     w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2, w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2], 1))
+        out["scale"].append(base["scale"].astype(np.float64) * sc)
+        out["alpha"].append(base["alpha"].astype(np.float64) * sc ** 2)  # keeps peak density (alpha ~ s^3 / s)
+    n = nb * copies
+    q = np.concatenate(out["quat"])
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    return {"name": "cfg5", "n": n, "P": base["P"], "K": base["K"],
+            "mu": np.concatenate(out["mu"]).astype(np.float32), "quat": q.astype(np.float32),
+            "scale": np.concatenate(out["scale"]).astype(np.float32),
+            "alpha": np.concatenate(out["alpha"]).astype(np.float32),
+            "omega": np.tile(base["omega"], copies), "extent": np.full(n, 3.0, np.float32),
+            "level": np.tile(base["level"], copies), "bin": np.full(n, 255, np.uint8),
+            "bin_axes": base["bin_axes"]}
+
+
 def empty_scene(P=P_DEFAULT, K=K_DEFAULT):
     z = np.zeros((0, 3), np.float32)
     return _finish(z, np.zeros((0, 4), np.float32), z, np.zeros(0), np.zeros(0), np.zeros(0, np.uint8), P, K,
@@ -240,6 +346,32 @@ def render_desc_cfg2(mask_index=3, width=1024, height=1024, seed=RENDER_SEED + 2
     m = level_mask(CFG2_LOD_LEVELS[mask_index])
     d.update(mode=1, max_depth=1, jitter=1, albedo=0.8, hg_g=0.0, sun_dir=SUN, sun_E=3.0, env_L=0.2,
              seed=seed + 0x100 * mask_index, ext=policy(static_mask=m), nee=policy(static_mask=m))
+    return d
+
+
+def render_desc_cfg3(width=1024, height=1024, seed=RENDER_SEED + 3):
+    """Config 3: multiple scattering, depth 8, albedo 0.95, HG g = 0.6, full mask (4 spp per frame)."""
+    d = camera((0, 4, 34), (0, 2, 0), (0, 1, 0), 60.0, width, height)
+    d.update(mode=1, max_depth=8, jitter=1, albedo=0.95, hg_g=0.6, sun_dir=SUN, sun_E=3.0, env_L=0.2, seed=seed,
+             ext=policy(), nee=policy())
+    return d
+
+
+def render_desc_cfg4(width=2048, height=2048, seed=RENDER_SEED + 4):
+    """Config 4: multiple scattering depth 8 with stochastic per-recursion masks: extension rays
+    PL+CV(Accum.) beta = 0.2 x orientation Importance, NEE 'Zero NEE' (level 0 only)."""
+    d = camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, width, height)
+    d.update(mode=1, max_depth=8, jitter=1, albedo=0.8, hg_g=0.3, sun_dir=SUN, sun_E=3.0, env_L=0.2, seed=seed,
+             ext=policy(level_strategy=5, beta=0.2, orient_strategy=3), nee=policy(static_mask=1))
+    return d
+
+
+def render_desc_cfg5(mask_levels=(0, 1, 2, 3), width=4096, height=4096, seed=RENDER_SEED + 5):
+    """Config 5: multiple scattering depth 8 over the army, one global static LOD mask."""
+    d = camera((0, 6, 22), (0, 0, 0), (0, 1, 0), 50.0, width, height)
+    m = level_mask(mask_levels)
+    d.update(mode=1, max_depth=8, jitter=1, albedo=0.8, hg_g=0.0, sun_dir=SUN, sun_E=3.0, env_L=0.2, seed=seed,
+             ext=policy(static_mask=m), nee=policy(static_mask=m))
     return d
 
 

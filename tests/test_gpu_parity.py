@@ -308,3 +308,60 @@ def test_cfg2_bench_configuration_sampled(gfm, orc):
         flips = np.mean(np.abs(vg - vo[:, 0]) > 1e-3 * (np.abs(vo[:, 0]) + 1e-2))
         assert flips <= 0.03, (mi, flips)
         assert int(rc[0]) == 1024 * 1024
+
+
+# ------------------------------------------------------------------------------ configs 3-5
+def test_cfg3_clouds_sampled(gfm, orc):
+    """Config 3 (procedural clouds, 327,600 primitives): camera-ray tau parity at sampled pixels and
+    multiple-scattering (depth 8, g = 0.6) probe paths with identical Philox streams."""
+    sc = I.scene_cfg3()
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    desc = I.render_desc_cfg3()
+    rays = camera_rays(desc, 400, seed=31)
+    tau, T, _ = f.trace_transmittance(rays)
+    r = S.trace(rays)
+    assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), "cfg3 camera")
+    # probes on cloud pixels (tau > 0) so the paths scatter
+    W = desc["width"]
+    idx = np.random.default_rng(31).integers(0, W * W, 400)
+    probes = idx[r["tau"] > 0.2][:24].astype(np.int32)
+    _probe_compare(gfm, orc, sc, desc, probes, 4, "cfg3 multi scatter", frac_tol=0.08)
+
+
+def test_cfg4_dense_sampled(gfm, orc):
+    """Config 4 (1M primitives, dense cube): tau parity at sampled camera rays (full mask and a
+    static LOD mask) and stochastic per-recursion masks (PL+CV Accum. beta 0.2 x Importance, Zero
+    NEE) in multiple scattering at probe pixels."""
+    sc = I.scene_cfg4()
+    f0 = I.group_f0(sc)
+    f = field(gfm, sc, group_f0=f0)
+    S = orc.Scene(sc)
+    desc = I.render_desc_cfg4()
+    rays = camera_rays(desc, 64, seed=41)
+    for m in (0xFFFFFFFF, I.level_mask([0, 1])):
+        f.set_lod_mask({"static_mask": m})
+        tau, T, _ = f.trace_transmittance(rays)
+        r = S.trace(rays, mask=m)
+        assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), f"cfg4 mask {m:#x}")
+    probes = np.random.default_rng(41).integers(0, desc["width"] * desc["height"], 12).astype(np.int32)
+    d = dict(desc, max_depth=4)
+    _probe_compare(gfm, orc, sc, d, probes, 4, "cfg4 stochastic multi scatter", frac_tol=0.1, f0=f0)
+
+
+def test_cfg5_army_primary_tau(gfm, orc):
+    """Config 5 (3,993,600 primitives): primary-ray tau parity under the full and a coarse LOD mask
+    (16-bit leaf starts and 24-bit primitive indices exercised at 4M)."""
+    sc = I.scene_cfg5()
+    assert sc["n"] == 3993600
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    desc = I.render_desc_cfg5()
+    rays = camera_rays(desc, 32, seed=51)
+    for m in (0xFFFFFFFF, I.level_mask([0, 1])):
+        f.set_lod_mask({"static_mask": m})
+        tau, T, _ = f.trace_transmittance(rays)
+        r = S.trace(rays, mask=m)
+        assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), f"cfg5 mask {m:#x}")
+    acc, rc = f.render(dict(desc, width=256, height=256), 0, 1)
+    assert np.isfinite(acc.cpu().numpy()).all() and int(rc[0]) >= 256 * 256
