@@ -94,6 +94,21 @@ def workload(config):
         sc = I.scene_cfg1()
         descs = [I.render_desc_cfg1()]
         name = "cfg1: 1k random Gabor primitives, 64x64, 1 spp primary-ray transmittance (tomography), full LOD"
+    elif config == 3:
+        sc = I.scene_cfg3()
+        descs = [I.render_desc_cfg3()]
+        name = ("cfg3: procedural clouds, 327,600 primitives (15,600 Gaussian cores + 312,000 Gabors), 1024x1024, "
+                "multiple scattering depth 8, full LOD, 1 spp per step per GPU")
+    elif config == 4:
+        sc = I.scene_cfg4()
+        descs = [I.render_desc_cfg4()]
+        name = ("cfg4: dense 1M-primitive asset, 2048x2048, multiple scattering depth 8, stochastic per-recursion "
+                "masks (PL+CV Accum. beta 0.2 x orientation Importance, Zero NEE), 1 spp per step per GPU")
+    elif config == 5:
+        sc = I.scene_cfg5()
+        descs = [I.render_desc_cfg5(lv, 4096, 4096) for lv in ((0,), (0, 1), (0, 1, 2), (0, 1, 2, 3))]
+        name = ("cfg5: 4M-primitive army (120 x 33,280-primitive bunnies), 4096x4096, multiple scattering depth 8, "
+                "LOD sweep over 4 global static masks, 1 spp per mask per step per GPU")
     else:
         sc = I.scene_cfg2()
         descs = [I.render_desc_cfg2(i) for i in range(4)]
@@ -153,7 +168,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gabor", choices=["gabor", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-pass", action="store_true", help="only run warmup+steps (for ncu launch lists)")
@@ -171,7 +186,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sc, descs, name = workload(args.config)
     f = gf.GaborField(local)
-    f.load_primitives(sc)
+    f.load_primitives(sc, group_f0=I.group_f0(sc))
     f.build_bvh()
     H, W = descs[0]["height"], descs[0]["width"]
     shard = (gf.SHARD_SAMPLES, rank, world)
@@ -271,7 +286,7 @@ def main():
             a.record()
             dev = {kk: v.to(f.device, non_blocking=True) for kk, v in host.items()}
             scd = dict(sc, **dev)
-            g2.load_primitives(scd)
+            g2.load_primitives(scd, group_f0=I.group_f0(sc))
             g2.build_bvh()
             accum.zero_()
             for i, d in enumerate(descs):
@@ -299,7 +314,7 @@ def main():
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(sc, descs, 4096)
+            cb = cpu_baseline(sc, descs, {1: 4096, 2: 4096, 3: 512, 4: 32, 5: 16}[args.config])
         line = {"metric": "Mrays/s (transmittance + scattering)", "value": value, "unit": "Mrays/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms_max / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",

@@ -478,9 +478,60 @@ __device__ inline float seg_J(const Setup& s, float ua, float ub, Work& wk) {
     return amp * fmaf(cp, Fb.x - Fa.x, -sp * (Fb.y - Fa.y));
 }
 
+// One erf call site for all lanes evaluating together (SIMT-uniform): the real erf if every
+// participating lane has Omega == 0, otherwise the complex series for all of them (a Gaussian lane
+// in a mixed group gets the same value from the series).  Inlining erf_shift at several call sites
+// instead left each copy running with ~6 of 32 lanes (ncu source view, round 1).
+#ifndef GF_ERF_WARP_UNIFORM
+#define GF_ERF_WARP_UNIFORM 0
+#endif
+__device__ __forceinline__ float2 erf_warp(float u, float Om, Work& wk) {
+    const float zr = u * kRsqrt2, zi = -Om * kRsqrt2;
+    if (GF_ERF_WARP_UNIFORM ? __all_sync(__activemask(), Om == 0.0f) : Om == 0.0f) {
+        ++wk.erfr;
+        return make_float2(erff(zr), 0.0f);
+    }
+    ++wk.erfc;
+    return erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
+}
+
+// Rare special cases of a piece [ua, ub]: midpoint rule (whitened length < 1e-4) or
+// Gauss-Legendre (outside the series domain).  Returns false if the series path applies.
+__device__ __forceinline__ bool seg_J_special(const Setup& s, float ua, float ub, float& res, Work& wk) {
+    const float wmax = 0.5f * (fmaxf(ua * ua, ub * ub) + s.Om * s.Om);
+    if (ub - ua < 1e-4f || (wmax > kWMaxSeries && s.Om != 0.0f)) {
+        res = seg_J(s, ua, ub, wk);
+        return true;
+    }
+    return false;
+}
+
+// Segment integral of a hit over its clipped chord, SIMT-uniform version of seg_J: the series
+// endpoints of all lanes go through one erf call site (a symmetric full chord needs one endpoint,
+// F(h) - F(-h) = 2 Re F(h); otherwise two).
+__device__ __forceinline__ float seg_J_u(const Setup& s, float ua, float ub, Work& wk) {
+    float res = 0.0f;
+    int ne = 0;
+    if (!seg_J_special(s, ua, ub, res, wk)) ne = (ua == -s.h && ub == s.h) ? 1 : 2;
+    float sp, cp;
+    sincos_red(s.phi0, &sp, &cp);
+    const float amp = 0.5f * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+    float2 Fa = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+    for (int e = 0; e < 2; ++e) {
+        if (e < ne) {
+            const float2 F = erf_warp(e == 0 && ne == 2 ? ua : ub, s.Om, wk);
+            if (ne == 1) res = 2.0f * amp * cp * F.x;
+            else if (e == 1) res = amp * fmaf(cp, F.x - Fa.x, -sp * (F.y - Fa.y));
+            Fa = F;
+        }
+    }
+    return res;
+}
+
 // contribution of a hit over its clipped chord: c/j * Jw
 __device__ __forceinline__ float hit_tau(const GPrim& P, const Setup& s, Work& wk) {
-    return P.d.w * s.ij * seg_J(s, s.u0, s.u1, wk);
+    return P.d.w * s.ij * seg_J_u(s, s.u0, s.u1, wk);
 }
 
 __device__ __forceinline__ uint32_t node_mask(uint32_t skipw, uint32_t info) {

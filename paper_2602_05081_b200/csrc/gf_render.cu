@@ -177,7 +177,7 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #define GF_MINB_FFA 6
 #endif
 #ifndef GF_MINB_NEE
-#define GF_MINB_NEE 1
+#define GF_MINB_NEE 6
 #endif
 #ifndef GF_SPLIT_FFA
 #define GF_SPLIT_FFA 0
