@@ -344,7 +344,10 @@ gf_status gf_trace_candidates(gf_ctx* c, const float* rays, int64_t n, uint32_t 
     return GF_OK;
 }
 
-static constexpr int64_t kRenderChunk = 1 << 20;  // paths per wavefront chunk (scratch ~9 GB)
+#ifndef GF_CHUNK_LOG2
+#define GF_CHUNK_LOG2 20
+#endif
+static constexpr int64_t kRenderChunk = 1ll << GF_CHUNK_LOG2;  // paths per wavefront chunk (scratch ~34 GB at 2^20)
 
 static int64_t render_paths(const gf_render_desc* d) {
     if (d->probe_pixels) return d->n_probe;

@@ -16,7 +16,10 @@ namespace gfk {
 
 constexpr int kMaxGroups = 32;
 constexpr int kMaxLevels = 8;
-constexpr int kLeafMax = 4;
+#ifndef GF_LEAFMAX
+#define GF_LEAFMAX 4
+#endif
+constexpr int kLeafMax = GF_LEAFMAX;  // primitives per BVH leaf (<= 7: 3-bit count)
 constexpr uint32_t kLeafBit = 0x80000000u;
 
 struct __align__(16) GPrim {

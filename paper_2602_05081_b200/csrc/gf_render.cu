@@ -15,9 +15,18 @@
 
 namespace gfk {
 
-constexpr int kBins = 32;
+#ifndef GF_BINS
+#define GF_BINS 24
+#endif
+constexpr int kBins = GF_BINS;
 constexpr int kHitCap = 1024;  // hits recorded per path by ffA for ffB (overflow -> traversal gather)
-constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6, kWorkT = 7;
+constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6, kWorkT = 7;  // qcount slots: work cursors
+constexpr int kCntT = 8, kCntO = 9, kWorkAT = 10, kWorkAI = 11, kWorkAO = 12;  // record pass A queues
+constexpr int kCntB2 = 13, kWorkBW = 14;  // single-pass (record overflow) paths for ffB; warp ffB cursor
+#ifndef GF_REC_CAP
+#define GF_REC_CAP 1024
+#endif
+constexpr int kRecCap = GF_REC_CAP;  // 32-byte hit records per path (overflow -> single-pass ffA)
 
 template <bool COUNT, class F>
 __device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint32_t n_nodes,
@@ -229,8 +238,12 @@ __global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
 }
 
 // ---------------------------------------------------------------- ffA: binned tau over the ray
+// Single-pass version (traversal with the bin integrals inline).  Used for the paths whose hit
+// records overflow the record buffer of k_ffA_T (input queue q, counter slots cnt/work).
 template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t sample, int32_t depth,
+                                                           const uint32_t* __restrict__ q, int cnt_slot, int work_slot,
+                                                           int ray_count) {
     Work wk;
     Trav T;
     uint32_t p = 0;
@@ -260,10 +273,10 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
         fin_p = p;
     };
     flat_loop<COUNT, kBatch, GF_SPLIT_FFA>(
-        R.qcount + kWorkA, R.qcount[0], R.nodes, R.n_nodes, R.prims, T, wk,
+        R.qcount + work_slot, R.qcount[cnt_slot], R.nodes, R.n_nodes, R.prims, T, wk,
         [&](uint32_t idx) -> bool {
-            p = R.qA[idx];
-            began = true;
+            p = q[idx];
+            began = ray_count != 0;
             if (COUNT) ++wk.paths;
             const uint32_t pix = R.pix[p];
             const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
@@ -306,11 +319,245 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
             finish(-2, 0.0, 0.0, 0);
         },
         [&]() {
-            push(R.qB, R.qcount + 1, fin && collide, fin_p);
+            push(R.qB2, R.qcount + kCntB2, fin && collide, fin_p);
             count_rays(R.rays + 0, began);
             fin = false;
             began = false;
         });
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+}
+
+
+// ---------------------------------------------------------------- ffA as two kernels
+// k_ffA_T: lean traversal that emits one 32-byte record per accepted primitive,
+//   a = (u0, u1, Omega, phi0), b = (amp = c/j w e^{-(r2+Omega^2)/2} / 2, j, t_c, b'),
+// Gaussians (Omega == 0) from the front of the path's region, Gabors from the back;
+// k_ffA_I: one warp per path expands its records into erf endpoints (chord start, every bin
+//   boundary inside the chord, chord end; a symmetric single-bin chord needs one) and evaluates
+//   one endpoint per lane, type-uniform (real erf for the Gaussian part, the series for the Gabor
+//   part), accumulating the pieces into shared per-path bins; then brackets tau*.
+// Both read/write the records, which ffB also uses, so no primitive is reloaded after traversal.
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128, GF_MINB_NEE) k_ffA_T(RenderDev R, int32_t sample, int32_t depth) {
+    Work wk;
+    Trav T;
+    uint32_t p = 0, ng = 0, nb = 0;
+    double tstar = 0.0;
+    float w[kMaxGroups];
+    bool began = false, fin_b = false, fin_t = false, fin_o = false;
+    uint32_t fin_p = 0;
+    const uint32_t cap = (uint32_t)R.rec_cap;
+    auto finish_early = [&](int32_t bin) {
+        if (bin == -2) {
+            R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+        } else {
+            R.bin[p] = bin;
+            R.cum[p + R.n_paths] = tstar;
+            fin_b = true;
+            fin_p = p;
+        }
+    };
+    flat_loop<COUNT, kBatch, false>(
+        R.qcount + kWorkAT, R.qcount[0], R.nodes, R.n_nodes, R.prims, T, wk,
+        [&](uint32_t idx) -> bool {
+            p = R.qA[idx];
+            began = true;
+            if (COUNT) ++wk.paths;
+            const uint32_t pix = R.pix[p];
+            const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                     ST_EXT, 1, w)
+                                        : R.ext.static_mask;
+            const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
+            tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
+            if (tstar <= 0.0) { finish_early(-1); return false; }
+            const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+            float tlo, thi;
+            if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
+                finish_early(-2);
+                return false;
+            }
+            R.tlo[p] = tlo;
+            R.tbw[p] = (thi - tlo) * (1.0f / kBins);
+            R.cum[p + R.n_paths] = tstar;
+            ng = nb = 0;
+            trav_begin(T, r, tlo, thi, mask);
+            return true;
+        },
+        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
+            float cj = coef * s.ij;
+            if (STOCH) cj *= w[g];
+            if (ng + nb < cap) {
+                const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                const size_t slot = (size_t)p * cap + (s.Om == 0.0f ? ng : cap - 1 - nb);
+                float4* rp = R.rec + 2 * slot;
+                rp[0] = make_float4(s.u0, s.u1, s.Om, s.phi0);
+                rp[1] = make_float4(amp, s.j, s.tc, s.bp);
+            }
+            if (s.Om == 0.0f) ++ng; else ++nb;
+            return true;
+        },
+        [&]() {
+            fin_p = p;
+            if (ng + nb <= cap) {
+                R.nrg[p] = ng;
+                R.nrb[p] = nb;
+                fin_t = true;
+            } else {
+                R.nrg[p] = 0xFFFFFFFFu;  // overflow: the single-pass kernel redoes this path
+                fin_o = true;
+            }
+        },
+        [&]() {
+            push(R.qB, R.qcount + 1, fin_b, fin_p);
+            push(R.qT, R.qcount + kCntT, fin_t, fin_p);
+            push(R.qO, R.qcount + kCntO, fin_o, fin_p);
+            count_rays(R.rays + 0, began);
+            fin_b = fin_t = fin_o = began = false;
+        });
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+}
+
+// chord bin span of a record in the path's bins [tlo, tlo + kBins bw)
+__device__ __forceinline__ void rec_span(float4 a, float4 b, float tlo, float ibw, int& ka, int& kb) {
+    const float ij = 1.0f / b.y;
+    const float ta = fmaf(a.x - b.w, ij, b.z), tb = fmaf(a.y - b.w, ij, b.z);
+    ka = min(kBins - 1, max(0, (int)((ta - tlo) * ibw)));
+    kb = min(kBins - 1, max(0, (int)((tb - tlo) * ibw)));
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(128) k_ffA_I(RenderDev R) {
+    __shared__ float s_bins[4][kBins];
+    __shared__ uint32_t s_cnts[4][kBins];
+    __shared__ int s_off[4][33];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned FULL = 0xFFFFFFFFu;
+    float* bins = s_bins[wid];
+    uint32_t* cnts = s_cnts[wid];
+    int* off = s_off[wid];
+    const uint32_t count = R.qcount[kCntT], cap = (uint32_t)R.rec_cap;
+    Work wk;
+    while (true) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(R.qcount + kWorkAI, 1u);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= count) break;
+        const uint32_t p = R.qT[idx];
+        const float tlo = R.tlo[p], bw = R.tbw[p], ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
+        for (int k = lane; k < kBins; k += 32) { bins[k] = 0.0f; cnts[k] = 0; }
+        __syncwarp();
+        const uint32_t nside[2] = {R.nrg[p], R.nrb[p]};
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {  // 0: Gaussian records (real erf), 1: Gabor records (series)
+            const uint32_t n = nside[side];
+            for (uint32_t base = 0; base < n; base += 32) {
+                const uint32_t i = base + lane;
+                const bool valid = i < n;
+                float4 a = make_float4(0, 0, 0, 0), b = make_float4(0, 1, 0, 0);
+                int ka = 0, kb = 0, ne = 0;
+                if (valid) {
+                    const size_t slot = (size_t)p * cap + (side == 0 ? i : cap - 1 - i);
+                    a = R.rec[2 * slot];
+                    b = R.rec[2 * slot + 1];
+                    rec_span(a, b, tlo, ibw, ka, kb);
+                    for (int m = ka; m <= kb; ++m) atomicAdd(&cnts[m], 1u);
+                    const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
+                    if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
+                        // rare: midpoint / Gauss-Legendre pieces, lane-local (seg_J without e^{-r2/2}
+                        // and the 1/2 e^{-Om^2/2} folded into amp)
+                        Setup s;
+                        s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                        s.Om = a.z; s.phi0 = a.w;
+                        const float scale = 2.0f * b.x * __expf(0.5f * a.z * a.z);  // cj e^{-r2/2}
+                        float ua = a.x;
+                        for (int m = ka + 1; m <= kb + 1; ++m) {
+                            const float ub = (m > kb) ? a.y
+                                                      : fminf(fmaxf(fmaf(b.y, (tlo + m * bw) - b.z, b.w), ua), a.y);
+                            atomicAdd(&bins[m - 1], scale * seg_J(s, ua, ub, wk));
+                            ua = ub;
+                        }
+                    } else {
+                        ne = (ka == kb && a.x == -a.y) ? 1 : (kb - ka + 2);
+                    }
+                }
+                // exclusive prefix of endpoint counts over the chunk
+                int incl = ne;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                off[lane + 1] = incl;
+                if (lane == 0) off[0] = 0;
+                __syncwarp();
+                const int total = __shfl_sync(FULL, incl, 31);
+                for (int e0 = 0; e0 < total; e0 += 32) {
+                    const int e = e0 + lane;
+                    // owner record of endpoint e: largest r with off[r] <= e (binary search)
+                    int lo = 0, hi = 31;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (off[mid] <= e) lo = mid; else hi = mid - 1;
+                    }
+                    const int r = lo;
+                    const float u0 = __shfl_sync(FULL, a.x, r), u1 = __shfl_sync(FULL, a.y, r);
+                    const float Om = __shfl_sync(FULL, a.z, r), phi = __shfl_sync(FULL, a.w, r);
+                    const float amp = __shfl_sync(FULL, b.x, r), jj = __shfl_sync(FULL, b.y, r);
+                    const float tc = __shfl_sync(FULL, b.z, r), bp = __shfl_sync(FULL, b.w, r);
+                    const int rka = __shfl_sync(FULL, ka, r), rne = __shfl_sync(FULL, ne, r);
+                    if (e < total) {
+                        const int je = e - off[r];
+                        float u;
+                        if (rne == 1 || je == rne - 1) u = u1;
+                        else if (je == 0) u = u0;
+                        else u = fminf(fmaxf(fmaf(jj, (tlo + (rka + je) * bw) - tc, bp), u0), u1);
+                        float sp = 0.0f, cp = 1.0f;
+                        float2 F;
+                        if (side == 0) {
+                            F = make_float2(erff(u * kRsqrt2), 0.0f);
+                            if (phi != 0.0f) sincos_red(phi, &sp, &cp);  // Gabor along its modulation plane
+                            if (COUNT) ++wk.erfr;
+                        } else {
+                            const float zr = u * kRsqrt2, zi = -Om * kRsqrt2;
+                            F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
+                            sincos_red(phi, &sp, &cp);
+                            if (COUNT) ++wk.erfc;
+                        }
+                        if (rne == 1) {
+                            atomicAdd(&bins[rka], 2.0f * amp * cp * F.x);
+                        } else {
+                            const float v = amp * fmaf(cp, F.x, -sp * F.y);
+                            if (je >= 1) atomicAdd(&bins[rka + je - 1], v);
+                            if (je <= rne - 2) atomicAdd(&bins[rka + je], -v);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const double tstar = R.cum[p + R.n_paths];
+            int32_t bin = -2;
+            double cum = 0.0, cum_before = 0.0, bin_tau = 0.0;
+            uint32_t nact = 0;
+            for (int k = 0; k < kBins; ++k) {
+                const double c2 = cum + (double)bins[k];
+                if (c2 >= tstar) { bin = k; cum_before = cum; bin_tau = bins[k]; nact = cnts[k]; break; }
+                cum = c2;
+            }
+            if (bin == -2) {
+                R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+            } else {
+                R.bin[p] = bin | (int32_t)(min(nact, 32767u) << 16);
+                R.cum[p] = cum_before;
+                R.cum[p + 2 * R.n_paths] = bin_tau;
+                R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
+            }
+        }
+        __syncwarp();
+    }
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
 }
 
@@ -359,15 +606,18 @@ __device__ __forceinline__ double actb_tau(const ActB& a, float t, double& kap, 
     return (double)(a.amp * fmaf(a.cp, F.x - a.F0r, -a.sp * (F.y - a.F0i)));
 }
 
+// Per-thread version (local-memory active lists), used for the record-overflow paths (queue qB2);
+// each processed path is appended to qB for the NEE stage.
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_t depth) {
-    const uint32_t count = R.qcount[1];
+    const uint32_t count = R.qcount[kCntB2];
     uint32_t base;
     Work wk;
     while (fetch(R.qcount + kWorkB, count, base)) {
         const uint32_t idx = base + (threadIdx.x & 31);
         if (idx >= count) continue;
-        const uint32_t p = R.qB[idx];
+        const uint32_t p = R.qB2[idx];
+        R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
         const int32_t binw = R.bin[p];
         const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
         float tres = 0.0f;
@@ -417,8 +667,48 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
                     ++nb;
                 }
             };
-            const uint32_t nh = R.nhit[p];
-            if (nh <= (uint32_t)R.hit_cap) {  // scan the path's hit list from ffA (no traversal)
+            const bool recpath = R.nrg[p] != 0xFFFFFFFFu;
+            const uint32_t nh = recpath ? 0xFFFFFFFFu : R.nhit[p];
+            if (recpath) {  // the path's hit records from k_ffA_T: clip to the bracket, no primitive reload
+                const float ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
+                const uint32_t cap = (uint32_t)R.rec_cap;
+                const uint32_t nside[2] = {R.nrg[p], R.nrb[p]};
+                for (int side = 0; side < 2; ++side) {
+                    for (uint32_t i = 0; i < nside[side]; ++i) {
+                        const size_t slot = (size_t)p * cap + (side == 0 ? i : cap - 1 - i);
+                        const float4 a = R.rec[2 * slot], b = R.rec[2 * slot + 1];
+                        int ka, kb;
+                        rec_span(a, b, tlo, ibw, ka, kb);
+                        if (COUNT) ++wk.tests;
+                        if (ka > bin || kb < bin) continue;
+                        const float ua = fmaxf(a.x, fmaf(b.y, ta - b.z, b.w));
+                        const float ub = fminf(a.y, fmaf(b.y, tb - b.z, b.w));
+                        if (!(ub > ua)) continue;
+                        if (COUNT) ++wk.hits;
+                        const float kap0 = b.x * b.y * 0.79788456080286536f * __expf(0.5f * a.z * a.z);
+                        if (a.z == 0.0f && a.w == 0.0f) {
+                            if (ng < kCapG) {
+                                ActG& g = ag[ng];
+                                g.amp = b.x; g.kap0 = kap0; g.j = b.y; g.tc = b.z; g.bp = b.w; g.u0 = ua; g.u1 = ub;
+                                g.F0 = erff(ua * kRsqrt2);
+                                if (COUNT) ++wk.erfr;
+                            }
+                            ++ng;
+                        } else {
+                            if (nb < kCapB) {
+                                ActB& q = ab[nb];
+                                q.amp = b.x; q.kap0 = kap0; q.Om = a.z; q.phi0 = a.w; q.j = b.y; q.tc = b.z; q.bp = b.w;
+                                q.u0 = ua; q.u1 = ub;
+                                sincos_red(a.w, &q.sp, &q.cp);
+                                const float2 F0 = erf_shift(ua, a.z);
+                                if (COUNT) wk.erf(a.z, 1);
+                                q.F0r = F0.x; q.F0i = F0.y;
+                            }
+                            ++nb;
+                        }
+                    }
+                }
+            } else if (nh <= (uint32_t)R.hit_cap) {  // scan the path's hit list from single-pass ffA
                 for (uint32_t k = 0; k < nh; ++k) {
                     const uint2 e = R.hits[(size_t)p * R.hit_cap + k];
                     if ((int)(e.y & 0xFFu) > bin || (int)(e.y >> 8) < bin) continue;
@@ -499,6 +789,131 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFB, wk);
 }
 
+
+// ---------------------------------------------------------------- ffB, one warp per path
+// The bracket's active primitives are the path's hit records overlapping bin k.  Lanes scan the
+// records in parallel (coalesced); every Newton evaluation is a warp reduction of
+//   f(t) = cum0 - tau* + sum_i amp_i [G_i(clamp(u_i(t))) - G_i(lower_i)],  G = Re(e^{i phi} F),
+//   kappa(t) = sum_i kap0_i e^{-u^2/2} cos(phi_i + Omega_i u)      (derivative of tau, analytic),
+// so all lanes take the same (safeguarded Newton / bisection) steps.  No per-lane lists.
+template <bool COUNT>
+__global__ void __launch_bounds__(128) k_ffB_W(RenderDev R) {
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xFFFFFFFFu;
+    const uint32_t count = R.qcount[1], cap = (uint32_t)R.rec_cap;
+    Work wk;
+    while (true) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(R.qcount + kWorkBW, 1u);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= count) break;
+        const uint32_t p = R.qB[idx];
+        const int32_t binw = R.bin[p];
+        const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+        float tres = 0.0f;
+        if (binw >= 0) {
+            const int bin = binw & 0xFFFF;
+            const float tlo = R.tlo[p], bw = R.tbw[p], ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
+            const float ta = tlo + bin * bw;
+            const float tb = tlo + (bin + 1) * bw;
+            const float tbc = (bin == kBins - 1) ? INFINITY : tb;  // clip window (records end at thi)
+            const double tstar = R.cum[p + R.n_paths], cum0 = R.cum[p], span = R.cum[p + 2 * R.n_paths];
+            const uint32_t nside[2] = {R.nrg[p], R.nrb[p]};
+            // one scan over the records: mode 0 -> S0 = sum amp G(lower); mode 1 -> sum amp G(clamp(u_t)), kappa
+            auto scan = [&](int mode, float t, double& kap_out) -> double {
+                float acc = 0.0f, kap = 0.0f;
+#pragma unroll 1
+                for (int side = 0; side < 2; ++side) {
+                    for (uint32_t i = lane; i < nside[side]; i += 32) {
+                        const size_t slot = (size_t)p * cap + (side == 0 ? i : cap - 1 - i);
+                        const float4 a = R.rec[2 * slot], b = R.rec[2 * slot + 1];
+                        int ka, kb;
+                        rec_span(a, b, tlo, ibw, ka, kb);
+                        if (ka > bin || kb < bin) continue;
+                        const float lower = fmaxf(a.x, fmaf(b.y, ta - b.z, b.w));
+                        const float upper = fminf(a.y, fmaf(b.y, tbc - b.z, b.w));
+                        if (!(upper > lower)) continue;
+                        if (COUNT && mode == 0) ++wk.hits;
+                        const float wmax = 0.5f * (fmaxf(lower * lower, upper * upper) + a.z * a.z);
+                        const bool special = upper - lower < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f);
+                        float u = lower;
+                        if (mode == 1) {
+                            const float ut = fmaf(b.y, t - b.z, b.w);
+                            if (ut > lower && ut < upper) {
+                                float sp, cp;
+                                sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
+                                kap += b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut)) * cp;
+                            }
+                            u = fminf(fmaxf(ut, lower), upper);
+                        }
+                        if (special) {  // rare: midpoint / Gauss-Legendre from lower (no S0 term)
+                            if (mode == 1 && u > lower) {
+                                Setup s;
+                                s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                                s.Om = a.z; s.phi0 = a.w;
+                                acc += 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, lower, u, wk);
+                            }
+                            continue;
+                        }
+                        float2 F;
+                        float sp = 0.0f, cp = 1.0f;
+                        if (side == 0) {
+                            F = make_float2(erff(u * kRsqrt2), 0.0f);
+                            if (a.w != 0.0f) sincos_red(a.w, &sp, &cp);
+                            if (COUNT) ++wk.erfr;
+                        } else {
+                            const float zr = u * kRsqrt2, zi = -a.z * kRsqrt2;
+                            F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
+                            sincos_red(a.w, &sp, &cp);
+                            if (COUNT) ++wk.erfc;
+                        }
+                        acc += b.x * fmaf(cp, F.x, -sp * F.y);
+                    }
+                }
+                double x = acc, k = kap;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    x += __shfl_xor_sync(FULL, x, off);
+                    k += __shfl_xor_sync(FULL, k, off);
+                }
+                kap_out = k;
+                return x;
+            };
+            double kap;
+            const double S0 = scan(0, 0.0f, kap);
+            auto eval = [&](float t, double& kp) -> double {
+                if (COUNT) ++wk.root;
+                return cum0 - tstar - S0 + scan(1, t, kp);
+            };
+            float lo = ta, hi = tb;
+            const double need = tstar - cum0;
+            float t = ta + 0.5f * (tb - ta);
+            if (span > 0.0 && need >= 0.0) t = ta + (float)(need / span) * (tb - ta);
+            t = fminf(fmaxf(t, lo), hi);
+            for (int it = 0; it < 48; ++it) {
+                const double f = eval(t, kap);
+                if (f >= 0.0) hi = t; else lo = t;
+                if (!(hi - lo > 1e-6f * bw)) break;
+                if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
+                float tn = (kap > 0.0) ? (float)((double)t - f / kap) : 0.5f * (lo + hi);
+                const bool newton = tn > lo && tn < hi;
+                if (!newton) tn = 0.5f * (lo + hi);
+                const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
+                t = tn;
+                if (small) break;
+            }
+            tres = t;
+        }
+        if (lane == 0) {  // collision point becomes the new origin
+            R.ox[p] = fmaf(tres, d.x, o.x);
+            R.oy[p] = fmaf(tres, d.y, o.y);
+            R.oz[p] = fmaf(tres, d.z, o.z);
+        }
+        __syncwarp();
+    }
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFB, wk);
+}
+
 // ---------------------------------------------------------------- NEE + phase sampling
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t sample, int32_t depth) {
@@ -557,6 +972,8 @@ __global__ void k_rotate(uint32_t* qc) {
     qc[0] = qc[2];
     qc[1] = 0; qc[2] = 0;
     qc[kWorkA] = 0; qc[kWorkB] = 0; qc[kWorkN] = 0;
+    qc[kCntT] = 0; qc[kCntO] = 0; qc[kWorkAT] = 0; qc[kWorkAI] = 0; qc[kWorkAO] = 0;
+    qc[kCntB2] = 0; qc[kWorkBW] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_finish(RenderDev R, int32_t slot) {
@@ -587,12 +1004,17 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     double* cum = (double*)take(sizeof(double) * 3 * (size_t)n);
     int32_t* bin = (int32_t*)take(nu); uint32_t* pix = (uint32_t*)take(nu); uint32_t* nhit = (uint32_t*)take(nu);
     uint2* hits = (uint2*)take(sizeof(uint2) * (size_t)kHitCap * (size_t)n);
+    float4* rec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * (size_t)n);
+    uint32_t* nrg = (uint32_t*)take(nu); uint32_t* nrb = (uint32_t*)take(nu);
+    float* tlo = (float*)take(nf); float* tbw = (float*)take(nf);
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
+    uint32_t* qT = (uint32_t*)take(nu); uint32_t* qO = (uint32_t*)take(nu); uint32_t* qB2 = (uint32_t*)take(nu);
     uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
         R->cum = cum; R->bin = bin; R->pix = pix; R->nhit = nhit; R->hits = hits; R->hit_cap = kHitCap;
-        R->qA = qA; R->qB = qB; R->qNext = qN; R->qcount = qc;
+        R->rec = rec; R->rec_cap = kRecCap; R->nrg = nrg; R->nrb = nrb; R->tlo = tlo; R->tbw = tbw;
+        R->qA = qA; R->qB = qB; R->qNext = qN; R->qT = qT; R->qO = qO; R->qB2 = qB2; R->qcount = qc;
     }
     return off;
 }
@@ -604,9 +1026,18 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, cu
                          bool stoch_nee) {
     cudaEvent_t e;
     T.pre(STAGE_FFA, st, e);
-    k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    k_ffA_T<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    T.post(STAGE_FFA, st, e);
+    T.pre(STAGE_FFA, st, e);
+    k_ffA_I<C><<<pgrid, 128, 0, st>>>(R);
+    T.post(STAGE_FFA, st, e);
+    T.pre(STAGE_FFA, st, e);  // record-overflow paths: single-pass kernel
+    k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
     T.post(STAGE_FFA, st, e);
     T.pre(STAGE_FFB, st, e);
+    k_ffB_W<C><<<pgrid, 128, 0, st>>>(R);
+    T.post(STAGE_FFB, st, e);
+    T.pre(STAGE_FFB, st, e);  // record-overflow paths (appended to qB for NEE)
     k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFB, st, e);
     T.pre(STAGE_NEE, st, e);
