@@ -16,7 +16,7 @@
 namespace gfk {
 
 #ifndef GF_BINS
-#define GF_BINS 24
+#define GF_BINS 1
 #endif
 constexpr int kBins = GF_BINS;
 constexpr int kHitCap = 1024;  // hits recorded per path by ffA for ffB (overflow -> traversal gather)
