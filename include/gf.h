@@ -216,7 +216,7 @@ gf_status gf_render(gf_ctx *ctx, const gf_render_desc *desc, float *accum, void 
 #define GF_PROFILE_WORK 2u    /* use the counting kernel variants (work[] below; slower)          */
 /* Stages: 0 gen (camera rays), 1 ffA (free flight, binned tau), 2 ffB (root find), 3 nee (shadow
  * rays + phase sampling), 4 finish (queue rotation + accumulation), 5 tomo, 6 trace
- * (gf_trace_transmittance), 7 build (unused). */
+ * (gf_trace_transmittance), 7 integrate (warp-per-path integration of hit records). */
 typedef struct {
     uint64_t launches;           /* kernels launched by the library since the last reset        */
     uint64_t stage_launches[8];

@@ -52,7 +52,7 @@ struct TraceArgs {
 
 // Stage timing with CUDA events recorded on the launching stream (gf_set_profiling).
 enum { STAGE_GEN = 0, STAGE_FFA = 1, STAGE_FFB = 2, STAGE_NEE = 3, STAGE_FINISH = 4, STAGE_TOMO = 5,
-       STAGE_TRACE = 6, STAGE_BUILD = 7, N_STAGES = 8 };
+       STAGE_TRACE = 6, STAGE_FFAI = 7, N_STAGES = 8 };
 struct StageTimer {
     bool on = false;  // record events around every launch
     unsigned long long launches = 0;
@@ -101,6 +101,7 @@ struct RenderDev {
     float *tlo, *tbw;     // the path's bin origin and width
     uint32_t *qT, *qO;    // paths to integrate / record-overflow paths
     uint32_t* qB2;        // record-overflow paths after single-pass ffA (per-thread ffB)
+    uint32_t *qNT, *qNO;  // shadow rays to integrate / record-overflow shadow rays
     // queues
     uint32_t *qA, *qB, *qNext;
     uint32_t* qcount;  // [4]: A, B, next, overflow

@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(128) k_ffA_I(RenderDev R) {
         }
         __syncwarp();
     }
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFAI, wk);
 }
 
 // ---------------------------------------------------------------- ffB: root in the bracketing bin
@@ -1028,9 +1028,9 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, cu
     T.pre(STAGE_FFA, st, e);
     k_ffA_T<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFA, st, e);
-    T.pre(STAGE_FFA, st, e);
+    T.pre(STAGE_FFAI, st, e);
     k_ffA_I<C><<<pgrid, 128, 0, st>>>(R);
-    T.post(STAGE_FFA, st, e);
+    T.post(STAGE_FFAI, st, e);
     T.pre(STAGE_FFA, st, e);  // record-overflow paths: single-pass kernel
     k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
     T.post(STAGE_FFA, st, e);
