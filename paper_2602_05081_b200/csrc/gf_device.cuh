@@ -569,6 +569,8 @@ __device__ __forceinline__ bool trav_done(const Trav& T, uint32_t n_nodes) {
 // The op with the most eligible lanes wins, so node/prim/integral code never diverge against
 // each other.  Callbacks (lane-local): begin(idx) -> bool (false: item needs no traversal);
 // hit(setup, coef, group, sorted prim index) -> bool done (a hit may take several ops); end().  sync() is called by all lanes once per iteration.
+// BATCH = 0: no pending state -- hit() runs right inside the primitive-test op (for callbacks as
+// cheap as a record store).
 template <bool COUNT, int BATCH, bool SPLIT, class Begin, class Hit, class End, class Sync>
 __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const GNode* __restrict__ nodes,
                                           uint32_t n_nodes, const GPrim* __restrict__ prims, Trav& T, Work& wk,
@@ -637,10 +639,14 @@ __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const 
                         P.b = __ldg(&q->b); P.c = __ldg(&q->c); P.d = __ldg(&q->d);
                         if (prim_setup(P, T.r, T.t0, T.t1, s)) {
                             if (COUNT) ++wk.hits;
-                            coef = P.d.w;
-                            pg = g;
-                            pidx = k;
-                            pend = true;
+                            if (BATCH == 0) {
+                                hit(s, P.d.w, g, k);
+                            } else {
+                                coef = P.d.w;
+                                pg = g;
+                                pidx = k;
+                                pend = true;
+                            }
                         }
                     }
                 }

@@ -194,6 +194,12 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #ifndef GF_SPLIT_NEE
 #define GF_SPLIT_NEE 0
 #endif
+#ifndef GF_BATCH_T
+#define GF_BATCH_T 0  // record-emitting traversal: the hit callback (one 32-byte store) runs inline
+#endif
+#ifndef GF_MINB_T
+#define GF_MINB_T 8
+#endif
 constexpr int kBatch = GF_BATCH;  // integrate pending hits once this many lanes (or most blocked lanes) have one
 
 template <bool STOCH, bool COUNT>
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
 //   part), accumulating the pieces into shared per-path bins; then brackets tau*.
 // Both read/write the records, which ffB also uses, so no primitive is reloaded after traversal.
 template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128, GF_MINB_NEE) k_ffA_T(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128, GF_MINB_T) k_ffA_T(RenderDev R, int32_t sample, int32_t depth) {
     Work wk;
     Trav T;
     uint32_t p = 0, ng = 0, nb = 0;
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(128, GF_MINB_NEE) k_ffA_T(RenderDev R, int32_t
             fin_p = p;
         }
     };
-    flat_loop<COUNT, kBatch, false>(
+    flat_loop<COUNT, GF_BATCH_T, false>(
         R.qcount + kWorkAT, R.qcount[0], R.nodes, R.n_nodes, R.prims, T, wk,
         [&](uint32_t idx) -> bool {
             p = R.qA[idx];
