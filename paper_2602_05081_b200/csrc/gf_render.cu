@@ -180,7 +180,7 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 
 // tuning knobs (compile-time; bench variants are built with -D overrides)
 #ifndef GF_BATCH
-#define GF_BATCH 24
+#define GF_BATCH 0
 #endif
 #ifndef GF_MINB_FFA
 #define GF_MINB_FFA 6
