@@ -26,7 +26,10 @@ struct gf_ctx {
     GNode* nodes = nullptr;    // bvh_ws
     GPrim* sorted = nullptr;
     int32_t* perm = nullptr;   // sorted -> input index (bvh_ws, after the nodes)
+    GNode2* nodes2 = nullptr;  // children pairs (bvh_ws, after perm)
     uint32_t n_nodes = 0;
+    uint32_t max_depth = 0;
+    int32_t stk_limit = 0;
     float root[6] = {0, 0, 0, 0, 0, 0};
     // policies
     gf_lod_policy ext{0xFFFFFFFFu, 0, 0.0f, 0, 1.0f}, nee{0xFFFFFFFFu, 0, 0.0f, 0, 1.0f};
@@ -184,7 +187,8 @@ gf_status gf_query_workspace(int64_t n, size_t* prim_bytes, size_t* bvh_bytes, s
     const size_t n1 = (size_t)std::max<int64_t>(n, 1);
     if (prim_bytes) *prim_bytes = align256(sizeof(GPrim) * n1) + align256(n1);
     if (bvh_bytes)
-        *bvh_bytes = align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1) + align256(sizeof(int32_t) * n1);
+        *bvh_bytes = align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1) + align256(sizeof(int32_t) * n1) +
+                     align256(sizeof(GNode2) * 2 * n1);
     if (scratch_bytes) {
         if (n > 0) {
             int ndev = 0;
@@ -263,11 +267,18 @@ gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch,
     c->sorted = (GPrim*)base;
     c->nodes = (GNode*)(base + align256(sizeof(GPrim) * n1));
     c->perm = (int32_t*)(base + align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1));
+    c->nodes2 = (GNode2*)(base + align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1) +
+                          align256(sizeof(int32_t) * n1));
     BuildScratch S = gf_scratch_layout(c->n, (char*)scratch);
-    uint32_t nn = 0;
-    GF_CUDA(c, gf_launch_build(c->prims, c->group, c->n, S, c->nodes, c->sorted, c->perm, &nn, c->root, st),
+    uint32_t nn = 0, md = 0;
+    GF_CUDA(c, gf_launch_build(c->prims, c->group, c->n, S, c->nodes, c->nodes2, c->sorted, c->perm, &nn, &md, c->root,
+                               st),
             "gf_build_bvh");
+    // warp traversal stack bound (gf_device.cuh: warp_traverse)
+    if ((int)md + 34 + 64 > kWStk) return fail(c, GF_E_INVALID_ARGUMENT, "BVH deeper than the traversal stack allows");
     c->n_nodes = nn;
+    c->max_depth = md;
+    c->stk_limit = kWStk - 34 - (int)md;
     c->built = true;
     return GF_OK;
 }
@@ -296,6 +307,8 @@ static gf_status trace_common(gf_ctx* c, const float* rays, int64_t n, TraceArgs
     A = TraceArgs{};
     const bool brute = flags & GF_TRACE_BRUTE_FORCE;
     A.nodes = c->nodes;
+    A.nodes2 = c->nodes2;
+    A.stk_limit = c->stk_limit;
     A.n_nodes = c->built ? c->n_nodes : 0;
     A.prims = brute ? c->prims : c->sorted;
     A.group = c->group;
@@ -399,6 +412,8 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     RenderDev R{};
     gf_render_state_bytes(chunk, (char*)scratch, &R);
     R.nodes = c->nodes;
+    R.nodes2 = c->nodes2;
+    R.stk_limit = c->stk_limit;
     R.n_nodes = c->n_nodes;
     R.prims = c->sorted;
     R.ext = c->dext;

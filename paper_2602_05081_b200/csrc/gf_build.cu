@@ -252,6 +252,7 @@ struct LayoutArgs {
     const uint32_t *nmask, *ncount, *nsize;
     GNode* out;
     uint32_t total;
+    uint32_t* max_depth;
 };
 
 __global__ void k_layout(LayoutArgs A) {
@@ -264,14 +265,16 @@ __global__ void k_layout(LayoutArgs A) {
         if (collapsed(A.ncount[p], A.nmask[p])) return;  // inside a collapsed leaf
     }
     // pre-order index: walk to the root
-    uint32_t idx = 0;
+    uint32_t idx = 0, depth = 0;
     int64_t cur = x;
     while (cur != root) {
         int32_t p = A.parent[cur];
         idx += 1;
+        ++depth;
         if (A.right[p] == cur) idx += A.nsize[A.left[p]];
         cur = p;
     }
+    atomicMax(A.max_depth, depth);
     uint32_t cnt = A.ncount[x], m = A.nmask[x];
     bool leaf = collapsed(cnt, m);
     uint32_t skip = idx + A.nsize[x];
@@ -287,6 +290,26 @@ __global__ void k_layout(LayoutArgs A) {
     N.lo = make_float4(b[0], b[1], b[2], __uint_as_float(skip | (leaf ? kLeafBit : 0u)));
     N.hi = make_float4(b[3], b[4], b[5], __uint_as_float(info));
     A.out[idx] = N;
+}
+
+// children pairs for the warp traversal: internal node i has children i + 1 and skip(i + 1)
+__global__ void k_pair(const GNode* __restrict__ nodes, uint32_t total, GNode2* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const uint32_t sk = __float_as_uint(nodes[i].lo.w);
+    if (sk & kLeafBit) return;
+    const uint32_t c0 = i + 1;
+    const GNode a = nodes[c0];
+    const uint32_t c1 = __float_as_uint(a.lo.w) & ~kLeafBit;
+    const GNode b = nodes[c1];
+    const uint32_t r0 = (__float_as_uint(a.lo.w) & kLeafBit) ? kLeafBit : c0;
+    const uint32_t r1 = (__float_as_uint(b.lo.w) & kLeafBit) ? kLeafBit : c1;
+    GNode2 o;
+    o.lo0 = make_float4(a.lo.x, a.lo.y, a.lo.z, __uint_as_float(r0));
+    o.hi0 = a.hi;
+    o.lo1 = make_float4(b.lo.x, b.lo.y, b.lo.z, __uint_as_float(r1));
+    o.hi1 = b.hi;
+    out[i] = o;
 }
 
 __global__ void k_gather(const GPrim* in, const int32_t* perm, int64_t n, GPrim* out, int32_t* perm_out) {
@@ -346,11 +369,13 @@ BuildScratch gf_scratch_layout(int64_t n, char* base) {
 
 // builds into nodes/sorted; returns node count via *n_nodes (host, after sync)
 cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes_v,
-                            void* sorted_v, int32_t* perm, uint32_t* n_nodes, float* root_box, cudaStream_t st) {
+                            void* nodes2_v, void* sorted_v, int32_t* perm, uint32_t* n_nodes, uint32_t* max_depth,
+                            float* root_box, cudaStream_t st) {
     const GPrim* prims = (const GPrim*)prims_v;
     GNode* nodes = (GNode*)nodes_v;
     cudaError_t e;
     *n_nodes = 0;
+    *max_depth = 0;
     if (n == 0) return cudaSuccess;
     uint32_t init[8] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u, 0u};
     if ((e = cudaMemcpyAsync(S.cbounds, init, sizeof(init), cudaMemcpyHostToDevice, st))) return e;
@@ -371,10 +396,13 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
     uint32_t total = 0;
     if ((e = cudaMemcpyAsync(&total, S.nsize, sizeof(uint32_t), cudaMemcpyDeviceToHost, st))) return e;
     if ((e = cudaStreamSynchronize(st))) return e;
-    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, total};
+    if ((e = cudaMemsetAsync(S.cbounds, 0, sizeof(uint32_t), st))) return e;  // reused: max depth
+    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, total, S.cbounds};
     k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
+    k_pair<<<nblk(total, 256), 256, 0, st>>>(nodes, total, (GNode2*)nodes2_v);
     k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
     if ((e = cudaMemcpyAsync(root_box, S.nbox, sizeof(float) * 6, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaMemcpyAsync(max_depth, S.cbounds, sizeof(uint32_t), cudaMemcpyDeviceToHost, st))) return e;
     if ((e = cudaStreamSynchronize(st))) return e;
     *n_nodes = total;
     return cudaGetLastError();

@@ -8,6 +8,9 @@
 //   GNode  32 B  = 2 x float4 : (lo.xyz, skip | leaf<<31) (hi.xyz, info)
 //          depth-first layout, hit -> i+1, miss -> skip; info = group mask (internal) or
 //          first<<8 | count<<5 | group (leaf).
+//   GNode2 64 B  = the two children of internal node i (same DFS index): (lo.xyz, ref) (hi.xyz, info)
+//          per child, ref = the child's DFS index (internal) or kLeafBit (leaf); used by the
+//          warp-per-ray traversal, which tests both children of a node in one step.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -27,6 +30,9 @@ struct __align__(16) GPrim {
 };
 struct __align__(16) GNode {
     float4 lo, hi;
+};
+struct __align__(16) GNode2 {
+    float4 lo0, hi0, lo1, hi1;
 };
 
 // ------------------------------------------------------------------ policy (Tables B1/B2)
@@ -671,6 +677,203 @@ __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const 
             if (__any_sync(FULL, active && !pend && trav_done(T, n_nodes))) break;
         }
     }
+}
+
+// ------------------------------------------------------------------ warp-per-ray traversal
+// One warp owns one ray.  Its frontier lives in shared memory: a stack of internal nodes known
+// to be hit and a list of pending primitive references (sorted index | group << 27).  Every step
+// is one warp-uniform operation over up to 32 entries:
+//   PRIM  (>= 32 pending, or no node left): one primitive test per lane (a5), on_prims callback;
+//   NODE  pop up to 32 nodes, test both children of each (a4), push the hit internal children
+//         and append the primitives of the hit leaves (warp prefix sums, no atomics).
+// So node tests, primitive tests and (through the callbacks' queues) the integrals all run with
+// full warps instead of the divergent per-lane depth-first walk.  Stack bound: a full step grows
+// the stack by <= 32; above `stk_limit` one node per step is popped (depth-first, growth <= 1
+// per level), and stk_limit = kWStk - 34 - max_depth keeps it in bounds (gf_build_bvh).
+constexpr int kWStk = 512;
+constexpr int kWPrm = 32 + 64 * kLeafMax;
+struct WarpTrav {
+    uint32_t stk[kWStk];
+    uint32_t prm[kWPrm];
+};
+constexpr uint32_t kRefIdx = 0x07FFFFFFu;
+
+template <bool COUNT, class OnPrims>
+__device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
+                                              uint32_t n_nodes, int stk_limit, const RayDev& r, float t0, float t1,
+                                              uint32_t mask, WarpTrav& sm, Work& wk, OnPrims&& on_prims) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int ns = 0, np = 0;
+    if (n_nodes == 0) return;
+    {  // root
+        const float4 lo = __ldg(&nodes[0].lo), hi = __ldg(&nodes[0].hi);
+        const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+        if (COUNT && lane == 0) ++wk.nodes;
+        if (!((node_mask(sk, info) & mask) && slab(r, lo, hi, t0, t1))) return;
+        if (sk & kLeafBit) {
+            const int cnt = (int)((info >> 5) & 7u);
+            if (lane < cnt) sm.prm[lane] = ((info >> 8) + lane) | ((info & 31u) << 27);
+            np = cnt;
+        } else {
+            if (lane == 0) sm.stk[0] = 0;
+            ns = 1;
+        }
+        __syncwarp();
+    }
+    while (true) {
+        if (np >= 32 || (ns == 0 && np > 0)) {
+            const int take = min(np, 32);
+            const bool valid = lane < take;
+            const uint32_t ref = valid ? sm.prm[np - take + lane] : 0u;
+            np -= take;
+            __syncwarp();
+            on_prims(valid, ref);
+        } else if (ns > 0) {
+            const int take = ns > stk_limit ? 1 : min(ns, 32);
+            const bool valid = lane < take;
+            const uint32_t i = valid ? sm.stk[ns - take + lane] : 0u;
+            ns -= take;
+            __syncwarp();
+            bool h0 = false, h1 = false;
+            uint32_t ref0 = 0, ref1 = 0, inf0 = 0, inf1 = 0;
+            if (valid) {
+                const GNode2* q = n2 + i;
+                const float4 lo0 = __ldg(&q->lo0), hi0 = __ldg(&q->hi0), lo1 = __ldg(&q->lo1), hi1 = __ldg(&q->hi1);
+                ref0 = __float_as_uint(lo0.w); inf0 = __float_as_uint(hi0.w);
+                ref1 = __float_as_uint(lo1.w); inf1 = __float_as_uint(hi1.w);
+                h0 = (node_mask(ref0, inf0) & mask) && slab(r, lo0, hi0, t0, t1);
+                h1 = (node_mask(ref1, inf1) & mask) && slab(r, lo1, hi1, t0, t1);
+                if (COUNT) wk.nodes += 2;
+            }
+            const bool i0 = h0 && !(ref0 & kLeafBit), i1 = h1 && !(ref1 & kLeafBit);
+            const unsigned b0 = __ballot_sync(FULL, i0), b1 = __ballot_sync(FULL, i1);
+            if (i0) sm.stk[ns + __popc(b0 & lt)] = ref0;
+            if (i1) sm.stk[ns + __popc(b0) + __popc(b1 & lt)] = ref1;
+            ns += __popc(b0) + __popc(b1);
+            const uint32_t c0 = (h0 && (ref0 & kLeafBit)) ? ((inf0 >> 5) & 7u) : 0u;
+            const uint32_t c1 = (h1 && (ref1 & kLeafBit)) ? ((inf1 >> 5) & 7u) : 0u;
+            if (__any_sync(FULL, c0 + c1 > 0)) {
+                uint32_t incl = c0 + c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                uint32_t pos = (uint32_t)np + incl - (c0 + c1);
+                for (uint32_t k = 0; k < c0; ++k) sm.prm[pos + k] = ((inf0 >> 8) + k) | ((inf0 & 31u) << 27);
+                pos += c0;
+                for (uint32_t k = 0; k < c1; ++k) sm.prm[pos + k] = ((inf1 >> 8) + k) | ((inf1 & 31u) << 27);
+                np += (int)__shfl_sync(FULL, incl, 31);
+            }
+            __syncwarp();
+        } else {
+            break;
+        }
+    }
+}
+
+// Endpoint queues of the warp integrator: a hit's integral is Re{e^{i phi0} [F(u1) - F(u0)]} amp
+// (seg_J), i.e. one or two erf endpoints, each queued as (u, Omega, A, B) with the contribution
+// A Re F(u) + B Im F(u): symmetric full chord (F(h) - F(-h) = 2 Re F(h)): (h, Om, 2 amp cos phi0, 0);
+// otherwise (u1, Om, amp cos, -amp sin) and (u0, Om, -amp cos, amp sin).  Queue 0 holds the
+// Omega == 0 endpoints (real erf), queue 1 the series endpoints; a queue is evaluated 32 at a
+// time with one erf type per step.
+constexpr int kWEnd = 96;
+struct WarpEnd {
+    float4 e[2][kWEnd];
+};
+
+// tau of one ray (all 32 lanes call; the result is returned on every lane).  Weights w[g] apply
+// when STOCH (stochastic LOD masks).
+template <bool STOCH, bool COUNT>
+__device__ __forceinline__ double warp_tau(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
+                                           uint32_t n_nodes, int stk_limit, const GPrim* __restrict__ prims,
+                                           const RayDev& r, float t0, float t1, uint32_t mask, const float* w,
+                                           WarpTrav& sm, WarpEnd& q, Work& wk) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    double acc = 0.0;
+    int nq0 = 0, nq1 = 0;
+    auto run = [&](int t, int take) {
+        int& nq = t == 0 ? nq0 : nq1;
+        const bool valid = lane < take;
+        const float4 e = valid ? q.e[t][nq - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        nq -= take;
+        __syncwarp();
+        if (valid) {
+            const float zr = e.x * kRsqrt2;
+            if (t == 0) {
+                if (COUNT) ++wk.erfr;
+                acc += (double)(e.z * erff(zr));
+            } else {
+                if (COUNT) ++wk.erfc;
+                const float zi = -e.y * kRsqrt2;
+                const float2 F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
+                acc += (double)fmaf(e.z, F.x, e.w * F.y);
+            }
+        }
+    };
+    warp_traverse<COUNT>(nodes, n2, n_nodes, stk_limit, r, t0, t1, mask, sm, wk, [&](bool valid, uint32_t ref) {
+        int ne = 0;
+        bool real = false;
+        float4 e0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), e1 = e0;
+        if (valid) {
+            const uint32_t k = ref & kRefIdx;
+            const GPrim* pp = prims + k;
+            GPrim P;
+            P.a = __ldg(&pp->a);
+            if (COUNT) ++wk.tests;
+            Setup s;
+            if (sphere_pretest(P.a, r, t0, t1)) {
+                P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                if (prim_setup(P, r, t0, t1, s)) {
+                    if (COUNT) ++wk.hits;
+                    float cj = P.d.w * s.ij;
+                    if (STOCH) cj *= w[ref >> 27];
+                    float res;
+                    if (seg_J_special(s, s.u0, s.u1, res, wk)) {
+                        acc += (double)(cj * res);  // rare: midpoint / Gauss-Legendre, lane-local
+                    } else {
+                        const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                        float sp, cp;
+                        sincos_red(s.phi0, &sp, &cp);
+                        real = s.Om == 0.0f;
+                        if (s.u0 == -s.h && s.u1 == s.h) {
+                            ne = 1;
+                            e0 = make_float4(s.u1, s.Om, 2.0f * amp * cp, 0.0f);
+                        } else {
+                            ne = 2;
+                            e0 = make_float4(s.u1, s.Om, amp * cp, -amp * sp);
+                            e1 = make_float4(s.u0, s.Om, -amp * cp, amp * sp);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const bool mine = ne > 0 && (real == (t == 0));
+            const unsigned m1 = __ballot_sync(FULL, mine), m2 = __ballot_sync(FULL, mine && ne == 2);
+            if (m1) {
+                int& nq = t == 0 ? nq0 : nq1;
+                if (mine) {
+                    q.e[t][nq + __popc(m1 & lt)] = e0;
+                    if (ne == 2) q.e[t][nq + __popc(m1) + __popc(m2 & lt)] = e1;
+                }
+                nq += __popc(m1) + __popc(m2);
+                __syncwarp();
+                while (nq >= 32) run(t, 32);
+            }
+        }
+    });
+    while (nq0 > 0) run(0, min(nq0, 32));
+    while (nq1 > 0) run(1, min(nq1, 32));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+    return acc;
 }
 
 }  // namespace gfk

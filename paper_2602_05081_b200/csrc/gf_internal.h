@@ -31,7 +31,9 @@ struct BuildScratch {
 
 struct TraceArgs {
     const gfk::GNode* nodes;
+    const gfk::GNode2* nodes2;
     uint32_t n_nodes;
+    int32_t stk_limit;
     const gfk::GPrim* prims;  // BVH order (sorted) or input order (brute force)
     const uint8_t* group;     // input-order group ids (brute force)
     const int32_t* perm;      // sorted -> input index (candidates)
@@ -69,7 +71,9 @@ struct StageTimer {
 // render launch state (see gf_render.cu)
 struct RenderDev {
     const gfk::GNode* nodes;
+    const gfk::GNode2* nodes2;
     uint32_t n_nodes;
+    int32_t stk_limit;
     const gfk::GPrim* prims;
     gfk::PolicyDev ext, nee;
     gfk::SceneDev sc;
@@ -114,7 +118,8 @@ cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_
 size_t gf_sort_temp_bytes(int64_t n);
 BuildScratch gf_scratch_layout(int64_t n, char* base);
 cudaError_t gf_launch_build(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes,
-                            void* sorted, int32_t* perm, uint32_t* n_nodes, float* root_box, cudaStream_t st);
+                            void* nodes2, void* sorted, int32_t* perm, uint32_t* n_nodes, uint32_t* max_depth,
+                            float* root_box, cudaStream_t st);
 cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
 cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
 size_t gf_render_state_bytes(int64_t n_paths, char* base, RenderDev* R);

@@ -974,6 +974,83 @@ __global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t s
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
 }
 
+// NEE, one warp per path (warp_tau): shadow-ray transmittance, HG phase sampling of the next
+// direction.  Replaces the per-lane k_nee on the production path.
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int32_t depth) {
+    __shared__ WarpTrav s_t[4];
+    __shared__ WarpEnd s_e[4];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t count = R.qcount[1];
+    Work wk;
+    uint32_t nray = 0;
+    while (true) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(R.qcount + kWorkN, 1u);
+        idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+        if (idx >= count) break;
+        const uint32_t p = R.qB[idx];
+        const uint32_t pix = R.pix[p];
+        if (COUNT && lane == 0) ++wk.paths;
+        ++nray;
+        const float3 x = ld3(R.ox, R.oy, R.oz, p);
+        float w[kMaxGroups];
+        const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                 ST_NEE, 0, w)
+                                    : R.nee.static_mask;
+        const double tau = warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims,
+                                                  make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask, w,
+                                                  s_t[wid], s_e[wid], wk);
+        if (lane == 0) {
+            const float3 d = ld3(R.dx, R.dy, R.dz, p);
+            const float beta = R.beta[p];
+            const float cost = d.x * R.sun.x + d.y * R.sun.y + d.z * R.sun.z;
+            R.L[p] += beta * R.albedo * hg_eval(R.hg_g, cost) * (float)exp(-tau) * R.sun_E;
+            if (depth + 1 < R.max_depth) {
+                uint4 b = stream_block(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_SCAT, 0);
+                float3 nd = hg_sample(R.hg_g, d, u01(b.x), u01(b.y));
+                R.dx[p] = nd.x; R.dy[p] = nd.y; R.dz[p] = nd.z;
+                R.beta[p] = beta * R.albedo;
+                R.qNext[atomicAdd(R.qcount + 2, 1u)] = p;
+            }
+        }
+    }
+    if (lane == 0 && nray) atomicAdd(R.rays + 1, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
+}
+
+// tomography (mode 0), one warp per pixel: L = tau of the camera ray
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_tomo_w(RenderDev R, int32_t sample) {
+    __shared__ WarpTrav s_t[4];
+    __shared__ WarpEnd s_e[4];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Work wk;
+    uint32_t nray = 0;
+    for (int64_t p = (int64_t)blockIdx.x * 4 + wid; p < R.n_paths; p += (int64_t)gridDim.x * 4) {
+        const int32_t pix = path_pixel(R, p);
+        if (pix < 0) continue;
+        float jx = 0.5f, jy = 0.5f;
+        if (R.jitter) {
+            uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
+            jx = u01(b.x); jy = u01(b.y);
+        }
+        float3 o, d;
+        camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+        float w[kMaxGroups];
+        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_EXT, 1, w)
+                                    : R.ext.static_mask;
+        if (COUNT && lane == 0) ++wk.paths;
+        ++nray;
+        const double tau = warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims,
+                                                  make_ray(o, d, 0.0f, INFINITY), 0.0f, INFINITY, mask, w, s_t[wid],
+                                                  s_e[wid], wk);
+        if (lane == 0) R.L[p] = (float)tau;
+    }
+    if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
+}
+
 __global__ void k_rotate(uint32_t* qc) {
     qc[0] = qc[2];
     qc[1] = 0; qc[2] = 0;
@@ -1028,7 +1105,8 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
 static int g_persist_blocks = 0;
 
 template <bool S, bool C>
-static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, cudaStream_t st, StageTimer& T,
+static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, unsigned wgrid, cudaStream_t st,
+                         StageTimer& T,
                          bool stoch_nee) {
     cudaEvent_t e;
     T.pre(STAGE_FFA, st, e);
@@ -1047,8 +1125,8 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, cu
     k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFB, st, e);
     T.pre(STAGE_NEE, st, e);
-    if (stoch_nee) k_nee<true, C><<<pgrid, 128, 0, st>>>(R, sample, d);
-    else k_nee<false, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    if (stoch_nee) k_nee_w<true, C><<<wgrid, 128, 0, st>>>(R, sample, d);
+    else k_nee_w<false, C><<<wgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_NEE, st, e);
 }
 
@@ -1066,16 +1144,17 @@ cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cu
     const bool stoch_nee = !(R.nee.ls == 0 && R.nee.os == 0);
     const unsigned grid = (unsigned)((R.n_paths + 127) / 128);
     const unsigned pgrid = (unsigned)std::min<int64_t>((int64_t)g_persist_blocks, (R.n_paths + 127) / 128);
+    const unsigned wgrid = (unsigned)std::min<int64_t>((int64_t)g_persist_blocks, (R.n_paths + 3) / 4);  // warp/path
     if ((e = cudaMemsetAsync(R.qcount, 0, sizeof(uint32_t) * 16, st))) return e;
     cudaEvent_t ev;
     if (R.mode == 0) {
         T.pre(STAGE_TOMO, st, ev);
         if (stoch_ext) {
-            if (cnt) k_tomo<true, true><<<pgrid, 128, 0, st>>>(R, sample);
-            else k_tomo<true, false><<<pgrid, 128, 0, st>>>(R, sample);
+            if (cnt) k_tomo_w<true, true><<<wgrid, 128, 0, st>>>(R, sample);
+            else k_tomo_w<true, false><<<wgrid, 128, 0, st>>>(R, sample);
         } else {
-            if (cnt) k_tomo<false, true><<<pgrid, 128, 0, st>>>(R, sample);
-            else k_tomo<false, false><<<pgrid, 128, 0, st>>>(R, sample);
+            if (cnt) k_tomo_w<false, true><<<wgrid, 128, 0, st>>>(R, sample);
+            else k_tomo_w<false, false><<<wgrid, 128, 0, st>>>(R, sample);
         }
         T.post(STAGE_TOMO, st, ev);
     } else {
@@ -1084,11 +1163,11 @@ cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cu
         T.post(STAGE_GEN, st, ev);
         for (int d = 0; d < R.max_depth; ++d) {
             if (stoch_ext) {
-                if (cnt) launch_depth<true, true>(R, sample, d, pgrid, st, T, stoch_nee);
-                else launch_depth<true, false>(R, sample, d, pgrid, st, T, stoch_nee);
+                if (cnt) launch_depth<true, true>(R, sample, d, pgrid, wgrid, st, T, stoch_nee);
+                else launch_depth<true, false>(R, sample, d, pgrid, wgrid, st, T, stoch_nee);
             } else {
-                if (cnt) launch_depth<false, true>(R, sample, d, pgrid, st, T, stoch_nee);
-                else launch_depth<false, false>(R, sample, d, pgrid, st, T, stoch_nee);
+                if (cnt) launch_depth<false, true>(R, sample, d, pgrid, wgrid, st, T, stoch_nee);
+                else launch_depth<false, false>(R, sample, d, pgrid, wgrid, st, T, stoch_nee);
             }
             T.pre(STAGE_FINISH, st, ev);
             k_rotate<<<1, 1, 0, st>>>(R.qcount);

@@ -1,5 +1,7 @@
 // gf_trace.cu -- a4 masked all-hits traversal + a5 ellipsoid clip + a6 fused line integral
 // + a7 transmittance (Eq. 2-3; masks P:L344-L350).
+#include <algorithm>
+
 #include "gf_device.cuh"
 #include "gf_internal.h"
 
@@ -93,6 +95,48 @@ __global__ void __launch_bounds__(128) k_trace(TraceArgs A) {
     }
 }
 
+// BVH path: one warp per ray (warp_traverse + endpoint queues, gf_device.cuh)
+template <bool COUNT, bool STOCH>
+__global__ void __launch_bounds__(128) k_trace_w(TraceArgs A) {
+    __shared__ WarpTrav s_t[4];
+    __shared__ WarpEnd s_e[4];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Work tot;
+    for (int64_t i = (int64_t)blockIdx.x * 4 + wid; i < A.n; i += (int64_t)gridDim.x * 4) {
+        const float4 r0 = __ldg((const float4*)A.rays + 2 * i);
+        const float4 r1 = __ldg((const float4*)A.rays + 2 * i + 1);
+        const float3 o = make_float3(r0.x, r0.y, r0.z), d = make_float3(r1.x, r1.y, r1.z);
+        const RayDev r = make_ray(o, d, r0.w, r1.w);
+        float w[kMaxGroups];
+        uint32_t mask;
+        if (STOCH) mask = policy_for(A.pol, A.sc, d, A.seed, (uint32_t)i, 0, 0, ST_EXT, 1, w);
+        else mask = A.pol.static_mask;
+        Work wk;
+        const double tau = warp_tau<STOCH, COUNT>(A.nodes, A.nodes2, A.n_nodes, A.stk_limit, A.prims, r, r.tmin,
+                                                  r.tmax, mask, w, s_t[wid], s_e[wid], wk);
+        if (lane == 0) {
+            A.tau[i] = (float)tau;
+            if (A.T) A.T[i] = (float)exp(-tau);
+        }
+        if (COUNT) {
+            uint32_t v[3] = {wk.nodes, wk.tests, wk.hits};
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
+            if (lane == 0 && A.counters) {
+                A.counters[3 * i] = v[0];
+                A.counters[3 * i + 1] = v[1];
+                A.counters[3 * i + 2] = v[2];
+            }
+            tot.nodes += wk.nodes; tot.tests += wk.tests; tot.hits += wk.hits;
+            tot.erfc += wk.erfc; tot.erfr += wk.erfr; tot.gl += wk.gl;
+            if (lane == 0) ++tot.paths;
+        }
+    }
+    if (COUNT && A.work) flush_work(A.work + kWorkSlots * STAGE_TRACE, tot);
+}
+
 template <bool BRUTE>
 __global__ void __launch_bounds__(128) k_candidates(TraceArgs A) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -129,8 +173,20 @@ cudaError_t gf_launch_trace(const TraceArgs& A, bool brute_force, bool count, cu
         if (count) { if (stoch) GF_T(true, true, true); else GF_T(true, true, false); }
         else { if (stoch) GF_T(true, false, true); else GF_T(true, false, false); }
     } else {
-        if (count) { if (stoch) GF_T(false, true, true); else GF_T(false, true, false); }
-        else { if (stoch) GF_T(false, false, true); else GF_T(false, false, false); }
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const unsigned wgrid = (unsigned)std::min<int64_t>((A.n + 3) / 4, (int64_t)sms * 16);
+        if (count) {
+            if (stoch) k_trace_w<true, true><<<wgrid, 128, 0, st>>>(A);
+            else k_trace_w<true, false><<<wgrid, 128, 0, st>>>(A);
+        } else {
+            if (stoch) k_trace_w<false, true><<<wgrid, 128, 0, st>>>(A);
+            else k_trace_w<false, false><<<wgrid, 128, 0, st>>>(A);
+        }
     }
 #undef GF_T
     return cudaGetLastError();

@@ -1,0 +1,14 @@
+#!/bin/bash
+# round-end style measurement: gpu tests, full bench, launch list, full captures of the top kernels
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
+timeout 300 python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/plain.log 2>&1; rc=$?; echo "plain rc=$rc"
+if [ $rc = 0 ]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu1.log 2>&1; echo "ncu launches rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_nee -s 4 -c 1 -f -o gpurun_out/prof_nee \
+    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu2.log 2>&1; echo "ncu nee rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ffA_T -s 4 -c 1 -f -o gpurun_out/prof_ffAT \
+    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu3.log 2>&1; echo "ncu ffAT rc=$?"
+fi
