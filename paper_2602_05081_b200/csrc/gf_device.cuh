@@ -761,10 +761,14 @@ __device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, c
                     const uint32_t v = __shfl_up_sync(FULL, incl, o);
                     if (lane >= o) incl += v;
                 }
-                uint32_t pos = (uint32_t)np + incl - (c0 + c1);
-                for (uint32_t k = 0; k < c0; ++k) sm.prm[pos + k] = ((inf0 >> 8) + k) | ((inf0 & 31u) << 27);
-                pos += c0;
-                for (uint32_t k = 0; k < c1; ++k) sm.prm[pos + k] = ((inf1 >> 8) + k) | ((inf1 & 31u) << 27);
+                const uint32_t pos = (uint32_t)np + incl - (c0 + c1);
+                const uint32_t v0 = (inf0 >> 8) | ((inf0 & 31u) << 27), v1 = (inf1 >> 8) | ((inf1 & 31u) << 27);
+#pragma unroll
+                for (uint32_t k = 0; k < (uint32_t)kLeafMax; ++k)  // predicated, no divergent loop
+                    if (k < c0) sm.prm[pos + k] = v0 + k;
+#pragma unroll
+                for (uint32_t k = 0; k < (uint32_t)kLeafMax; ++k)
+                    if (k < c1) sm.prm[pos + c0 + k] = v1 + k;
                 np += (int)__shfl_sync(FULL, incl, 31);
             }
             __syncwarp();

@@ -99,13 +99,11 @@ struct RenderDev {
     uint32_t* nhit;  // hits recorded by ffA
     uint2* hits;     // [n_paths][hit_cap]: sorted prim index | group << 24, bin span ka | kb << 8
     int32_t hit_cap;
-    float4* rec;     // [n_paths][rec_cap] x 2 float4 hit records (k_ffA_T -> k_ffA_I, k_ffB)
+    float4* wrec;    // [k_ff warp][rec_cap] x 2 float4 hit records (per warp, reused across paths)
+    float4* waux;    // [k_ff warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;
-    uint32_t *nrg, *nrb;  // Gaussian / Gabor record counts per path (nrg = ~0: record overflow)
-    float *tlo, *tbw;     // the path's bin origin and width
-    uint32_t *qT, *qO;    // paths to integrate / record-overflow paths
-    uint32_t* qB2;        // record-overflow paths after single-pass ffA (per-thread ffB)
-    uint32_t *qNT, *qNO;  // shadow rays to integrate / record-overflow shadow rays
+    uint32_t* qO;    // record-overflow paths (single-pass k_ffA)
+    uint32_t* qB2;   // record-overflow paths after single-pass ffA (per-thread ffB)
     // queues
     uint32_t *qA, *qB, *qNext;
     uint32_t* qcount;  // [4]: A, B, next, overflow

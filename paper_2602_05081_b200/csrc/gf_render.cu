@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
 
 // ---------------------------------------------------------------- ffA: binned tau over the ray
 // Single-pass version (traversal with the bin integrals inline).  Used for the paths whose hit
-// records overflow the record buffer of k_ffA_T (input queue q, counter slots cnt/work).
+// records overflow the record buffer of k_ff (input queue q, counter slots cnt/work).
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t sample, int32_t depth,
                                                            const uint32_t* __restrict__ q, int cnt_slot, int work_slot,
@@ -333,239 +333,6 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
 }
 
-
-// ---------------------------------------------------------------- ffA as two kernels
-// k_ffA_T: lean traversal that emits one 32-byte record per accepted primitive,
-//   a = (u0, u1, Omega, phi0), b = (amp = c/j w e^{-(r2+Omega^2)/2} / 2, j, t_c, b'),
-// Gaussians (Omega == 0) from the front of the path's region, Gabors from the back;
-// k_ffA_I: one warp per path expands its records into erf endpoints (chord start, every bin
-//   boundary inside the chord, chord end; a symmetric single-bin chord needs one) and evaluates
-//   one endpoint per lane, type-uniform (real erf for the Gaussian part, the series for the Gabor
-//   part), accumulating the pieces into shared per-path bins; then brackets tau*.
-// Both read/write the records, which ffB also uses, so no primitive is reloaded after traversal.
-template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128, GF_MINB_T) k_ffA_T(RenderDev R, int32_t sample, int32_t depth) {
-    Work wk;
-    Trav T;
-    uint32_t p = 0, ng = 0, nb = 0;
-    double tstar = 0.0;
-    float w[kMaxGroups];
-    bool began = false, fin_b = false, fin_t = false, fin_o = false;
-    uint32_t fin_p = 0;
-    const uint32_t cap = (uint32_t)R.rec_cap;
-    auto finish_early = [&](int32_t bin) {
-        if (bin == -2) {
-            R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
-        } else {
-            R.bin[p] = bin;
-            R.cum[p + R.n_paths] = tstar;
-            fin_b = true;
-            fin_p = p;
-        }
-    };
-    flat_loop<COUNT, GF_BATCH_T, false>(
-        R.qcount + kWorkAT, R.qcount[0], R.nodes, R.n_nodes, R.prims, T, wk,
-        [&](uint32_t idx) -> bool {
-            p = R.qA[idx];
-            began = true;
-            if (COUNT) ++wk.paths;
-            const uint32_t pix = R.pix[p];
-            const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
-            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
-                                                     ST_EXT, 1, w)
-                                        : R.ext.static_mask;
-            const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
-            tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
-            if (tstar <= 0.0) { finish_early(-1); return false; }
-            const RayDev r = make_ray(o, d, 0.0f, INFINITY);
-            float tlo, thi;
-            if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
-                finish_early(-2);
-                return false;
-            }
-            R.tlo[p] = tlo;
-            R.tbw[p] = (thi - tlo) * (1.0f / kBins);
-            R.cum[p + R.n_paths] = tstar;
-            ng = nb = 0;
-            trav_begin(T, r, tlo, thi, mask);
-            return true;
-        },
-        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
-            float cj = coef * s.ij;
-            if (STOCH) cj *= w[g];
-            if (ng + nb < cap) {
-                const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
-                const size_t slot = (size_t)p * cap + (s.Om == 0.0f ? ng : cap - 1 - nb);
-                float4* rp = R.rec + 2 * slot;
-                rp[0] = make_float4(s.u0, s.u1, s.Om, s.phi0);
-                rp[1] = make_float4(amp, s.j, s.tc, s.bp);
-            }
-            if (s.Om == 0.0f) ++ng; else ++nb;
-            return true;
-        },
-        [&]() {
-            fin_p = p;
-            if (ng + nb <= cap) {
-                R.nrg[p] = ng;
-                R.nrb[p] = nb;
-                fin_t = true;
-            } else {
-                R.nrg[p] = 0xFFFFFFFFu;  // overflow: the single-pass kernel redoes this path
-                fin_o = true;
-            }
-        },
-        [&]() {
-            push(R.qB, R.qcount + 1, fin_b, fin_p);
-            push(R.qT, R.qcount + kCntT, fin_t, fin_p);
-            push(R.qO, R.qcount + kCntO, fin_o, fin_p);
-            count_rays(R.rays + 0, began);
-            fin_b = fin_t = fin_o = began = false;
-        });
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
-}
-
-// chord bin span of a record in the path's bins [tlo, tlo + kBins bw)
-__device__ __forceinline__ void rec_span(float4 a, float4 b, float tlo, float ibw, int& ka, int& kb) {
-    const float ij = 1.0f / b.y;
-    const float ta = fmaf(a.x - b.w, ij, b.z), tb = fmaf(a.y - b.w, ij, b.z);
-    ka = min(kBins - 1, max(0, (int)((ta - tlo) * ibw)));
-    kb = min(kBins - 1, max(0, (int)((tb - tlo) * ibw)));
-}
-
-template <bool COUNT>
-__global__ void __launch_bounds__(128) k_ffA_I(RenderDev R) {
-    __shared__ float s_bins[4][kBins];
-    __shared__ uint32_t s_cnts[4][kBins];
-    __shared__ int s_off[4][33];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned FULL = 0xFFFFFFFFu;
-    float* bins = s_bins[wid];
-    uint32_t* cnts = s_cnts[wid];
-    int* off = s_off[wid];
-    const uint32_t count = R.qcount[kCntT], cap = (uint32_t)R.rec_cap;
-    Work wk;
-    while (true) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(R.qcount + kWorkAI, 1u);
-        idx = __shfl_sync(FULL, idx, 0);
-        if (idx >= count) break;
-        const uint32_t p = R.qT[idx];
-        const float tlo = R.tlo[p], bw = R.tbw[p], ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
-        for (int k = lane; k < kBins; k += 32) { bins[k] = 0.0f; cnts[k] = 0; }
-        __syncwarp();
-        const uint32_t nside[2] = {R.nrg[p], R.nrb[p]};
-#pragma unroll 1
-        for (int side = 0; side < 2; ++side) {  // 0: Gaussian records (real erf), 1: Gabor records (series)
-            const uint32_t n = nside[side];
-            for (uint32_t base = 0; base < n; base += 32) {
-                const uint32_t i = base + lane;
-                const bool valid = i < n;
-                float4 a = make_float4(0, 0, 0, 0), b = make_float4(0, 1, 0, 0);
-                int ka = 0, kb = 0, ne = 0;
-                if (valid) {
-                    const size_t slot = (size_t)p * cap + (side == 0 ? i : cap - 1 - i);
-                    a = R.rec[2 * slot];
-                    b = R.rec[2 * slot + 1];
-                    rec_span(a, b, tlo, ibw, ka, kb);
-                    for (int m = ka; m <= kb; ++m) atomicAdd(&cnts[m], 1u);
-                    const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
-                    if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
-                        // rare: midpoint / Gauss-Legendre pieces, lane-local (seg_J without e^{-r2/2}
-                        // and the 1/2 e^{-Om^2/2} folded into amp)
-                        Setup s;
-                        s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
-                        s.Om = a.z; s.phi0 = a.w;
-                        const float scale = 2.0f * b.x * __expf(0.5f * a.z * a.z);  // cj e^{-r2/2}
-                        float ua = a.x;
-                        for (int m = ka + 1; m <= kb + 1; ++m) {
-                            const float ub = (m > kb) ? a.y
-                                                      : fminf(fmaxf(fmaf(b.y, (tlo + m * bw) - b.z, b.w), ua), a.y);
-                            atomicAdd(&bins[m - 1], scale * seg_J(s, ua, ub, wk));
-                            ua = ub;
-                        }
-                    } else {
-                        ne = (ka == kb && a.x == -a.y) ? 1 : (kb - ka + 2);
-                    }
-                }
-                // exclusive prefix of endpoint counts over the chunk
-                int incl = ne;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(FULL, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                off[lane + 1] = incl;
-                if (lane == 0) off[0] = 0;
-                __syncwarp();
-                const int total = __shfl_sync(FULL, incl, 31);
-                for (int e0 = 0; e0 < total; e0 += 32) {
-                    const int e = e0 + lane;
-                    // owner record of endpoint e: largest r with off[r] <= e (binary search)
-                    int lo = 0, hi = 31;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (off[mid] <= e) lo = mid; else hi = mid - 1;
-                    }
-                    const int r = lo;
-                    const float u0 = __shfl_sync(FULL, a.x, r), u1 = __shfl_sync(FULL, a.y, r);
-                    const float Om = __shfl_sync(FULL, a.z, r), phi = __shfl_sync(FULL, a.w, r);
-                    const float amp = __shfl_sync(FULL, b.x, r), jj = __shfl_sync(FULL, b.y, r);
-                    const float tc = __shfl_sync(FULL, b.z, r), bp = __shfl_sync(FULL, b.w, r);
-                    const int rka = __shfl_sync(FULL, ka, r), rne = __shfl_sync(FULL, ne, r);
-                    if (e < total) {
-                        const int je = e - off[r];
-                        float u;
-                        if (rne == 1 || je == rne - 1) u = u1;
-                        else if (je == 0) u = u0;
-                        else u = fminf(fmaxf(fmaf(jj, (tlo + (rka + je) * bw) - tc, bp), u0), u1);
-                        float sp = 0.0f, cp = 1.0f;
-                        float2 F;
-                        if (side == 0) {
-                            F = make_float2(erff(u * kRsqrt2), 0.0f);
-                            if (phi != 0.0f) sincos_red(phi, &sp, &cp);  // Gabor along its modulation plane
-                            if (COUNT) ++wk.erfr;
-                        } else {
-                            const float zr = u * kRsqrt2, zi = -Om * kRsqrt2;
-                            F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
-                            sincos_red(phi, &sp, &cp);
-                            if (COUNT) ++wk.erfc;
-                        }
-                        if (rne == 1) {
-                            atomicAdd(&bins[rka], 2.0f * amp * cp * F.x);
-                        } else {
-                            const float v = amp * fmaf(cp, F.x, -sp * F.y);
-                            if (je >= 1) atomicAdd(&bins[rka + je - 1], v);
-                            if (je <= rne - 2) atomicAdd(&bins[rka + je], -v);
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            const double tstar = R.cum[p + R.n_paths];
-            int32_t bin = -2;
-            double cum = 0.0, cum_before = 0.0, bin_tau = 0.0;
-            uint32_t nact = 0;
-            for (int k = 0; k < kBins; ++k) {
-                const double c2 = cum + (double)bins[k];
-                if (c2 >= tstar) { bin = k; cum_before = cum; bin_tau = bins[k]; nact = cnts[k]; break; }
-                cum = c2;
-            }
-            if (bin == -2) {
-                R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
-            } else {
-                R.bin[p] = bin | (int32_t)(min(nact, 32767u) << 16);
-                R.cum[p] = cum_before;
-                R.cum[p + 2 * R.n_paths] = bin_tau;
-                R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
-            }
-        }
-        __syncwarp();
-    }
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFAI, wk);
-}
 
 // ---------------------------------------------------------------- ffB: root in the bracketing bin
 // Active primitives of the bracket, split into Gaussians (Omega == 0: real erf, 8 floats) and
@@ -673,48 +440,8 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
                     ++nb;
                 }
             };
-            const bool recpath = R.nrg[p] != 0xFFFFFFFFu;
-            const uint32_t nh = recpath ? 0xFFFFFFFFu : R.nhit[p];
-            if (recpath) {  // the path's hit records from k_ffA_T: clip to the bracket, no primitive reload
-                const float ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
-                const uint32_t cap = (uint32_t)R.rec_cap;
-                const uint32_t nside[2] = {R.nrg[p], R.nrb[p]};
-                for (int side = 0; side < 2; ++side) {
-                    for (uint32_t i = 0; i < nside[side]; ++i) {
-                        const size_t slot = (size_t)p * cap + (side == 0 ? i : cap - 1 - i);
-                        const float4 a = R.rec[2 * slot], b = R.rec[2 * slot + 1];
-                        int ka, kb;
-                        rec_span(a, b, tlo, ibw, ka, kb);
-                        if (COUNT) ++wk.tests;
-                        if (ka > bin || kb < bin) continue;
-                        const float ua = fmaxf(a.x, fmaf(b.y, ta - b.z, b.w));
-                        const float ub = fminf(a.y, fmaf(b.y, tb - b.z, b.w));
-                        if (!(ub > ua)) continue;
-                        if (COUNT) ++wk.hits;
-                        const float kap0 = b.x * b.y * 0.79788456080286536f * __expf(0.5f * a.z * a.z);
-                        if (a.z == 0.0f && a.w == 0.0f) {
-                            if (ng < kCapG) {
-                                ActG& g = ag[ng];
-                                g.amp = b.x; g.kap0 = kap0; g.j = b.y; g.tc = b.z; g.bp = b.w; g.u0 = ua; g.u1 = ub;
-                                g.F0 = erff(ua * kRsqrt2);
-                                if (COUNT) ++wk.erfr;
-                            }
-                            ++ng;
-                        } else {
-                            if (nb < kCapB) {
-                                ActB& q = ab[nb];
-                                q.amp = b.x; q.kap0 = kap0; q.Om = a.z; q.phi0 = a.w; q.j = b.y; q.tc = b.z; q.bp = b.w;
-                                q.u0 = ua; q.u1 = ub;
-                                sincos_red(a.w, &q.sp, &q.cp);
-                                const float2 F0 = erf_shift(ua, a.z);
-                                if (COUNT) wk.erf(a.z, 1);
-                                q.F0r = F0.x; q.F0i = F0.y;
-                            }
-                            ++nb;
-                        }
-                    }
-                }
-            } else if (nh <= (uint32_t)R.hit_cap) {  // scan the path's hit list from single-pass ffA
+            const uint32_t nh = R.nhit[p];
+            if (nh <= (uint32_t)R.hit_cap) {  // scan the path's hit list from single-pass ffA
                 for (uint32_t k = 0; k < nh; ++k) {
                     const uint2 e = R.hits[(size_t)p * R.hit_cap + k];
                     if ((int)(e.y & 0xFFu) > bin || (int)(e.y >> 8) < bin) continue;
@@ -796,130 +523,6 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
 }
 
 
-// ---------------------------------------------------------------- ffB, one warp per path
-// The bracket's active primitives are the path's hit records overlapping bin k.  Lanes scan the
-// records in parallel (coalesced); every Newton evaluation is a warp reduction of
-//   f(t) = cum0 - tau* + sum_i amp_i [G_i(clamp(u_i(t))) - G_i(lower_i)],  G = Re(e^{i phi} F),
-//   kappa(t) = sum_i kap0_i e^{-u^2/2} cos(phi_i + Omega_i u)      (derivative of tau, analytic),
-// so all lanes take the same (safeguarded Newton / bisection) steps.  No per-lane lists.
-template <bool COUNT>
-__global__ void __launch_bounds__(128) k_ffB_W(RenderDev R) {
-    const int lane = threadIdx.x & 31;
-    const unsigned FULL = 0xFFFFFFFFu;
-    const uint32_t count = R.qcount[1], cap = (uint32_t)R.rec_cap;
-    Work wk;
-    while (true) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(R.qcount + kWorkBW, 1u);
-        idx = __shfl_sync(FULL, idx, 0);
-        if (idx >= count) break;
-        const uint32_t p = R.qB[idx];
-        const int32_t binw = R.bin[p];
-        const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
-        float tres = 0.0f;
-        if (binw >= 0) {
-            const int bin = binw & 0xFFFF;
-            const float tlo = R.tlo[p], bw = R.tbw[p], ibw = bw > 0.0f ? 1.0f / bw : 0.0f;
-            const float ta = tlo + bin * bw;
-            const float tb = tlo + (bin + 1) * bw;
-            const float tbc = (bin == kBins - 1) ? INFINITY : tb;  // clip window (records end at thi)
-            const double tstar = R.cum[p + R.n_paths], cum0 = R.cum[p], span = R.cum[p + 2 * R.n_paths];
-            const uint32_t nside[2] = {R.nrg[p], R.nrb[p]};
-            // one scan over the records: mode 0 -> S0 = sum amp G(lower); mode 1 -> sum amp G(clamp(u_t)), kappa
-            auto scan = [&](int mode, float t, double& kap_out) -> double {
-                float acc = 0.0f, kap = 0.0f;
-#pragma unroll 1
-                for (int side = 0; side < 2; ++side) {
-                    for (uint32_t i = lane; i < nside[side]; i += 32) {
-                        const size_t slot = (size_t)p * cap + (side == 0 ? i : cap - 1 - i);
-                        const float4 a = R.rec[2 * slot], b = R.rec[2 * slot + 1];
-                        int ka, kb;
-                        rec_span(a, b, tlo, ibw, ka, kb);
-                        if (ka > bin || kb < bin) continue;
-                        const float lower = fmaxf(a.x, fmaf(b.y, ta - b.z, b.w));
-                        const float upper = fminf(a.y, fmaf(b.y, tbc - b.z, b.w));
-                        if (!(upper > lower)) continue;
-                        if (COUNT && mode == 0) ++wk.hits;
-                        const float wmax = 0.5f * (fmaxf(lower * lower, upper * upper) + a.z * a.z);
-                        const bool special = upper - lower < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f);
-                        float u = lower;
-                        if (mode == 1) {
-                            const float ut = fmaf(b.y, t - b.z, b.w);
-                            if (ut > lower && ut < upper) {
-                                float sp, cp;
-                                sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
-                                kap += b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut)) * cp;
-                            }
-                            u = fminf(fmaxf(ut, lower), upper);
-                        }
-                        if (special) {  // rare: midpoint / Gauss-Legendre from lower (no S0 term)
-                            if (mode == 1 && u > lower) {
-                                Setup s;
-                                s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
-                                s.Om = a.z; s.phi0 = a.w;
-                                acc += 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, lower, u, wk);
-                            }
-                            continue;
-                        }
-                        float2 F;
-                        float sp = 0.0f, cp = 1.0f;
-                        if (side == 0) {
-                            F = make_float2(erff(u * kRsqrt2), 0.0f);
-                            if (a.w != 0.0f) sincos_red(a.w, &sp, &cp);
-                            if (COUNT) ++wk.erfr;
-                        } else {
-                            const float zr = u * kRsqrt2, zi = -a.z * kRsqrt2;
-                            F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
-                            sincos_red(a.w, &sp, &cp);
-                            if (COUNT) ++wk.erfc;
-                        }
-                        acc += b.x * fmaf(cp, F.x, -sp * F.y);
-                    }
-                }
-                double x = acc, k = kap;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    x += __shfl_xor_sync(FULL, x, off);
-                    k += __shfl_xor_sync(FULL, k, off);
-                }
-                kap_out = k;
-                return x;
-            };
-            double kap;
-            const double S0 = scan(0, 0.0f, kap);
-            auto eval = [&](float t, double& kp) -> double {
-                if (COUNT) ++wk.root;
-                return cum0 - tstar - S0 + scan(1, t, kp);
-            };
-            float lo = ta, hi = tb;
-            const double need = tstar - cum0;
-            float t = ta + 0.5f * (tb - ta);
-            if (span > 0.0 && need >= 0.0) t = ta + (float)(need / span) * (tb - ta);
-            t = fminf(fmaxf(t, lo), hi);
-            for (int it = 0; it < 48; ++it) {
-                const double f = eval(t, kap);
-                if (f >= 0.0) hi = t; else lo = t;
-                if (!(hi - lo > 1e-6f * bw)) break;
-                if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
-                float tn = (kap > 0.0) ? (float)((double)t - f / kap) : 0.5f * (lo + hi);
-                const bool newton = tn > lo && tn < hi;
-                if (!newton) tn = 0.5f * (lo + hi);
-                const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
-                t = tn;
-                if (small) break;
-            }
-            tres = t;
-        }
-        if (lane == 0) {  // collision point becomes the new origin
-            R.ox[p] = fmaf(tres, d.x, o.x);
-            R.oy[p] = fmaf(tres, d.y, o.y);
-            R.oz[p] = fmaf(tres, d.z, o.z);
-        }
-        __syncwarp();
-    }
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFB, wk);
-}
-
 // ---------------------------------------------------------------- NEE + phase sampling
 template <bool STOCH, bool COUNT>
 __global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t sample, int32_t depth) {
@@ -972,6 +575,274 @@ __global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t s
             began = false;
         });
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
+}
+
+// ---------------------------------------------------------------- free flight, one warp per path
+// k_ff fuses the whole free-flight step of a path (a8):
+//  1. warp_traverse over [t_lo, t_hi] (the root box span) emitting one 32-byte record per
+//     accepted primitive into the warp's own record buffer (coalesced, warp prefix offsets):
+//     a = (u0, u1, Omega, phi0), b = (amp = c/j w e^{-(r2+Omega^2)/2} / 2, j, t_c, b');
+//     Gaussians (Omega == 0) from the front, Gabors from the back, so erf work is type-uniform;
+//  2. per record its full-chord integral amp (G(u1) - G(u0)), G(u) = Re{e^{i phi0} F(u)}, and
+//     amp G(u0), amp cos phi0, -amp sin phi0 (aux); tau_total = sum -> escape test (Eq. 5);
+//  3. safeguarded Newton / bisection on tau(t) = tau* over the whole ray: each evaluation scans
+//     the records -- a chord wholly before t adds its full integral, one straddling t queues the
+//     endpoint u(t) (one erf, evaluated 32 at a time, type-uniform) and adds its kappa term --
+//     so no erf is spent on chords that t has passed or not reached.
+// The buffer (rec_cap records per warp) stays L2-resident between the three phases; a path with
+// more records than rec_cap goes to the single-pass fallback (k_ffA + k_ffB).
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t depth) {
+    __shared__ WarpTrav s_t[4];
+    __shared__ WarpEnd s_e[4];
+    __shared__ float s_h[4][64];  // coarse tau(t) histogram of the chord integrals -> Newton start
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t count = R.qcount[0], cap = (uint32_t)R.rec_cap;
+    float* hist = s_h[wid];
+    const size_t gw = (size_t)blockIdx.x * 4 + wid;
+    float4* __restrict__ rec = R.wrec + gw * cap * 2;
+    float4* __restrict__ aux = R.waux + gw * cap;
+    WarpEnd& q = s_e[wid];
+    Work wk;
+    uint32_t nray = 0;
+    while (true) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(R.qcount + kWorkAT, 1u);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= count) break;
+        const uint32_t p = R.qA[idx];
+        ++nray;
+        if (COUNT && lane == 0) ++wk.paths;
+        const uint32_t pix = R.pix[p];
+        const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+        float w[kMaxGroups];
+        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                 ST_EXT, 1, w)
+                                    : R.ext.static_mask;
+        const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
+        const double tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
+        if (tstar <= 0.0) {  // collision at the origin
+            if (lane == 0) R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
+            continue;
+        }
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        float tlo, thi;
+        if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
+            if (lane == 0) R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+            continue;
+        }
+        // 1. records
+        uint32_t ng = 0, nb = 0;
+        warp_traverse<COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, r, tlo, thi, mask, s_t[wid], wk,
+                             [&](bool valid, uint32_t ref) {
+            bool hit = false;
+            Setup s;
+            float cj = 0.0f;
+            if (valid) {
+                const GPrim* pp = R.prims + (ref & kRefIdx);
+                GPrim P;
+                P.a = __ldg(&pp->a);
+                if (COUNT) ++wk.tests;
+                if (sphere_pretest(P.a, r, tlo, thi)) {
+                    P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                    hit = prim_setup(P, r, tlo, thi, s);
+                    cj = P.d.w * s.ij;
+                    if (STOCH) cj *= w[ref >> 27];
+                }
+            }
+            const bool hg = hit && s.Om == 0.0f, hb = hit && s.Om != 0.0f;
+            const unsigned mg = __ballot_sync(FULL, hg), mb = __ballot_sync(FULL, hb);
+            if (hit) {
+                if (COUNT) ++wk.hits;
+                const uint32_t slot = hg ? ng + __popc(mg & lt) : cap - 1 - (nb + __popc(mb & lt));
+                if (ng + nb + __popc(mg) + __popc(mb) <= cap) {
+                    const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                    rec[2 * slot] = make_float4(s.u0, s.u1, s.Om, s.phi0);
+                    rec[2 * slot + 1] = make_float4(amp, s.j, s.tc, s.bp);
+                }
+            }
+            ng += __popc(mg);
+            nb += __popc(mb);
+        });
+        if (ng + nb > cap) {  // record overflow: single-pass fallback
+            if (lane == 0) R.qO[atomicAdd(R.qcount + kCntO, 1u)] = p;
+            continue;
+        }
+        __syncwarp();
+        // 2. per-record full integrals -> tau_total, histogram over 64 t-bins by chord centre
+        float tot = 0.0f;
+        const float hscale = 64.0f / fmaxf(thi - tlo, 1e-30f);
+        hist[lane] = 0.0f;
+        hist[lane + 32] = 0.0f;
+        __syncwarp();
+        const uint32_t nside[2] = {ng, nb};
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+            for (uint32_t i = lane; i < nside[side]; i += 32) {
+                const uint32_t slot = side == 0 ? i : cap - 1 - i;
+                const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
+                float full, g0 = 0.0f, ac = 0.0f, as = 0.0f;
+                const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
+                if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
+                    // rare: midpoint / Gauss-Legendre (seg_J with e^{-r2/2} and 1/2 e^{-Om^2/2} in amp)
+                    Setup s;
+                    s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                    s.Om = a.z; s.phi0 = a.w;
+                    full = 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, a.y, wk);
+                    g0 = __int_as_float(0x7fc00000);  // NaN marks a special record
+                } else {
+                    float sp = 0.0f, cp = 1.0f;
+                    if (side == 1 || a.w != 0.0f) sincos_red(a.w, &sp, &cp);
+                    ac = b.x * cp; as = -b.x * sp;
+                    float2 F1;
+                    if (side == 0) { F1 = make_float2(erff(a.y * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
+                    else { F1 = erf_shift(a.y, a.z); if (COUNT) ++wk.erfc; }
+                    const float G1 = fmaf(ac, F1.x, as * F1.y);
+                    if (a.x == -a.y) {
+                        g0 = -fmaf(ac, F1.x, -as * F1.y);  // F(-h) = -conj F(h)
+                    } else {
+                        float2 F0;
+                        if (side == 0) { F0 = make_float2(erff(a.x * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
+                        else { F0 = erf_shift(a.x, a.z); if (COUNT) ++wk.erfc; }
+                        g0 = fmaf(ac, F0.x, as * F0.y);
+                    }
+                    full = G1 - g0;
+                }
+                aux[slot] = make_float4(full, g0, ac, as);
+                tot += full;
+                const float tm = b.z + (0.5f * (a.x + a.y) - b.w) / b.y;
+                atomicAdd(&hist[min(63, max(0, (int)((tm - tlo) * hscale)))], full);
+            }
+        }
+        double tau_tot = tot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tau_tot += __shfl_xor_sync(FULL, tau_tot, o);
+        if (tau_tot < tstar) {  // escape -> environment
+            if (lane == 0) R.L[p] += R.beta[p] * R.env_L;
+            continue;
+        }
+        __syncwarp();
+        // 3. Newton / bisection on f(t) = tau(t) - tau*
+        int nq0 = 0, nq1 = 0;
+        double acc = 0.0;
+        auto run = [&](int t, int take) {
+            int& nq = t == 0 ? nq0 : nq1;
+            const bool v = lane < take;
+            const float4 e = v ? q.e[t][nq - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            nq -= take;
+            __syncwarp();
+            if (v) {
+                const float zr = e.x * kRsqrt2;
+                if (t == 0) {
+                    if (COUNT) ++wk.erfr;
+                    acc += (double)(e.z * erff(zr));
+                } else {
+                    if (COUNT) ++wk.erfc;
+                    const float zi = -e.y * kRsqrt2;
+                    const float2 F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
+                    acc += (double)fmaf(e.z, F.x, e.w * F.y);
+                }
+            }
+        };
+        auto eval = [&](float t, double& kap_out) -> double {
+            if (COUNT && lane == 0) ++wk.root;
+            acc = 0.0;
+            float part = 0.0f, kap = 0.0f;
+#pragma unroll 1
+            for (int side = 0; side < 2; ++side) {
+                const uint32_t n = nside[side];
+                for (uint32_t base = 0; base < n; base += 32) {
+                    const uint32_t i = base + lane;
+                    bool push = false;
+                    float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    if (i < n) {
+                        const uint32_t slot = side == 0 ? i : cap - 1 - i;
+                        const float4 a = rec[2 * slot], b = rec[2 * slot + 1], x = aux[slot];
+                        const float ut = fmaf(b.y, t - b.z, b.w);
+                        if (ut >= a.y) {
+                            part += x.x;
+                        } else if (ut > a.x) {
+                            float sp, cp;
+                            sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
+                            kap += b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut)) * cp;
+                            if (x.y != x.y) {  // special record: lane-local partial integral
+                                Setup s;
+                                s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                                s.Om = a.z; s.phi0 = a.w;
+                                part += 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, ut, wk);
+                            } else {
+                                part -= x.y;
+                                push = true;
+                                e = make_float4(ut, a.z, x.z, x.w);
+                            }
+                        }
+                    }
+                    const unsigned m = __ballot_sync(FULL, push);
+                    if (m) {
+                        int& nq = side == 0 ? nq0 : nq1;
+                        if (push) q.e[side][nq + __popc(m & lt)] = e;
+                        nq += __popc(m);
+                        __syncwarp();
+                        if (nq >= 32) run(side, 32);
+                    }
+                }
+            }
+            while (nq0 > 0) run(0, min(nq0, 32));
+            while (nq1 > 0) run(1, min(nq1, 32));
+            double x = acc + (double)part, k = kap;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                x += __shfl_xor_sync(FULL, x, o);
+                k += __shfl_xor_sync(FULL, k, o);
+            }
+            kap_out = k;
+            return x - tstar;
+        };
+        const float bw = thi - tlo;
+        float lo = tlo, hi = thi;
+        float t;
+        {  // start: first crossing of tau* in the histogram's running sum (linear inside the bin)
+            const float h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+            float incl = h0 + h1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned m = __ballot_sync(FULL, (double)incl >= tstar);
+            const int L = m ? __ffs(m) - 1 : 31;
+            const float ts = (float)tstar, prev = incl - (h0 + h1);
+            float pos;
+            if (prev + h0 >= ts) pos = 2 * lane + fminf(fmaxf((ts - prev) / fmaxf(h0, 1e-30f), 0.0f), 1.0f);
+            else pos = 2 * lane + 1 + fminf(fmaxf((ts - prev - h0) / fmaxf(h1, 1e-30f), 0.0f), 1.0f);
+            pos = __shfl_sync(FULL, pos, L);
+            t = fminf(fmaxf(tlo + pos * (bw * (1.0f / 64.0f)), lo), hi);
+        }
+        double kap = 0.0;
+        for (int it = 0; it < 48; ++it) {
+            const double f = eval(t, kap);
+            if (f >= 0.0) hi = t; else lo = t;
+            if (!(hi - lo > 1e-6f * bw)) break;
+            if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
+            float tn = (kap > 0.0) ? (float)((double)t - f / kap) : 0.5f * (lo + hi);
+            const bool newton = tn > lo && tn < hi;
+            if (!newton) tn = 0.5f * (lo + hi);
+            const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
+            t = tn;
+            if (small) break;
+        }
+        if (lane == 0) {  // collision point becomes the new origin
+            R.ox[p] = fmaf(t, d.x, o.x);
+            R.oy[p] = fmaf(t, d.y, o.y);
+            R.oz[p] = fmaf(t, d.z, o.z);
+            R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
 }
 
 // NEE, one warp per path (warp_tau): shadow-ray transmittance, HG phase sampling of the next
@@ -1077,6 +948,18 @@ __global__ void __launch_bounds__(256) k_finish(RenderDev R, int32_t slot) {
 
 using namespace gfk;
 
+// persistent grid: 16 blocks of 128 threads per SM (the kernels' occupancy is <= 8 resident)
+static int persist_blocks() {
+    static int b = 0;
+    if (!b) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        b = (sms > 0 ? sms : 148) * 16;
+    }
+    return b;
+}
+
 size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     size_t off = 0;
     auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += (bytes + 255) & ~(size_t)255; return p; };
@@ -1087,22 +970,21 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     double* cum = (double*)take(sizeof(double) * 3 * (size_t)n);
     int32_t* bin = (int32_t*)take(nu); uint32_t* pix = (uint32_t*)take(nu); uint32_t* nhit = (uint32_t*)take(nu);
     uint2* hits = (uint2*)take(sizeof(uint2) * (size_t)kHitCap * (size_t)n);
-    float4* rec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * (size_t)n);
-    uint32_t* nrg = (uint32_t*)take(nu); uint32_t* nrb = (uint32_t*)take(nu);
-    float* tlo = (float*)take(nf); float* tbw = (float*)take(nf);
+    const size_t nw = (size_t)4 * (size_t)std::min<int64_t>((int64_t)persist_blocks(), (n + 3) / 4);  // k_ff warps
+    float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
+    float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
-    uint32_t* qT = (uint32_t*)take(nu); uint32_t* qO = (uint32_t*)take(nu); uint32_t* qB2 = (uint32_t*)take(nu);
+    uint32_t* qO = (uint32_t*)take(nu); uint32_t* qB2 = (uint32_t*)take(nu);
     uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
         R->cum = cum; R->bin = bin; R->pix = pix; R->nhit = nhit; R->hits = hits; R->hit_cap = kHitCap;
-        R->rec = rec; R->rec_cap = kRecCap; R->nrg = nrg; R->nrb = nrb; R->tlo = tlo; R->tbw = tbw;
-        R->qA = qA; R->qB = qB; R->qNext = qN; R->qT = qT; R->qO = qO; R->qB2 = qB2; R->qcount = qc;
+        R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap;
+        R->qA = qA; R->qB = qB; R->qNext = qN; R->qO = qO; R->qB2 = qB2; R->qcount = qc;
     }
     return off;
 }
 
-static int g_persist_blocks = 0;
 
 template <bool S, bool C>
 static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, unsigned wgrid, cudaStream_t st,
@@ -1110,17 +992,11 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
                          bool stoch_nee) {
     cudaEvent_t e;
     T.pre(STAGE_FFA, st, e);
-    k_ffA_T<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
+    k_ff<S, C><<<wgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFA, st, e);
-    T.pre(STAGE_FFAI, st, e);
-    k_ffA_I<C><<<pgrid, 128, 0, st>>>(R);
-    T.post(STAGE_FFAI, st, e);
     T.pre(STAGE_FFA, st, e);  // record-overflow paths: single-pass kernel
     k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
     T.post(STAGE_FFA, st, e);
-    T.pre(STAGE_FFB, st, e);
-    k_ffB_W<C><<<pgrid, 128, 0, st>>>(R);
-    T.post(STAGE_FFB, st, e);
     T.pre(STAGE_FFB, st, e);  // record-overflow paths (appended to qB for NEE)
     k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFB, st, e);
@@ -1133,18 +1009,12 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
 cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cudaStream_t st, StageTimer& T) {
     cudaError_t e;
     if (R.n_paths == 0) return cudaSuccess;
-    if (!g_persist_blocks) {
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        g_persist_blocks = sms * 16;
-    }
     const bool cnt = R.work != nullptr;
     const bool stoch_ext = !(R.ext.ls == 0 && R.ext.os == 0);
     const bool stoch_nee = !(R.nee.ls == 0 && R.nee.os == 0);
     const unsigned grid = (unsigned)((R.n_paths + 127) / 128);
-    const unsigned pgrid = (unsigned)std::min<int64_t>((int64_t)g_persist_blocks, (R.n_paths + 127) / 128);
-    const unsigned wgrid = (unsigned)std::min<int64_t>((int64_t)g_persist_blocks, (R.n_paths + 3) / 4);  // warp/path
+    const unsigned pgrid = (unsigned)std::min<int64_t>((int64_t)persist_blocks(), (R.n_paths + 127) / 128);
+    const unsigned wgrid = (unsigned)std::min<int64_t>((int64_t)persist_blocks(), (R.n_paths + 3) / 4);  // warp/path
     if ((e = cudaMemsetAsync(R.qcount, 0, sizeof(uint32_t) * 16, st))) return e;
     cudaEvent_t ev;
     if (R.mode == 0) {
