@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -90,6 +91,17 @@ static gf_status cuda_fail(gf_ctx* c, cudaError_t e, const char* where) {
     } while (0)
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Test-only overrides (environment, read per call): GF_DEBUG_REC_CAP=n lowers k_ff's record
+// capacity so paths take the single-pass fallback; GF_DEBUG_STK_LIMIT=n lowers the warp
+// traversal's stack threshold so it runs its depth-first (one node per step) mode.
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+static int32_t stk_limit_of(const gf_ctx* c) {
+    return std::max(1, std::min<int32_t>(c->stk_limit, env_int("GF_DEBUG_STK_LIMIT", c->stk_limit)));
+}
 
 static PolicyDev make_policy_dev(const gf_lod_policy& p, int P) {
     PolicyDev d{};
@@ -308,7 +320,7 @@ static gf_status trace_common(gf_ctx* c, const float* rays, int64_t n, TraceArgs
     const bool brute = flags & GF_TRACE_BRUTE_FORCE;
     A.nodes = c->nodes;
     A.nodes2 = c->nodes2;
-    A.stk_limit = c->stk_limit;
+    A.stk_limit = stk_limit_of(c);
     A.n_nodes = c->built ? c->n_nodes : 0;
     A.prims = brute ? c->prims : c->sorted;
     A.group = c->group;
@@ -411,9 +423,10 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     if (gf_status s = check_sticky(c)) return s;
     RenderDev R{};
     gf_render_state_bytes(chunk, (char*)scratch, &R);
+    R.rec_cap = std::max(0, std::min(R.rec_cap, env_int("GF_DEBUG_REC_CAP", R.rec_cap)));
     R.nodes = c->nodes;
     R.nodes2 = c->nodes2;
-    R.stk_limit = c->stk_limit;
+    R.stk_limit = stk_limit_of(c);
     R.n_nodes = c->n_nodes;
     R.prims = c->sorted;
     R.ext = c->dext;

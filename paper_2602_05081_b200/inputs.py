@@ -278,6 +278,19 @@ def empty_scene(P=P_DEFAULT, K=K_DEFAULT):
                    name="empty")
 
 
+def scene_column(seed=SCENE_SEED + 9, n=1500, density=0.02):
+    """Stress case (not a paper workload): n small primitives strung along the x axis in [-1, 1]
+    (80% Gaussians, 20% Gabors), so a ray along the axis overlaps all of them -- more hit records
+    than the free-flight record buffer holds (1024), exercising the single-pass fallback."""
+    rng = np.random.default_rng(seed)
+    mu = np.stack([np.linspace(-1, 1, n), rng.normal(0, 0.002, n), rng.normal(0, 0.002, n)], 1)
+    scale = 0.02 * np.exp(rng.normal(0, 0.2, (n, 3)))
+    level = np.where(rng.random(n) < 0.8, 0, rng.integers(1, 4, n)).astype(np.uint8)
+    omega = np.where(level == 0, 0.0, rng.uniform(0.7, 1.5, n))
+    peak = density * rng.uniform(0.5, 1.0, n)
+    return _finish(mu, random_quats(rng, n), scale, peak, omega, level, name="column")
+
+
 def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
     """32-bit group mask selecting whole pyramid levels: level 0 -> bit 0, Gabor level l ->
     bits 1+(l-1)K .. (l)K (the group numbering g(l,b) of DESIGN.md §5; paper V_l = 2^l)."""

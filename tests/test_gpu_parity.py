@@ -291,6 +291,53 @@ def test_render_tomography_stochastic_probes(gfm, orc):
     vg, vo, _ = _probe_compare(gfm, orc, sc, desc, probes, 32, "stochastic tomography", frac_tol=0.0)
 
 
+def test_render_record_fallback_paths(gfm, orc, monkeypatch):
+    """Free-flight paths whose hit records exceed k_ff's buffer take the single-pass kernels
+    (k_ffA + k_ffB): forcing a 4-record buffer routes nearly every path there, same estimates."""
+    monkeypatch.setenv("GF_DEBUG_REC_CAP", "4")
+    sc = I.scene_cfg1p()
+    desc = I.render_desc_cfg2(3, 32, 32)
+    desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 32, 32))
+    desc.update(max_depth=3, albedo=0.9, ext=I.policy(), nee=I.policy())
+    probes = np.random.default_rng(6).integers(0, 32 * 32, 24)
+    _probe_compare(gfm, orc, sc, desc, probes, 16, "record fallback", frac_tol=0.05)
+
+
+def test_column_more_hits_than_record_buffer(gfm, orc):
+    """1500 primitives along one axis: rays along it exceed the 1024-record buffer (real overflow);
+    transmittance parity, then free flight through the column vs the oracle."""
+    sc = I.scene_column()
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    o = np.array([[-1.5, 0.0005 * k, -0.0003 * k] for k in range(8)])
+    d = np.tile([[1.0, 0.0, 0.0]], (8, 1))
+    rays = I.pack_rays(o, d)
+    tau, T, cnt = f.trace_transmittance(rays, counters=True)
+    r = S.trace(rays)
+    assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), "column")
+    assert cnt.cpu().numpy()[:, 2].min() > 1024
+    desc = I.render_desc_cfg2(3, 16, 16)
+    desc.update(**I.camera((-1.5, 0, 0), (0, 0, 0), (0, 1, 0), 1.0, 16, 16))
+    desc.update(max_depth=2, albedo=0.9, ext=I.policy(), nee=I.policy())
+    probes = np.arange(16 * 16)[::8]
+    _probe_compare(gfm, orc, sc, desc, probes, 8, "column free flight", frac_tol=0.05)
+
+
+def test_warp_traversal_depth_first_mode(gfm, orc, monkeypatch):
+    """The warp traversal pops one node per step above its stack threshold (bounded stack);
+    forcing that mode everywhere gives the same hits and transmittance."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    rays = camera_rays(I.render_desc_cfg2(3), 300, seed=23)
+    tau0, _, c0 = f.trace_transmittance(rays, counters=True)
+    monkeypatch.setenv("GF_DEBUG_STK_LIMIT", "1")
+    tau1, _, c1 = f.trace_transmittance(rays, counters=True)
+    assert torch.equal(c0[:, 1:], c1[:, 1:])
+    r = orc.Scene(sc).trace(rays)
+    assert_tau_parity(tau1.cpu().numpy(), r["tau"], r["A"], None, "depth-first mode")
+    assert np.array_equal(c1.cpu().numpy()[:, 2], r["nhits"])
+
+
 def test_cfg2_bench_configuration_sampled(gfm, orc):
     """Config 2 at full size in the launch configuration bench.py times (1024^2, 1 spp per LOD
     mask, single scattering): sampled pixels of the full-image render vs the oracle's paths."""
