@@ -82,6 +82,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def load_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+    try:
+        t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")))
+        return t[f"cfg{config}"][kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_peaks():
     try:
         return json.load(open(PEAKS_FILE))
@@ -262,8 +271,11 @@ def main():
     props = torch.cuda.get_device_properties(local)
     peak = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
     clocks = clk.summary()
-    roofline = {"bound": "alu", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+    kernel = {"ff": "k_ff", "nee": "k_nee_w", "tomo": "k_tomo_w", "ff_fallback": "k_ffA+k_ffB"}.get(dom, dom)
+    roofline = {"bound": "alu", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": load_traffic(args.config, kernel),
+                "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                "profiles/r01_traffic.json)",
                 "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz "
                                "(sm_max_mhz of MEASURED_PEAKS.json)",
                 "stage_share": {k: v / sum(stage_ms.values()) for k, v in stage_ms.items()},

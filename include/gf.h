@@ -214,9 +214,11 @@ gf_status gf_render(gf_ctx *ctx, const gf_render_desc *desc, float *accum, void 
 /* ---- measurement (bench.py roofline / launch counts) ---------------------- */
 #define GF_PROFILE_TIMING 1u  /* record CUDA events around every kernel launch (on its stream)   */
 #define GF_PROFILE_WORK 2u    /* use the counting kernel variants (work[] below; slower)          */
-/* Stages: 0 gen (camera rays), 1 ffA (free flight, binned tau), 2 ffB (root find), 3 nee (shadow
- * rays + phase sampling), 4 finish (queue rotation + accumulation), 5 tomo, 6 trace
- * (gf_trace_transmittance), 7 integrate (warp-per-path integration of hit records). */
+/* Stages: 0 gen (camera rays), 1 ff (free flight, k_ff: traversal -> hit records -> tau_total ->
+ * root of tau(t) = tau*), 2 ff_fallback (single-pass free flight for paths with more hit records
+ * than the record buffer), 3 nee (shadow rays + phase sampling), 4 finish (queue rotation +
+ * accumulation), 5 tomo, 6 trace (gf_trace_transmittance), 7 unused.  work[s][0] counts node box
+ * tests (the warp traversal tests both children of a popped node). */
 typedef struct {
     uint64_t launches;           /* kernels launched by the library since the last reset        */
     uint64_t stage_launches[8];

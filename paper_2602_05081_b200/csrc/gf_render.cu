@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
             fin = false;
             began = false;
         });
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFB, wk);
 }
 
 
@@ -994,9 +994,9 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
     T.pre(STAGE_FFA, st, e);
     k_ff<S, C><<<wgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFA, st, e);
-    T.pre(STAGE_FFA, st, e);  // record-overflow paths: single-pass kernel
+    T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")
     k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
-    T.post(STAGE_FFA, st, e);
+    T.post(STAGE_FFB, st, e);
     T.pre(STAGE_FFB, st, e);  // record-overflow paths (appended to qB for NEE)
     k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFB, st, e);

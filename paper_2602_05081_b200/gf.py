@@ -47,7 +47,7 @@ class Stats(ctypes.Structure):
                 ("stage_ms", ctypes.c_double * 8), ("work", (ctypes.c_uint64 * 12) * 8)]
 
 
-STAGES = ("gen", "ffA", "ffB", "nee", "finish", "tomo", "trace", "integrate")
+STAGES = ("gen", "ff", "ff_fallback", "nee", "finish", "tomo", "trace", "unused")
 WORK = ("nodes", "tests", "hits", "erf_complex", "erf_real", "gl_fallbacks", "ffb_overflow", "root_evals", "paths")
 PROFILE_TIMING, PROFILE_WORK = 1, 2
 

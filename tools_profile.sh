@@ -1,5 +1,6 @@
 #!/bin/bash
 # round-end style measurement: gpu tests, full bench, launch list, full captures of the top kernels
+# (the 4 launches of the second step = the 4 LOD masks of config 2)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
 timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
@@ -7,8 +8,8 @@ timeout 300 python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/pla
 if [ $rc = 0 ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu1.log 2>&1; echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_nee -s 4 -c 1 -f -o gpurun_out/prof_nee \
-    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu2.log 2>&1; echo "ncu nee rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ffA_T -s 4 -c 1 -f -o gpurun_out/prof_ffAT \
-    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu3.log 2>&1; echo "ncu ffAT rc=$?"
+  timeout 1200 ncu --set full --clock-control none --import-source on -k k_ff -s 4 -c 4 -f -o gpurun_out/prof_ff \
+    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu2.log 2>&1; echo "ncu ff rc=$?"
+  timeout 1200 ncu --set full --clock-control none --import-source on -k k_nee_w -s 4 -c 4 -f -o gpurun_out/prof_nee \
+    python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu3.log 2>&1; echo "ncu nee rc=$?"
 fi
