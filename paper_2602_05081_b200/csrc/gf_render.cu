@@ -1,13 +1,13 @@
 // gf_render.cu -- a8 free-flight distance sampling, a9 scatter loop, a10 accumulation
 // (Eq. 4-5, bisection/root finding P:L254, pipeline P:L352-L365).
 //
-// Wavefront over the paths of one sample pass: gen -> [ffA -> ffB -> nee] x max_depth -> finish.
-//  ffA: one traversal of the ray's scene interval accumulating tau into kBins t-bins
-//       (tau_total gives the escape test, the bins bracket the root);
-//  ffB: one traversal restricted to the bracketing bin gathers its active primitives, then a
-//       safeguarded Newton/bisection on tau(t) = tau* (derivative = kappa(t), analytic);
-//  nee: shadow ray towards the directional light (analytic T), HG phase, next direction.
-// Queues are warp-aggregated; work is fetched dynamically 32 paths at a time.
+// Wavefront over the paths of one sample pass: gen -> [ff -> (fallback) -> nee] x max_depth -> finish.
+//  k_ff   (one warp per path): warp traversal emitting hit records, exact tau_total (escape test),
+//         safeguarded Newton on tau(t) = tau* (derivative = kappa(t), analytic);
+//  k_ffA + k_ffB (per thread): single-pass fallback for paths with more records than the buffer;
+//  k_nee_w (one warp per path): shadow ray towards the directional light (T = e^-tau), HG phase,
+//         next direction.
+// Queues are warp-aggregated; warps fetch paths dynamically from the queues.
 #include <algorithm>
 
 #include "gf_device.cuh"
@@ -20,9 +20,10 @@ namespace gfk {
 #endif
 constexpr int kBins = GF_BINS;
 constexpr int kHitCap = 1024;  // hits recorded per path by ffA for ffB (overflow -> traversal gather)
-constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6, kWorkT = 7;  // qcount slots: work cursors
-constexpr int kCntT = 8, kCntO = 9, kWorkAT = 10, kWorkAI = 11, kWorkAO = 12;  // record pass A queues
-constexpr int kCntB2 = 13, kWorkBW = 14;  // single-pass (record overflow) paths for ffB; warp ffB cursor
+// qcount slots: 0 qA count, 1 qB count, 2 qNext count, then work cursors and fallback queues
+constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6;  // cursors: (unused), k_ffB, k_nee_w
+constexpr int kCntO = 9, kWorkAT = 10, kWorkAO = 12;  // record-overflow queue count; k_ff / k_ffA cursors
+constexpr int kCntB2 = 13;  // single-pass ffA -> per-thread ffB queue
 #ifndef GF_REC_CAP
 #define GF_REC_CAP 1024
 #endif
@@ -185,63 +186,10 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #ifndef GF_MINB_FFA
 #define GF_MINB_FFA 6
 #endif
-#ifndef GF_MINB_NEE
-#define GF_MINB_NEE 6
-#endif
 #ifndef GF_SPLIT_FFA
 #define GF_SPLIT_FFA 0
 #endif
-#ifndef GF_SPLIT_NEE
-#define GF_SPLIT_NEE 0
-#endif
-#ifndef GF_BATCH_T
-#define GF_BATCH_T 0  // record-emitting traversal: the hit callback (one 32-byte store) runs inline
-#endif
-#ifndef GF_MINB_T
-#define GF_MINB_T 8
-#endif
 constexpr int kBatch = GF_BATCH;  // integrate pending hits once this many lanes (or most blocked lanes) have one
-
-template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128) k_tomo(RenderDev R, int32_t sample) {
-    Work wk;
-    Trav T;
-    uint32_t p = 0;
-    double tau = 0.0;
-    float w[kMaxGroups];
-    bool began = false;
-    flat_loop<COUNT, kBatch, GF_SPLIT_NEE>(
-        R.qcount + kWorkT, (uint32_t)R.n_paths, R.nodes, R.n_nodes, R.prims, T, wk,
-        [&](uint32_t idx) -> bool {
-            p = idx;
-            const int32_t pix = path_pixel(R, p);
-            if (pix < 0) return false;
-            float jx = 0.5f, jy = 0.5f;
-            if (R.jitter) {
-                uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
-                jx = u01(b.x); jy = u01(b.y);
-            }
-            float3 o, d;
-            camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
-            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0,
-                                                     ST_EXT, 1, w)
-                                        : R.ext.static_mask;
-            trav_begin(T, make_ray(o, d, 0.0f, INFINITY), 0.0f, INFINITY, mask);
-            tau = 0.0;
-            began = true;
-            if (COUNT) ++wk.paths;
-            return true;
-        },
-        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
-            float c = coef * s.ij * seg_J(s, s.u0, s.u1, wk);
-            if (STOCH) c *= w[g];
-            tau += (double)c;
-            return true;
-        },
-        [&]() { R.L[p] = (float)tau; },
-        [&]() { count_rays(R.rays + 0, began); began = false; });
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
-}
 
 // ---------------------------------------------------------------- ffA: binned tau over the ray
 // Single-pass version (traversal with the bin integrals inline).  Used for the paths whose hit
@@ -522,60 +470,6 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFB, wk);
 }
 
-
-// ---------------------------------------------------------------- NEE + phase sampling
-template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128, GF_MINB_NEE) k_nee(RenderDev R, int32_t sample, int32_t depth) {
-    Work wk;
-    Trav T;
-    uint32_t p = 0, pix = 0;
-    double tau = 0.0;
-    float w[kMaxGroups];
-    bool began = false, cont = false;
-    uint32_t fin_p = 0;
-    flat_loop<COUNT, kBatch, GF_SPLIT_NEE>(
-        R.qcount + kWorkN, R.qcount[1], R.nodes, R.n_nodes, R.prims, T, wk,
-        [&](uint32_t idx) -> bool {
-            p = R.qB[idx];
-            pix = R.pix[p];
-            began = true;
-            if (COUNT) ++wk.paths;
-            const float3 x = ld3(R.ox, R.oy, R.oz, p);
-            const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample,
-                                                     (uint32_t)depth, ST_NEE, 0, w)
-                                        : R.nee.static_mask;
-            trav_begin(T, make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask);
-            tau = 0.0;
-            return true;
-        },
-        [&](const Setup& s, float coef, uint32_t g, uint32_t k) -> bool {
-            float c = coef * s.ij * seg_J(s, s.u0, s.u1, wk);
-            if (STOCH) c *= w[g];
-            tau += (double)c;
-            return true;
-        },
-        [&]() {
-            const float3 d = ld3(R.dx, R.dy, R.dz, p);
-            const float beta = R.beta[p];
-            const float cost = d.x * R.sun.x + d.y * R.sun.y + d.z * R.sun.z;
-            R.L[p] += beta * R.albedo * hg_eval(R.hg_g, cost) * (float)exp(-tau) * R.sun_E;
-            if (depth + 1 < R.max_depth) {
-                uint4 b = stream_block(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_SCAT, 0);
-                float3 nd = hg_sample(R.hg_g, d, u01(b.x), u01(b.y));
-                R.dx[p] = nd.x; R.dy[p] = nd.y; R.dz[p] = nd.z;
-                R.beta[p] = beta * R.albedo;
-                cont = true;
-                fin_p = p;
-            }
-        },
-        [&]() {
-            push(R.qNext, R.qcount + 2, cont, fin_p);
-            count_rays(R.rays + 1, began);
-            cont = false;
-            began = false;
-        });
-    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
-}
 
 // ---------------------------------------------------------------- free flight, one warp per path
 // k_ff fuses the whole free-flight step of a path (a8):
@@ -926,8 +820,7 @@ __global__ void k_rotate(uint32_t* qc) {
     qc[0] = qc[2];
     qc[1] = 0; qc[2] = 0;
     qc[kWorkA] = 0; qc[kWorkB] = 0; qc[kWorkN] = 0;
-    qc[kCntT] = 0; qc[kCntO] = 0; qc[kWorkAT] = 0; qc[kWorkAI] = 0; qc[kWorkAO] = 0;
-    qc[kCntB2] = 0; qc[kWorkBW] = 0;
+    qc[kCntO] = 0; qc[kWorkAT] = 0; qc[kWorkAO] = 0; qc[kCntB2] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_finish(RenderDev R, int32_t slot) {
