@@ -25,9 +25,9 @@ constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6;  // cursors: (unused), k_ffB, 
 constexpr int kCntO = 9, kWorkAT = 10, kWorkAO = 12;  // record-overflow queue count; k_ff / k_ffA cursors
 constexpr int kCntB2 = 13;  // single-pass ffA -> per-thread ffB queue
 #ifndef GF_REC_CAP
-#define GF_REC_CAP 1024
+#define GF_REC_CAP 16384
 #endif
-constexpr int kRecCap = GF_REC_CAP;  // 32-byte hit records per path (overflow -> single-pass ffA)
+constexpr int kRecCap = GF_REC_CAP;  // hit records per k_ff warp buffer (overflow -> single-pass ffA)
 
 template <bool COUNT, class F>
 __device__ __forceinline__ void traverse_r(const GNode* __restrict__ nodes, uint32_t n_nodes,
@@ -853,6 +853,20 @@ static int persist_blocks() {
     return b;
 }
 
+// k_ff runs one resident wave (its 26 KB of shared memory per block allow <= 8 blocks per SM), so
+// record buffers exist for sms x 8 blocks x 4 warps at most
+static int ff_max_blocks() { return persist_blocks() / 2; }
+template <bool S, bool C>
+static unsigned ff_grid(int64_t n_paths) {
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ff<S, C>, 128, 0);
+        occ = std::max(1, std::min(occ, 8));
+    }
+    const int64_t blocks = (int64_t)(persist_blocks() / 16) * occ;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (n_paths + 3) / 4));
+}
+
 size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     size_t off = 0;
     auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += (bytes + 255) & ~(size_t)255; return p; };
@@ -863,7 +877,7 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     double* cum = (double*)take(sizeof(double) * 3 * (size_t)n);
     int32_t* bin = (int32_t*)take(nu); uint32_t* pix = (uint32_t*)take(nu); uint32_t* nhit = (uint32_t*)take(nu);
     uint2* hits = (uint2*)take(sizeof(uint2) * (size_t)kHitCap * (size_t)n);
-    const size_t nw = (size_t)4 * (size_t)std::min<int64_t>((int64_t)persist_blocks(), (n + 3) / 4);  // k_ff warps
+    const size_t nw = (size_t)4 * (size_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)ff_max_blocks(), (n + 3) / 4));
     float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
     float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
@@ -885,7 +899,7 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
                          bool stoch_nee) {
     cudaEvent_t e;
     T.pre(STAGE_FFA, st, e);
-    k_ff<S, C><<<wgrid, 128, 0, st>>>(R, sample, d);
+    k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFA, st, e);
     T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")
     k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);

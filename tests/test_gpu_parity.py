@@ -303,9 +303,13 @@ def test_render_record_fallback_paths(gfm, orc, monkeypatch):
     _probe_compare(gfm, orc, sc, desc, probes, 16, "record fallback", frac_tol=0.05)
 
 
-def test_column_more_hits_than_record_buffer(gfm, orc):
-    """1500 primitives along one axis: rays along it exceed the 1024-record buffer (real overflow);
-    transmittance parity, then free flight through the column vs the oracle."""
+@pytest.mark.parametrize("rec_cap", [None, "1024"])
+def test_column_more_hits_than_record_buffer(gfm, orc, monkeypatch, rec_cap):
+    """1500 primitives along one axis: rays along it overlap all of them.  With a 1024-record buffer
+    the paths overflow mid-traversal (single-pass fallback); with the default buffer they fit.
+    Transmittance parity, then free flight through the column vs the oracle."""
+    if rec_cap:
+        monkeypatch.setenv("GF_DEBUG_REC_CAP", rec_cap)
     sc = I.scene_column()
     f = field(gfm, sc)
     S = orc.Scene(sc)
