@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--estimator", default="analytic", choices=["analytic", "tracking"],
+                    help="scatter estimator: closed-form tau + root (default) or delta/ratio tracking")
     ap.add_argument("--profile-pass", action="store_true", help="only run warmup+steps (for ncu launch lists)")
     args = ap.parse_args()
     rank, local, world = dist_env()
@@ -194,6 +196,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     sc, descs, name = workload(args.config)
+    if args.estimator == "tracking":
+        descs = [dict(d, estimator=1) for d in descs]
+        name += " [delta/ratio tracking estimator]"
     f = gf.GaborField(local)
     f.load_primitives(sc, group_f0=I.group_f0(sc))
     f.build_bvh()

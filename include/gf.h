@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 1
+#define GF_ABI_VERSION 2
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -182,7 +182,14 @@ typedef enum { GF_SHARD_NONE = 0, GF_SHARD_TILES = 1, GF_SHARD_SAMPLES = 2 } gf_
  *   directional light (sun_dir towards the light, irradiance sun_E) with the
  *   nee policy, Henyey-Greenstein phase (g), grey albedo, constant env_L on
  *   escape, max_depth vertices (1 = single scattering), no Russian roulette (C19).
- * RNG: Philox4x32-10, key = seed, counter = (pixel, sample, depth, stream<<16 | k>>2). */
+ * RNG: Philox4x32-10, key = seed, counter = (pixel, sample, depth, stream<<16 | k>>2).
+ * estimator (a9, SURVEY §8 a9 alternative): GF_EST_ANALYTIC = closed-form tau, free flight by the
+ *   root of tau(t) = tau*, NEE T = exp(-tau); GF_EST_TRACKING = null-collision delta tracking for
+ *   free flight and ratio tracking for NEE against a per-ray piecewise-constant majorant (64 bins
+ *   of the summed per-primitive density bounds); unbiased only where kappa >= 0 (C18); tracking
+ *   step j of a segment uses Philox block k = 4j of stream 4 (free flight: u0 distance, u1
+ *   acceptance) or stream 5 (NEE: u0 distance). */
+typedef enum { GF_EST_ANALYTIC = 0, GF_EST_TRACKING = 1 } gf_estimator;
 typedef struct {
     int32_t mode;               /* gf_render_mode */
     int32_t width, height;
@@ -196,6 +203,7 @@ typedef struct {
     float cam_pos[3], cam_fwd[3], cam_right[3], cam_up[3];
     float albedo, hg_g, sun_dir[3], sun_E, env_L;
     uint64_t seed;
+    int32_t estimator;          /* gf_estimator (SCATTER) */
 } gf_render_desc;
 
 /* Device scratch needed by gf_render for `desc`. */

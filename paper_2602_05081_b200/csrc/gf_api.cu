@@ -398,6 +398,8 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
     if (d->probe_pixels && (d->n_probe < 0 || d->shard_kind == GF_SHARD_TILES))
         return fail(c, GF_E_INVALID_ARGUMENT, "probe mode: n_probe >= 0 and no tile sharding");
     if (!(d->hg_g > -1.0f && d->hg_g < 1.0f)) return fail(c, GF_E_INVALID_ARGUMENT, "hg_g must be in (-1,1)");
+    if (d->estimator != GF_EST_ANALYTIC && d->estimator != GF_EST_TRACKING)
+        return fail(c, GF_E_INVALID_ARGUMENT, "bad estimator");
     return GF_OK;
 }
 
@@ -443,6 +445,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.mode = d->mode;
     R.max_depth = d->mode == GF_MODE_SCATTER ? d->max_depth : 1;
     R.jitter = d->jitter;
+    R.estimator = d->estimator;
     R.albedo = d->albedo; R.hg_g = d->hg_g; R.sun_E = d->sun_E; R.env_L = d->env_L;
     R.sun = make_float3(d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]);
     R.seed = d->seed;

@@ -79,7 +79,7 @@ struct RenderDev {
     gfk::SceneDev sc;
     gfk::CamDev cam;
     float4 root_lo, root_hi;
-    int32_t mode, max_depth, jitter;
+    int32_t mode, max_depth, jitter, estimator;
     float albedo, hg_g, sun_E, env_L;
     float3 sun;
     uint64_t seed;

@@ -739,6 +739,255 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
 }
 
+// ---------------------------------------------------------------- tracking estimators (a9 alternative)
+// Null-collision delta tracking (free flight) and ratio tracking (NEE transmittance) against a
+// per-ray piecewise-constant majorant, selected by gf_render_desc.estimator = GF_EST_TRACKING.
+// The ray's hit records (the same 32-byte records k_ff writes) give both the majorant -- 64 bins
+// over [t_lo, t_hi], bin k holding sum_i p_i over the chords overlapping it, p_i the bound of
+// |kappa_i| on its chord, amp j sqrt(2/pi) e^{(Omega^2 - u_min^2)/2} -- and kappa(t) at a tentative
+// point (one warp reduction over the records straddling t, no erf).  Unbiased where kappa >= 0.
+
+// hit records of one ray into rec (Gaussians from the front, Gabors from the back); false if the
+// ray has more than cap records
+template <bool STOCH, bool COUNT>
+__device__ __forceinline__ bool emit_records(const RenderDev& R, const RayDev& r, float t0, float t1, uint32_t mask,
+                                             const float* w, WarpTrav& sm, float4* __restrict__ rec, uint32_t cap,
+                                             uint32_t& ng, uint32_t& nb, Work& wk) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    ng = nb = 0;
+    warp_traverse<COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, r, t0, t1, mask, sm, wk,
+                         [&](bool valid, uint32_t ref) {
+        bool hit = false;
+        Setup s;
+        float cj = 0.0f;
+        if (valid) {
+            const GPrim* pp = R.prims + (ref & kRefIdx);
+            GPrim P;
+            P.a = __ldg(&pp->a);
+            if (COUNT) ++wk.tests;
+            if (sphere_pretest(P.a, r, t0, t1)) {
+                P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                hit = prim_setup(P, r, t0, t1, s);
+                cj = P.d.w * s.ij;
+                if (STOCH) cj *= w[ref >> 27];
+            }
+        }
+        const bool hg = hit && s.Om == 0.0f, hb = hit && s.Om != 0.0f;
+        const unsigned mg = __ballot_sync(FULL, hg), mb = __ballot_sync(FULL, hb);
+        if (hit) {
+            if (COUNT) ++wk.hits;
+            const uint32_t slot = hg ? ng + __popc(mg & lt) : cap - 1 - (nb + __popc(mb & lt));
+            if (ng + nb + __popc(mg) + __popc(mb) <= cap) {
+                const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                rec[2 * slot] = make_float4(s.u0, s.u1, s.Om, s.phi0);
+                rec[2 * slot + 1] = make_float4(amp, s.j, s.tc, s.bp);
+            }
+        }
+        ng += __popc(mg);
+        nb += __popc(mb);
+    });
+    __syncwarp();
+    return ng + nb <= cap;
+}
+
+// majorant bins M[0..63] over [wa, wb] (shared, per warp)
+__device__ __forceinline__ void majorant_bins(const float4* __restrict__ rec, uint32_t ng, uint32_t nb, uint32_t cap,
+                                              float wa, float wb, float* M) {
+    const int lane = threadIdx.x & 31;
+    M[lane] = 0.0f;
+    M[lane + 32] = 0.0f;
+    __syncwarp();
+    const float span = fmaxf(wb - wa, 1e-30f), sc = 64.0f / span, pad = 1e-5f * span;
+    const uint32_t nside[2] = {ng, nb};
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+        for (uint32_t i = lane; i < nside[side]; i += 32) {
+            const uint32_t slot = side == 0 ? i : cap - 1 - i;
+            const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
+            const float um = (a.x <= 0.0f && a.y >= 0.0f) ? 0.0f : fminf(fabsf(a.x), fabsf(a.y));
+            const float pk = 1.0001f * fabsf(b.x) * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - um * um));
+            const float ij = 1.0f / b.y;
+            const float ta = fmaf(a.x - b.w, ij, b.z) - pad, tb = fmaf(a.y - b.w, ij, b.z) + pad;
+            const int ka = min(63, max(0, (int)floorf((ta - wa) * sc))), kb = min(63, max(0, (int)floorf((tb - wa) * sc)));
+            for (int k = ka; k <= kb; ++k) atomicAdd(&M[k], pk);
+        }
+    }
+    __syncwarp();
+}
+
+// kappa(t) along the ray from its records (all lanes get the sum)
+__device__ __forceinline__ float kappa_at(const float4* __restrict__ rec, uint32_t ng, uint32_t nb, uint32_t cap,
+                                          float t) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nside[2] = {ng, nb};
+    float kap = 0.0f;
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+        for (uint32_t i = lane; i < nside[side]; i += 32) {
+            const uint32_t slot = side == 0 ? i : cap - 1 - i;
+            const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
+            const float ut = fmaf(b.y, t - b.z, b.w);
+            if (ut > a.x && ut < a.y) {
+                float sp, cp;
+                sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
+                kap += b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut)) * cp;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kap += __shfl_xor_sync(0xFFFFFFFFu, kap, o);
+    return kap;
+}
+
+// Next tentative collision: advance t through the majorant bins by an exponential step of unit
+// majorant optical depth (-ln(1-u)); false if the ray leaves [wa, wb].  k = current bin.
+__device__ __forceinline__ bool majorant_step(const float* M, float wa, float wb, float u, float& t, int& k) {
+    const float bw = (wb - wa) * (1.0f / 64.0f);
+    float tb = -log1pf(-u);
+    while (k < 64) {
+        const float be = (k == 63) ? wb : wa + (float)(k + 1) * bw;
+        const float m = M[k], seg = be - t;
+        if (m * seg <= tb) {
+            tb -= m * seg;
+            t = be;
+            ++k;
+        } else {
+            t += tb / m;
+            return true;
+        }
+    }
+    return false;
+}
+
+// free flight by delta tracking (one warp per path; records in the k_ff buffers)
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_ff_trk(RenderDev R, int32_t sample, int32_t depth) {
+    __shared__ WarpTrav s_t[4];
+    __shared__ float s_m[4][64];
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t count = R.qcount[0], cap = (uint32_t)R.rec_cap;
+    float4* __restrict__ rec = R.wrec + ((size_t)blockIdx.x * 4 + wid) * cap * 2;
+    float* M = s_m[wid];
+    Work wk;
+    uint32_t nray = 0;
+    while (true) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(R.qcount + kWorkAT, 1u);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= count) break;
+        const uint32_t p = R.qA[idx];
+        ++nray;
+        if (COUNT && lane == 0) ++wk.paths;
+        const uint32_t pix = R.pix[p];
+        const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
+        float w[kMaxGroups];
+        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                 ST_EXT, 1, w)
+                                    : R.ext.static_mask;
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        float tlo, thi;
+        if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
+            if (lane == 0) R.L[p] += R.beta[p] * R.env_L;
+            continue;
+        }
+        uint32_t ng, nb;
+        if (!emit_records<STOCH, COUNT>(R, r, tlo, thi, mask, w, s_t[wid], rec, cap, ng, nb, wk)) {
+            if (lane == 0) R.qO[atomicAdd(R.qcount + kCntO, 1u)] = p;  // analytic single-pass fallback
+            continue;
+        }
+        majorant_bins(rec, ng, nb, cap, tlo, thi, M);
+        float t = tlo;
+        int k = 0;
+        bool collide = false;
+        for (uint32_t j = 0; j < (1u << 20); ++j) {
+            const uint4 bl = stream_block(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_TRK, 4 * j);
+            if (!majorant_step(M, tlo, thi, u01(bl.x), t, k)) break;
+            if (COUNT && lane == 0) ++wk.root;
+            const float kap = kappa_at(rec, ng, nb, cap, t);
+            if (u01(bl.y) * M[k] < kap) { collide = true; break; }  // real collision
+        }
+        if (lane == 0) {
+            if (collide) {
+                R.ox[p] = fmaf(t, d.x, o.x);
+                R.oy[p] = fmaf(t, d.y, o.y);
+                R.oz[p] = fmaf(t, d.z, o.z);
+                R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
+            } else {
+                R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+}
+
+// NEE with ratio tracking: T = prod_j (1 - kappa(t_j) / M(t_j)) over the tentative points
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_nee_rt(RenderDev R, int32_t sample, int32_t depth) {
+    __shared__ WarpTrav s_t[4];
+    __shared__ WarpEnd s_e[4];
+    __shared__ float s_m[4][64];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t count = R.qcount[1], cap = (uint32_t)R.rec_cap;
+    float4* __restrict__ rec = R.wrec + ((size_t)blockIdx.x * 4 + wid) * cap * 2;
+    float* M = s_m[wid];
+    Work wk;
+    uint32_t nray = 0;
+    while (true) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(R.qcount + kWorkN, 1u);
+        idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+        if (idx >= count) break;
+        const uint32_t p = R.qB[idx];
+        const uint32_t pix = R.pix[p];
+        if (COUNT && lane == 0) ++wk.paths;
+        ++nray;
+        const float3 x = ld3(R.ox, R.oy, R.oz, p);
+        float w[kMaxGroups];
+        const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                 ST_NEE, 0, w)
+                                    : R.nee.static_mask;
+        const RayDev r = make_ray(x, R.sun, 0.0f, INFINITY);
+        float T = 1.0f, tlo, thi;
+        if (R.n_nodes > 0 && slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
+            uint32_t ng, nb;
+            if (emit_records<STOCH, COUNT>(R, r, tlo, thi, mask, w, s_t[wid], rec, cap, ng, nb, wk)) {
+                majorant_bins(rec, ng, nb, cap, tlo, thi, M);
+                float t = tlo;
+                int k = 0;
+                for (uint32_t j = 0; j < (1u << 20); ++j) {
+                    const uint4 bl = stream_block(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_TRK_NEE, 4 * j);
+                    if (!majorant_step(M, tlo, thi, u01(bl.x), t, k)) break;
+                    if (COUNT && lane == 0) ++wk.root;
+                    T *= 1.0f - kappa_at(rec, ng, nb, cap, t) / M[k];
+                }
+            } else {  // more records than the buffer: closed-form transmittance
+                T = (float)exp(-warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims, r, 0.0f,
+                                                       INFINITY, mask, w, s_t[wid], s_e[wid], wk));
+            }
+        }
+        if (lane == 0) {
+            const float3 d = ld3(R.dx, R.dy, R.dz, p);
+            const float beta = R.beta[p];
+            const float cost = d.x * R.sun.x + d.y * R.sun.y + d.z * R.sun.z;
+            R.L[p] += beta * R.albedo * hg_eval(R.hg_g, cost) * T * R.sun_E;
+            if (depth + 1 < R.max_depth) {
+                uint4 b = stream_block(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_SCAT, 0);
+                float3 nd = hg_sample(R.hg_g, d, u01(b.x), u01(b.y));
+                R.dx[p] = nd.x; R.dy[p] = nd.y; R.dz[p] = nd.z;
+                R.beta[p] = beta * R.albedo;
+                R.qNext[atomicAdd(R.qcount + 2, 1u)] = p;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && nray) atomicAdd(R.rays + 1, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_NEE, wk);
+}
+
 // NEE, one warp per path (warp_tau): shadow-ray transmittance, HG phase sampling of the next
 // direction.  Replaces the per-lane k_nee on the production path.
 template <bool STOCH, bool COUNT>
@@ -899,7 +1148,8 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
                          bool stoch_nee) {
     cudaEvent_t e;
     T.pre(STAGE_FFA, st, e);
-    k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    if (R.estimator == 1) k_ff_trk<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    else k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFA, st, e);
     T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")
     k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
@@ -908,8 +1158,13 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
     k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFB, st, e);
     T.pre(STAGE_NEE, st, e);
-    if (stoch_nee) k_nee_w<true, C><<<wgrid, 128, 0, st>>>(R, sample, d);
-    else k_nee_w<false, C><<<wgrid, 128, 0, st>>>(R, sample, d);
+    if (R.estimator == 1) {  // ratio tracking uses the k_ff record buffers (same grid)
+        if (stoch_nee) k_nee_rt<true, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+        else k_nee_rt<false, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    } else {
+        if (stoch_nee) k_nee_w<true, C><<<wgrid, 128, 0, st>>>(R, sample, d);
+        else k_nee_w<false, C><<<wgrid, 128, 0, st>>>(R, sample, d);
+    }
     T.post(STAGE_NEE, st, e);
 }
 

@@ -303,6 +303,35 @@ def test_render_record_fallback_paths(gfm, orc, monkeypatch):
     _probe_compare(gfm, orc, sc, desc, probes, 16, "record fallback", frac_tol=0.05)
 
 
+def _mean_parity(vg, vo, what, pix_frac=0.95):
+    """Different estimators of the same pixel values: global and per-pixel means within 3 combined SE."""
+    n = vg.shape[1]
+    se = math.sqrt(vg.var() / vg.size + vo.var() / vo.size)
+    assert abs(vg.mean() - vo.mean()) <= 3 * se + 1e-6, (what, vg.mean(), vo.mean(), se)
+    se_pix = np.sqrt(vg.var(1) / n + vo.var(1) / n) + 1e-9
+    ok = np.abs(vg.mean(1) - vo.mean(1)) <= 3 * se_pix + 1e-6
+    assert ok.mean() >= pix_frac, (what, ok.mean())
+
+
+@pytest.mark.parametrize("max_depth", [1, 3])
+def test_render_tracking_estimators_mean_parity(gfm, orc, max_depth):
+    """SURVEY §8 a9 alternative: delta tracking (free flight) + ratio tracking (NEE) against the
+    oracle's analytic estimator on a kappa >= 0 (paired-positive, C18) scene: same pixel means."""
+    sc = I.scene_cfg1p()
+    desc = I.render_desc_cfg2(3, 32, 32)
+    desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 32, 32))
+    desc.update(max_depth=max_depth, albedo=0.9, hg_g=0.3, ext=I.policy(), nee=I.policy())
+    probes = np.random.default_rng(7).integers(0, 32 * 32, 40)
+    spp = 96
+    f = field(gfm, sc)
+    vg, _ = f.render(dict(desc, estimator=1), 0, spp, probes=probes)
+    vg = vg.view(len(probes), spp).cpu().numpy().astype(np.float64)
+    vo, _ = orc.Scene(sc).render_probes(desc, probes, 0, spp)
+    _mean_parity(vg, vo, f"tracking depth {max_depth}")
+    va, _ = f.render(desc, 0, spp, probes=probes)  # analytic on the GPU: same means too
+    _mean_parity(vg, va.view(len(probes), spp).cpu().numpy().astype(np.float64), "tracking vs analytic gpu")
+
+
 @pytest.mark.parametrize("rec_cap", [None, "1024"])
 def test_column_more_hits_than_record_buffer(gfm, orc, monkeypatch, rec_cap):
     """1500 primitives along one axis: rays along it overlap all of them.  With a 1024-record buffer
