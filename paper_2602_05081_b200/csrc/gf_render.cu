@@ -640,10 +640,10 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
                 }
             }
         };
-        auto eval = [&](float t, double& kap_out) -> double {
+        auto eval = [&](float t, double& kap_out, double& dkap_out) -> double {
             if (COUNT && lane == 0) ++wk.root;
             acc = 0.0;
-            float part = 0.0f, kap = 0.0f;
+            float part = 0.0f, kap = 0.0f, dkap = 0.0f;
 #pragma unroll 1
             for (int side = 0; side < 2; ++side) {
                 const uint32_t n = nside[side];
@@ -660,7 +660,9 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
                         } else if (ut > a.x) {
                             float sp, cp;
                             sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
-                            kap += b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut)) * cp;
+                            const float kk = b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut));
+                            kap += kk * cp;
+                            dkap -= kk * b.y * fmaf(ut, cp, a.z * sp);  // d kappa / dt (Halley step)
                             if (x.y != x.y) {  // special record: lane-local partial integral
                                 Setup s;
                                 s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
@@ -685,13 +687,15 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
             }
             while (nq0 > 0) run(0, min(nq0, 32));
             while (nq1 > 0) run(1, min(nq1, 32));
-            double x = acc + (double)part, k = kap;
+            double x = acc + (double)part, k = kap, dk = dkap;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 x += __shfl_xor_sync(FULL, x, o);
                 k += __shfl_xor_sync(FULL, k, o);
+                dk += __shfl_xor_sync(FULL, dk, o);
             }
             kap_out = k;
+            dkap_out = dk;
             return x - tstar;
         };
         const float bw = thi - tlo;
@@ -714,13 +718,16 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
             pos = __shfl_sync(FULL, pos, L);
             t = fminf(fmaxf(tlo + pos * (bw * (1.0f / 64.0f)), lo), hi);
         }
-        double kap = 0.0;
+        double kap = 0.0, dkap = 0.0;
         for (int it = 0; it < 48; ++it) {
-            const double f = eval(t, kap);
+            const double f = eval(t, kap, dkap);
             if (f >= 0.0) hi = t; else lo = t;
             if (!(hi - lo > 1e-6f * bw)) break;
             if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
-            float tn = (kap > 0.0) ? (float)((double)t - f / kap) : 0.5f * (lo + hi);
+            // Halley step (f' = kappa, f'' = d kappa/dt: cubic convergence), Newton if its
+            // denominator degenerates, bisection if the step leaves the bracket
+            const double den = 2.0 * kap * kap - f * dkap;
+            float tn = (kap > 0.0) ? (float)((double)t - (den > 0.0 ? 2.0 * f * kap / den : f / kap)) : 0.5f * (lo + hi);
             const bool newton = tn > lo && tn < hi;
             if (!newton) tn = 0.5f * (lo + hi);
             const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
