@@ -471,6 +471,194 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
 }
 
 
+// Phases 2-3 of the free flight of path p (whole warp): per-record chord integrals -> tau_total ->
+// escape or the root of tau(t) = tau* (Halley / Newton / bisection over the records), then the
+// path's new origin or its environment contribution.  rec/aux: the ray's ng Gaussian (front) and
+// nb Gabor (back) records in a region of cap records.
+template <bool COUNT>
+__device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float3 o, float3 d, float tlo, float thi,
+                                           double tstar, const float4* __restrict__ rec, float4* __restrict__ aux,
+                                           uint32_t cap, uint32_t ng, uint32_t nb, float* hist, WarpEnd& q, Work& wk) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    // 2. per-record full integrals -> tau_total, histogram over 64 t-bins by chord centre
+    float tot = 0.0f;
+    const float hscale = 64.0f / fmaxf(thi - tlo, 1e-30f);
+    hist[lane] = 0.0f;
+    hist[lane + 32] = 0.0f;
+    __syncwarp();
+    const uint32_t nside[2] = {ng, nb};
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+        for (uint32_t i = lane; i < nside[side]; i += 32) {
+            const uint32_t slot = side == 0 ? i : cap - 1 - i;
+            const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
+            float full, g0 = 0.0f, ac = 0.0f, as = 0.0f;
+            const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
+            if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
+                // rare: midpoint / Gauss-Legendre (seg_J with e^{-r2/2} and 1/2 e^{-Om^2/2} in amp)
+                Setup s;
+                s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                s.Om = a.z; s.phi0 = a.w;
+                full = 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, a.y, wk);
+                g0 = __int_as_float(0x7fc00000);  // NaN marks a special record
+            } else {
+                float sp = 0.0f, cp = 1.0f;
+                if (side == 1 || a.w != 0.0f) sincos_red(a.w, &sp, &cp);
+                ac = b.x * cp; as = -b.x * sp;
+                float2 F1;
+                if (side == 0) { F1 = make_float2(erff(a.y * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
+                else { F1 = erf_shift(a.y, a.z); if (COUNT) ++wk.erfc; }
+                const float G1 = fmaf(ac, F1.x, as * F1.y);
+                if (a.x == -a.y) {
+                    g0 = -fmaf(ac, F1.x, -as * F1.y);  // F(-h) = -conj F(h)
+                } else {
+                    float2 F0;
+                    if (side == 0) { F0 = make_float2(erff(a.x * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
+                    else { F0 = erf_shift(a.x, a.z); if (COUNT) ++wk.erfc; }
+                    g0 = fmaf(ac, F0.x, as * F0.y);
+                }
+                full = G1 - g0;
+            }
+            aux[slot] = make_float4(full, g0, ac, as);
+            tot += full;
+            const float tm = b.z + (0.5f * (a.x + a.y) - b.w) / b.y;
+            atomicAdd(&hist[min(63, max(0, (int)((tm - tlo) * hscale)))], full);
+        }
+    }
+    double tau_tot = tot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tau_tot += __shfl_xor_sync(FULL, tau_tot, o);
+    if (tau_tot < tstar) {  // escape -> environment
+        if (lane == 0) R.L[p] += R.beta[p] * R.env_L;
+        return;
+    }
+    __syncwarp();
+    // 3. Newton / bisection on f(t) = tau(t) - tau*
+    int nq0 = 0, nq1 = 0;
+    double acc = 0.0;
+    auto run = [&](int t, int take) {
+        int& nq = t == 0 ? nq0 : nq1;
+        const bool v = lane < take;
+        const float4 e = v ? q.e[t][nq - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        nq -= take;
+        __syncwarp();
+        if (v) {
+            const float zr = e.x * kRsqrt2;
+            if (t == 0) {
+                if (COUNT) ++wk.erfr;
+                acc += (double)(e.z * erff(zr));
+            } else {
+                if (COUNT) ++wk.erfc;
+                const float zi = -e.y * kRsqrt2;
+                const float2 F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
+                acc += (double)fmaf(e.z, F.x, e.w * F.y);
+            }
+        }
+    };
+    auto eval = [&](float t, double& kap_out, double& dkap_out) -> double {
+        if (COUNT && lane == 0) ++wk.root;
+        acc = 0.0;
+        float part = 0.0f, kap = 0.0f, dkap = 0.0f;
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+            const uint32_t n = nside[side];
+            for (uint32_t base = 0; base < n; base += 32) {
+                const uint32_t i = base + lane;
+                bool push = false;
+                float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                if (i < n) {
+                    const uint32_t slot = side == 0 ? i : cap - 1 - i;
+                    const float4 a = rec[2 * slot], b = rec[2 * slot + 1], x = aux[slot];
+                    const float ut = fmaf(b.y, t - b.z, b.w);
+                    if (ut >= a.y) {
+                        part += x.x;
+                    } else if (ut > a.x) {
+                        float sp, cp;
+                        sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
+                        const float kk = b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut));
+                        kap += kk * cp;
+                        dkap -= kk * b.y * fmaf(ut, cp, a.z * sp);  // d kappa / dt (Halley step)
+                        if (x.y != x.y) {  // special record: lane-local partial integral
+                            Setup s;
+                            s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                            s.Om = a.z; s.phi0 = a.w;
+                            part += 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, ut, wk);
+                        } else {
+                            part -= x.y;
+                            push = true;
+                            e = make_float4(ut, a.z, x.z, x.w);
+                        }
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, push);
+                if (m) {
+                    int& nq = side == 0 ? nq0 : nq1;
+                    if (push) q.e[side][nq + __popc(m & lt)] = e;
+                    nq += __popc(m);
+                    __syncwarp();
+                    if (nq >= 32) run(side, 32);
+                }
+            }
+        }
+        while (nq0 > 0) run(0, min(nq0, 32));
+        while (nq1 > 0) run(1, min(nq1, 32));
+        double x = acc + (double)part, k = kap, dk = dkap;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            x += __shfl_xor_sync(FULL, x, o);
+            k += __shfl_xor_sync(FULL, k, o);
+            dk += __shfl_xor_sync(FULL, dk, o);
+        }
+        kap_out = k;
+        dkap_out = dk;
+        return x - tstar;
+    };
+    const float bw = thi - tlo;
+    float lo = tlo, hi = thi;
+    float t;
+    {  // start: first crossing of tau* in the histogram's running sum (linear inside the bin)
+        const float h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
+        float incl = h0 + h1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const unsigned m = __ballot_sync(FULL, (double)incl >= tstar);
+        const int L = m ? __ffs(m) - 1 : 31;
+        const float ts = (float)tstar, prev = incl - (h0 + h1);
+        float pos;
+        if (prev + h0 >= ts) pos = 2 * lane + fminf(fmaxf((ts - prev) / fmaxf(h0, 1e-30f), 0.0f), 1.0f);
+        else pos = 2 * lane + 1 + fminf(fmaxf((ts - prev - h0) / fmaxf(h1, 1e-30f), 0.0f), 1.0f);
+        pos = __shfl_sync(FULL, pos, L);
+        t = fminf(fmaxf(tlo + pos * (bw * (1.0f / 64.0f)), lo), hi);
+    }
+    double kap = 0.0, dkap = 0.0;
+    for (int it = 0; it < 48; ++it) {
+        const double f = eval(t, kap, dkap);
+        if (f >= 0.0) hi = t; else lo = t;
+        if (!(hi - lo > 1e-6f * bw)) break;
+        if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
+        // Halley step (f' = kappa, f'' = d kappa/dt: cubic convergence), Newton if its
+        // denominator degenerates, bisection if the step leaves the bracket
+        const double den = 2.0 * kap * kap - f * dkap;
+        float tn = (kap > 0.0) ? (float)((double)t - (den > 0.0 ? 2.0 * f * kap / den : f / kap)) : 0.5f * (lo + hi);
+        const bool newton = tn > lo && tn < hi;
+        if (!newton) tn = 0.5f * (lo + hi);
+        const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
+        t = tn;
+        if (small) break;
+    }
+    if (lane == 0) {  // collision point becomes the new origin
+        R.ox[p] = fmaf(t, d.x, o.x);
+        R.oy[p] = fmaf(t, d.y, o.y);
+        R.oz[p] = fmaf(t, d.z, o.z);
+        R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
+    }
+}
+
 // ---------------------------------------------------------------- free flight, one warp per path
 // k_ff fuses the whole free-flight step of a path (a8):
 //  1. warp_traverse over [t_lo, t_hi] (the root box span) emitting one 32-byte record per
@@ -565,181 +753,7 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
             continue;
         }
         __syncwarp();
-        // 2. per-record full integrals -> tau_total, histogram over 64 t-bins by chord centre
-        float tot = 0.0f;
-        const float hscale = 64.0f / fmaxf(thi - tlo, 1e-30f);
-        hist[lane] = 0.0f;
-        hist[lane + 32] = 0.0f;
-        __syncwarp();
-        const uint32_t nside[2] = {ng, nb};
-#pragma unroll 1
-        for (int side = 0; side < 2; ++side) {
-            for (uint32_t i = lane; i < nside[side]; i += 32) {
-                const uint32_t slot = side == 0 ? i : cap - 1 - i;
-                const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
-                float full, g0 = 0.0f, ac = 0.0f, as = 0.0f;
-                const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
-                if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
-                    // rare: midpoint / Gauss-Legendre (seg_J with e^{-r2/2} and 1/2 e^{-Om^2/2} in amp)
-                    Setup s;
-                    s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
-                    s.Om = a.z; s.phi0 = a.w;
-                    full = 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, a.y, wk);
-                    g0 = __int_as_float(0x7fc00000);  // NaN marks a special record
-                } else {
-                    float sp = 0.0f, cp = 1.0f;
-                    if (side == 1 || a.w != 0.0f) sincos_red(a.w, &sp, &cp);
-                    ac = b.x * cp; as = -b.x * sp;
-                    float2 F1;
-                    if (side == 0) { F1 = make_float2(erff(a.y * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
-                    else { F1 = erf_shift(a.y, a.z); if (COUNT) ++wk.erfc; }
-                    const float G1 = fmaf(ac, F1.x, as * F1.y);
-                    if (a.x == -a.y) {
-                        g0 = -fmaf(ac, F1.x, -as * F1.y);  // F(-h) = -conj F(h)
-                    } else {
-                        float2 F0;
-                        if (side == 0) { F0 = make_float2(erff(a.x * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
-                        else { F0 = erf_shift(a.x, a.z); if (COUNT) ++wk.erfc; }
-                        g0 = fmaf(ac, F0.x, as * F0.y);
-                    }
-                    full = G1 - g0;
-                }
-                aux[slot] = make_float4(full, g0, ac, as);
-                tot += full;
-                const float tm = b.z + (0.5f * (a.x + a.y) - b.w) / b.y;
-                atomicAdd(&hist[min(63, max(0, (int)((tm - tlo) * hscale)))], full);
-            }
-        }
-        double tau_tot = tot;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tau_tot += __shfl_xor_sync(FULL, tau_tot, o);
-        if (tau_tot < tstar) {  // escape -> environment
-            if (lane == 0) R.L[p] += R.beta[p] * R.env_L;
-            continue;
-        }
-        __syncwarp();
-        // 3. Newton / bisection on f(t) = tau(t) - tau*
-        int nq0 = 0, nq1 = 0;
-        double acc = 0.0;
-        auto run = [&](int t, int take) {
-            int& nq = t == 0 ? nq0 : nq1;
-            const bool v = lane < take;
-            const float4 e = v ? q.e[t][nq - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            nq -= take;
-            __syncwarp();
-            if (v) {
-                const float zr = e.x * kRsqrt2;
-                if (t == 0) {
-                    if (COUNT) ++wk.erfr;
-                    acc += (double)(e.z * erff(zr));
-                } else {
-                    if (COUNT) ++wk.erfc;
-                    const float zi = -e.y * kRsqrt2;
-                    const float2 F = erf_horner<kErfTerms>(zr, zi, fmaf(zr, zr, -zi * zi), 2.0f * zr * zi);
-                    acc += (double)fmaf(e.z, F.x, e.w * F.y);
-                }
-            }
-        };
-        auto eval = [&](float t, double& kap_out, double& dkap_out) -> double {
-            if (COUNT && lane == 0) ++wk.root;
-            acc = 0.0;
-            float part = 0.0f, kap = 0.0f, dkap = 0.0f;
-#pragma unroll 1
-            for (int side = 0; side < 2; ++side) {
-                const uint32_t n = nside[side];
-                for (uint32_t base = 0; base < n; base += 32) {
-                    const uint32_t i = base + lane;
-                    bool push = false;
-                    float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                    if (i < n) {
-                        const uint32_t slot = side == 0 ? i : cap - 1 - i;
-                        const float4 a = rec[2 * slot], b = rec[2 * slot + 1], x = aux[slot];
-                        const float ut = fmaf(b.y, t - b.z, b.w);
-                        if (ut >= a.y) {
-                            part += x.x;
-                        } else if (ut > a.x) {
-                            float sp, cp;
-                            sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
-                            const float kk = b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut));
-                            kap += kk * cp;
-                            dkap -= kk * b.y * fmaf(ut, cp, a.z * sp);  // d kappa / dt (Halley step)
-                            if (x.y != x.y) {  // special record: lane-local partial integral
-                                Setup s;
-                                s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
-                                s.Om = a.z; s.phi0 = a.w;
-                                part += 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, ut, wk);
-                            } else {
-                                part -= x.y;
-                                push = true;
-                                e = make_float4(ut, a.z, x.z, x.w);
-                            }
-                        }
-                    }
-                    const unsigned m = __ballot_sync(FULL, push);
-                    if (m) {
-                        int& nq = side == 0 ? nq0 : nq1;
-                        if (push) q.e[side][nq + __popc(m & lt)] = e;
-                        nq += __popc(m);
-                        __syncwarp();
-                        if (nq >= 32) run(side, 32);
-                    }
-                }
-            }
-            while (nq0 > 0) run(0, min(nq0, 32));
-            while (nq1 > 0) run(1, min(nq1, 32));
-            double x = acc + (double)part, k = kap, dk = dkap;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                x += __shfl_xor_sync(FULL, x, o);
-                k += __shfl_xor_sync(FULL, k, o);
-                dk += __shfl_xor_sync(FULL, dk, o);
-            }
-            kap_out = k;
-            dkap_out = dk;
-            return x - tstar;
-        };
-        const float bw = thi - tlo;
-        float lo = tlo, hi = thi;
-        float t;
-        {  // start: first crossing of tau* in the histogram's running sum (linear inside the bin)
-            const float h0 = hist[2 * lane], h1 = hist[2 * lane + 1];
-            float incl = h0 + h1;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const float v = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const unsigned m = __ballot_sync(FULL, (double)incl >= tstar);
-            const int L = m ? __ffs(m) - 1 : 31;
-            const float ts = (float)tstar, prev = incl - (h0 + h1);
-            float pos;
-            if (prev + h0 >= ts) pos = 2 * lane + fminf(fmaxf((ts - prev) / fmaxf(h0, 1e-30f), 0.0f), 1.0f);
-            else pos = 2 * lane + 1 + fminf(fmaxf((ts - prev - h0) / fmaxf(h1, 1e-30f), 0.0f), 1.0f);
-            pos = __shfl_sync(FULL, pos, L);
-            t = fminf(fmaxf(tlo + pos * (bw * (1.0f / 64.0f)), lo), hi);
-        }
-        double kap = 0.0, dkap = 0.0;
-        for (int it = 0; it < 48; ++it) {
-            const double f = eval(t, kap, dkap);
-            if (f >= 0.0) hi = t; else lo = t;
-            if (!(hi - lo > 1e-6f * bw)) break;
-            if (fabs(f) <= 1e-6 * (1.0 + tstar)) break;  // |tau(t) - tau*| at the fp32 noise floor
-            // Halley step (f' = kappa, f'' = d kappa/dt: cubic convergence), Newton if its
-            // denominator degenerates, bisection if the step leaves the bracket
-            const double den = 2.0 * kap * kap - f * dkap;
-            float tn = (kap > 0.0) ? (float)((double)t - (den > 0.0 ? 2.0 * f * kap / den : f / kap)) : 0.5f * (lo + hi);
-            const bool newton = tn > lo && tn < hi;
-            if (!newton) tn = 0.5f * (lo + hi);
-            const bool small = newton && fabsf(tn - t) <= 1e-5f * bw;  // converged Newton step
-            t = tn;
-            if (small) break;
-        }
-        if (lane == 0) {  // collision point becomes the new origin
-            R.ox[p] = fmaf(t, d.x, o.x);
-            R.oy[p] = fmaf(t, d.y, o.y);
-            R.oz[p] = fmaf(t, d.z, o.z);
-            R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
-        }
+        ff_resolve<COUNT>(R, p, o, d, tlo, thi, tstar, rec, aux, cap, ng, nb, hist, q, wk);
         __syncwarp();
     }
     if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
