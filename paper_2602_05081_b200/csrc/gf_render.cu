@@ -25,7 +25,7 @@ constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6;  // cursors: (unused), k_ffB, 
 constexpr int kCntO = 9, kWorkAT = 10, kWorkAO = 12;  // record-overflow queue count; k_ff / k_ffA cursors
 constexpr int kCntB2 = 13;  // single-pass ffA -> per-thread ffB queue
 #ifndef GF_REC_CAP
-#define GF_REC_CAP 16384
+#define GF_REC_CAP 32768
 #endif
 constexpr int kRecCap = GF_REC_CAP;  // hit records per k_ff warp buffer (overflow -> single-pass ffA)
 
@@ -182,6 +182,9 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 // tuning knobs (compile-time; bench variants are built with -D overrides)
 #ifndef GF_BATCH
 #define GF_BATCH 0
+#endif
+#ifndef GF_PACKET
+#define GF_PACKET 1  // depth-0 (camera) free flight with packet traversal (k_ff_pkt)
 #endif
 #ifndef GF_MINB_FFA
 #define GF_MINB_FFA 6
@@ -760,6 +763,153 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
 }
 
+// ---------------------------------------------------------------- free flight of coherent rays
+// k_ff_pkt: depth-0 camera rays, 32 consecutive paths per warp (one 8x4 pixel block of the tiled
+// path order, so the rays are nearly parallel and overlap the same primitives).  Packet traversal:
+// the warp walks ONE depth-first stack; each popped node's child pair is loaded once (broadcast)
+// and every lane tests it against its own ray; a child is descended if any lane's ray meets it,
+// and a hit leaf's primitives are loaded once and tested by each lane against its ray.  Each lane
+// writes its ray's hit records into its own region of the warp's buffer; then the warp resolves
+// the rays one after another with ff_resolve (chord integrals, escape test, root).
+constexpr int kPStk = 512;
+template <bool STOCH, bool COUNT>
+__global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int32_t depth) {
+    __shared__ uint32_t s_stk[4][kPStk];
+    __shared__ WarpEnd s_e[4];
+    __shared__ float s_h[4][64];
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t count = R.qcount[0], cap = (uint32_t)R.rec_cap, lcap = cap / 32;
+    const size_t gw = (size_t)blockIdx.x * 4 + wid;
+    float4* __restrict__ wrec = R.wrec + gw * cap * 2;
+    float4* __restrict__ waux = R.waux + gw * cap;
+    float4* __restrict__ myrec = wrec + (size_t)lane * lcap * 2;
+    uint32_t* stk = s_stk[wid];
+    Work wk;
+    uint32_t nray = 0;
+    while (true) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(R.qcount + kWorkAT, 32u);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= count) break;
+        const uint32_t idx = base + lane;
+        const bool valid = idx < count;
+        const uint32_t p = valid ? R.qA[idx] : 0u;
+        bool act = valid;
+        uint32_t pix = 0, mask = 0;
+        float3 o = make_float3(0.0f, 0.0f, 0.0f), d = make_float3(0.0f, 0.0f, 1.0f);
+        double tstar = 0.0;
+        float w[kMaxGroups];
+        if (valid) {
+            ++nray;
+            if (COUNT) ++wk.paths;
+            pix = R.pix[p];
+            o = ld3(R.ox, R.oy, R.oz, p);
+            d = ld3(R.dx, R.dy, R.dz, p);
+            mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 1, w)
+                         : R.ext.static_mask;
+            const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
+            tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
+            if (tstar <= 0.0) {  // collision at the origin
+                R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
+                act = false;
+            }
+        }
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        float tlo = 0.0f, thi = 0.0f;
+        if (act && (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi))) {
+            R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
+            act = false;
+        }
+        // packet traversal: one uniform depth-first walk for the 32 rays
+        uint32_t ng = 0, nb = 0;
+        auto leaf = [&](uint32_t info, bool mine) {
+            const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, g = info & 31u;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const GPrim* pp = R.prims + first + k;
+                GPrim P;
+                P.a = __ldg(&pp->a);
+                bool pass = false;
+                if (mine) {
+                    if (COUNT) ++wk.tests;
+                    pass = sphere_pretest(P.a, r, tlo, thi);
+                }
+                if (!__any_sync(FULL, pass)) continue;
+                P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                Setup s;
+                if (pass && prim_setup(P, r, tlo, thi, s)) {
+                    if (COUNT) ++wk.hits;
+                    float cj = P.d.w * s.ij;
+                    if (STOCH) cj *= w[g];
+                    const bool gs = s.Om == 0.0f;
+                    if (ng + nb < lcap) {
+                        const uint32_t slot = gs ? ng : lcap - 1 - nb;
+                        const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                        myrec[2 * slot] = make_float4(s.u0, s.u1, s.Om, s.phi0);
+                        myrec[2 * slot + 1] = make_float4(amp, s.j, s.tc, s.bp);
+                    }
+                    if (gs) ++ng; else ++nb;
+                }
+            }
+        };
+        if (__any_sync(FULL, act)) {
+            int ns = 0;
+            const float4 lo = __ldg(&R.nodes[0].lo), hi = __ldg(&R.nodes[0].hi);
+            const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+            if (COUNT && act) ++wk.nodes;
+            const bool hr = act && (node_mask(sk, info) & mask) && slab(r, lo, hi, tlo, thi);
+            if (__any_sync(FULL, hr)) {
+                if (sk & kLeafBit) leaf(info, hr);
+                else { stk[0] = 0; ns = 1; }
+            }
+            while (ns > 0) {
+                const uint32_t i = stk[--ns];
+                const GNode2* q = R.nodes2 + i;
+                const float4 lo0 = __ldg(&q->lo0), hi0 = __ldg(&q->hi0), lo1 = __ldg(&q->lo1), hi1 = __ldg(&q->hi1);
+                const uint32_t ref0 = __float_as_uint(lo0.w), inf0 = __float_as_uint(hi0.w);
+                const uint32_t ref1 = __float_as_uint(lo1.w), inf1 = __float_as_uint(hi1.w);
+                if (COUNT && act) wk.nodes += 2;
+                const bool h0 = act && (node_mask(ref0, inf0) & mask) && slab(r, lo0, hi0, tlo, thi);
+                const bool h1 = act && (node_mask(ref1, inf1) & mask) && slab(r, lo1, hi1, tlo, thi);
+                const bool a0 = __any_sync(FULL, h0), a1 = __any_sync(FULL, h1);
+                if (a1) {
+                    if (ref1 & kLeafBit) leaf(inf1, h1);
+                    else stk[ns++] = ref1;
+                }
+                if (a0) {
+                    if (ref0 & kLeafBit) leaf(inf0, h0);
+                    else stk[ns++] = ref0;
+                }
+                __syncwarp();
+            }
+        }
+        if (act && ng + nb > lcap) {  // record overflow: single-pass fallback
+            R.qO[atomicAdd(R.qcount + kCntO, 1u)] = p;
+            act = false;
+        }
+        __syncwarp();
+        // resolve the rays one after another with the whole warp
+        unsigned todo = __ballot_sync(FULL, act);
+        while (todo) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t pl = __shfl_sync(FULL, p, l);
+            const float3 ol = make_float3(__shfl_sync(FULL, o.x, l), __shfl_sync(FULL, o.y, l), __shfl_sync(FULL, o.z, l));
+            const float3 dl = make_float3(__shfl_sync(FULL, d.x, l), __shfl_sync(FULL, d.y, l), __shfl_sync(FULL, d.z, l));
+            const float tlol = __shfl_sync(FULL, tlo, l), thil = __shfl_sync(FULL, thi, l);
+            const double tsl = __shfl_sync(FULL, tstar, l);
+            const uint32_t ngl = __shfl_sync(FULL, ng, l), nbl = __shfl_sync(FULL, nb, l);
+            ff_resolve<COUNT>(R, pl, ol, dl, tlol, thil, tsl, wrec + (size_t)l * lcap * 2, waux + (size_t)l * lcap, lcap,
+                              ngl, nbl, s_h[wid], s_e[wid], wk);
+            __syncwarp();
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nray += __shfl_xor_sync(FULL, nray, off);
+    if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_FFA, wk);
+}
+
 // ---------------------------------------------------------------- tracking estimators (a9 alternative)
 // Null-collision delta tracking (free flight) and ratio tracking (NEE transmittance) against a
 // per-ray piecewise-constant majorant, selected by gf_render_desc.estimator = GF_EST_TRACKING.
@@ -1170,6 +1320,7 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
     cudaEvent_t e;
     T.pre(STAGE_FFA, st, e);
     if (R.estimator == 1) k_ff_trk<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    else if (d == 0 && GF_PACKET) k_ff_pkt<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
     else k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
     T.post(STAGE_FFA, st, e);
     T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")
