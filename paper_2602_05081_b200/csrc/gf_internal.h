@@ -102,7 +102,8 @@ struct RenderDev {
     float4* wrec;    // [k_ff warp][rec_cap] x 2 float4 hit records (per warp, reused across paths)
     float4* waux;    // [k_ff warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;
-    uint32_t* qO;    // record-overflow paths (single-pass k_ffA)
+    uint32_t* qO;    // record-overflow paths (k_ff redo after k_ff_pkt, else single-pass k_ffA)
+    uint32_t* qO2;   // record-overflow paths of the k_ff redo (single-pass k_ffA)
     uint32_t* qB2;   // record-overflow paths after single-pass ffA (per-thread ffB)
     // queues
     uint32_t *qA, *qB, *qNext;

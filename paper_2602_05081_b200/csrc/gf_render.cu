@@ -22,6 +22,7 @@ constexpr int kBins = GF_BINS;
 constexpr int kHitCap = 1024;  // hits recorded per path by ffA for ffB (overflow -> traversal gather)
 // qcount slots: 0 qA count, 1 qB count, 2 qNext count, then work cursors and fallback queues
 constexpr int kWorkA = 4, kWorkB = 5, kWorkN = 6;  // cursors: (unused), k_ffB, k_nee_w
+constexpr int kWorkRO = 7, kCntO2 = 8;  // k_ff redo of packet-overflow paths: cursor, its overflow count
 constexpr int kCntO = 9, kWorkAT = 10, kWorkAO = 12;  // record-overflow queue count; k_ff / k_ffA cursors
 constexpr int kCntB2 = 13;  // single-pass ffA -> per-thread ffB queue
 #ifndef GF_REC_CAP
@@ -677,14 +678,16 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
 // The buffer (rec_cap records per warp) stays L2-resident between the three phases; a path with
 // more records than rec_cap goes to the single-pass fallback (k_ffA + k_ffB).
 template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t depth,
+                                            const uint32_t* __restrict__ q_in, int cnt_slot, int cur_slot,
+                                            uint32_t* __restrict__ q_over, int over_slot) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];
     __shared__ float s_h[4][64];  // coarse tau(t) histogram of the chord integrals -> Newton start
     const unsigned FULL = 0xFFFFFFFFu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const uint32_t count = R.qcount[0], cap = (uint32_t)R.rec_cap;
+    const uint32_t count = R.qcount[cnt_slot], cap = (uint32_t)R.rec_cap;
     float* hist = s_h[wid];
     const size_t gw = (size_t)blockIdx.x * 4 + wid;
     float4* __restrict__ rec = R.wrec + gw * cap * 2;
@@ -694,10 +697,10 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
     uint32_t nray = 0;
     while (true) {
         uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(R.qcount + kWorkAT, 1u);
+        if (lane == 0) idx = atomicAdd(R.qcount + cur_slot, 1u);
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= count) break;
-        const uint32_t p = R.qA[idx];
+        const uint32_t p = q_in[idx];
         ++nray;
         if (COUNT && lane == 0) ++wk.paths;
         const uint32_t pix = R.pix[p];
@@ -752,7 +755,7 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
             nb += __popc(mb);
         });
         if (ng + nb > cap) {  // record overflow: single-pass fallback
-            if (lane == 0) R.qO[atomicAdd(R.qcount + kCntO, 1u)] = p;
+            if (lane == 0) q_over[atomicAdd(R.qcount + over_slot, 1u)] = p;
             continue;
         }
         __syncwarp();
@@ -1240,7 +1243,7 @@ __global__ void k_rotate(uint32_t* qc) {
     qc[0] = qc[2];
     qc[1] = 0; qc[2] = 0;
     qc[kWorkA] = 0; qc[kWorkB] = 0; qc[kWorkN] = 0;
-    qc[kCntO] = 0; qc[kWorkAT] = 0; qc[kWorkAO] = 0; qc[kCntB2] = 0;
+    qc[kCntO] = 0; qc[kWorkAT] = 0; qc[kWorkAO] = 0; qc[kCntB2] = 0; qc[kWorkRO] = 0; qc[kCntO2] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_finish(RenderDev R, int32_t slot) {
@@ -1301,13 +1304,13 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
     float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
-    uint32_t* qO = (uint32_t*)take(nu); uint32_t* qB2 = (uint32_t*)take(nu);
+    uint32_t* qO = (uint32_t*)take(nu); uint32_t* qB2 = (uint32_t*)take(nu); uint32_t* qO2 = (uint32_t*)take(nu);
     uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
         R->cum = cum; R->bin = bin; R->pix = pix; R->nhit = nhit; R->hits = hits; R->hit_cap = kHitCap;
         R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap;
-        R->qA = qA; R->qB = qB; R->qNext = qN; R->qO = qO; R->qB2 = qB2; R->qcount = qc;
+        R->qA = qA; R->qB = qB; R->qNext = qN; R->qO = qO; R->qB2 = qB2; R->qO2 = qO2; R->qcount = qc;
     }
     return off;
 }
@@ -1318,13 +1321,21 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
                          StageTimer& T,
                          bool stoch_nee) {
     cudaEvent_t e;
+    // coherent camera rays under one static mask: packet traversal
+    const bool packet = GF_PACKET && d == 0 && !S && R.estimator == 0;
     T.pre(STAGE_FFA, st, e);
     if (R.estimator == 1) k_ff_trk<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
-    else if (d == 0 && GF_PACKET) k_ff_pkt<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
-    else k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    else if (packet) k_ff_pkt<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    else k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qA, 0, kWorkAT, R.qO, kCntO);
     T.post(STAGE_FFA, st, e);
+    if (packet) {  // rays with more records than a packet lane holds: warp-per-ray k_ff (larger buffer),
+        T.pre(STAGE_FFB, st, e);  // timed with the fallbacks (stage "ff_fallback")
+        k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkRO, R.qO2, kCntO2);
+        T.post(STAGE_FFB, st, e);
+    }
     T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")
-    k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
+    if (packet) k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO2, kCntO2, kWorkAO, 0);
+    else k_ffA<S, C><<<pgrid, 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkAO, 0);
     T.post(STAGE_FFB, st, e);
     T.pre(STAGE_FFB, st, e);  // record-overflow paths (appended to qB for NEE)
     k_ffB<S, C><<<pgrid, 128, 0, st>>>(R, sample, d);
