@@ -82,13 +82,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def load_traffic(config, kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (or None)."""
+def load_traffic(config, stage):
+    """(kernel, DRAM bytes per launch) of the stage's kernel from the committed ncu --set full
+    capture, or (None, None)."""
     try:
         t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")))
-        return t[f"cfg{config}"][kernel]["dram_bytes_per_launch"]
+        e = t[f"cfg{config}"][stage]
+        return e["kernel"], e["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
-        return None
+        return None, None
 
 
 def load_peaks():
@@ -276,9 +278,11 @@ def main():
     props = torch.cuda.get_device_properties(local)
     peak = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
     clocks = clk.summary()
-    kernel = {"ff": "k_ff", "nee": "k_nee_w", "tomo": "k_tomo_w", "ff_fallback": "k_ffA+k_ffB"}.get(dom, dom)
+    tr_kernel, traffic = load_traffic(args.config, dom)
+    kernel = tr_kernel or {"ff": "k_ff_pkt (depth 0, static masks) / k_ff", "nee": "k_nee_w", "tomo": "k_tomo_w",
+                           "ff_fallback": "k_ffA+k_ffB"}.get(dom, dom)
     roofline = {"bound": "alu", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": load_traffic(args.config, kernel),
+                "frac": achieved / peak, "traffic": traffic,
                 "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
                                 "profiles/r01_traffic.json)",
                 "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz "

@@ -8,7 +8,7 @@ timeout 300 python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/pla
 if [ $rc = 0 ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu1.log 2>&1; echo "ncu launches rc=$?"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k k_ff -s 4 -c 4 -f -o gpurun_out/prof_ff \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k k_ff_pkt -s 4 -c 4 -f -o gpurun_out/prof_ff \
     python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu2.log 2>&1; echo "ncu ff rc=$?"
   timeout 1200 ncu --set full --clock-control none --import-source on -k k_nee_w -s 4 -c 4 -f -o gpurun_out/prof_nee \
     python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu3.log 2>&1; echo "ncu nee rc=$?"
