@@ -479,7 +479,42 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
 // escape or the root of tau(t) = tau* (Halley / Newton / bisection over the records), then the
 // path's new origin or its environment contribution.  rec/aux: the ray's ng Gaussian (front) and
 // nb Gabor (back) records in a region of cap records.
+// Per-record chord data of a hit record (a, b): full-chord integral amp (G(u1) - G(u0)),
+// amp G(u0) (NaN for a midpoint / Gauss-Legendre record), amp cos phi0, -amp sin phi0.
+// gabor: the series for Omega != 0 (else the real erf).
 template <bool COUNT>
+__device__ __forceinline__ float4 chord_aux(float4 a, float4 b, bool gabor, Work& wk) {
+    float full, g0 = 0.0f, ac = 0.0f, as = 0.0f;
+    const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
+    if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
+        // rare: midpoint / Gauss-Legendre (seg_J with e^{-r2/2} and 1/2 e^{-Om^2/2} in amp)
+        Setup s;
+        s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+        s.Om = a.z; s.phi0 = a.w;
+        full = 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, a.y, wk);
+        g0 = __int_as_float(0x7fc00000);  // NaN marks a special record
+    } else {
+        float sp = 0.0f, cp = 1.0f;
+        if (gabor || a.w != 0.0f) sincos_red(a.w, &sp, &cp);
+        ac = b.x * cp; as = -b.x * sp;
+        float2 F1;
+        if (!gabor) { F1 = make_float2(erff(a.y * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
+        else { F1 = erf_shift(a.y, a.z); if (COUNT) ++wk.erfc; }
+        const float G1 = fmaf(ac, F1.x, as * F1.y);
+        if (a.x == -a.y) {
+            g0 = -fmaf(ac, F1.x, -as * F1.y);  // F(-h) = -conj F(h)
+        } else {
+            float2 F0;
+            if (!gabor) { F0 = make_float2(erff(a.x * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
+            else { F0 = erf_shift(a.x, a.z); if (COUNT) ++wk.erfc; }
+            g0 = fmaf(ac, F0.x, as * F0.y);
+        }
+        full = G1 - g0;
+    }
+    return make_float4(full, g0, ac, as);
+}
+
+template <bool COUNT, bool PRE>
 __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float3 o, float3 d, float tlo, float thi,
                                            double tstar, const float4* __restrict__ rec, float4* __restrict__ aux,
                                            uint32_t cap, uint32_t ng, uint32_t nb, float* hist, WarpEnd& q, Work& wk) {
@@ -498,34 +533,14 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
         for (uint32_t i = lane; i < nside[side]; i += 32) {
             const uint32_t slot = side == 0 ? i : cap - 1 - i;
             const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
-            float full, g0 = 0.0f, ac = 0.0f, as = 0.0f;
-            const float wmax = 0.5f * (fmaxf(a.x * a.x, a.y * a.y) + a.z * a.z);
-            if (a.y - a.x < 1e-4f || (wmax > kWMaxSeries && a.z != 0.0f)) {
-                // rare: midpoint / Gauss-Legendre (seg_J with e^{-r2/2} and 1/2 e^{-Om^2/2} in amp)
-                Setup s;
-                s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
-                s.Om = a.z; s.phi0 = a.w;
-                full = 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, a.y, wk);
-                g0 = __int_as_float(0x7fc00000);  // NaN marks a special record
+            float full;
+            if (PRE) {
+                full = aux[slot].x;
             } else {
-                float sp = 0.0f, cp = 1.0f;
-                if (side == 1 || a.w != 0.0f) sincos_red(a.w, &sp, &cp);
-                ac = b.x * cp; as = -b.x * sp;
-                float2 F1;
-                if (side == 0) { F1 = make_float2(erff(a.y * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
-                else { F1 = erf_shift(a.y, a.z); if (COUNT) ++wk.erfc; }
-                const float G1 = fmaf(ac, F1.x, as * F1.y);
-                if (a.x == -a.y) {
-                    g0 = -fmaf(ac, F1.x, -as * F1.y);  // F(-h) = -conj F(h)
-                } else {
-                    float2 F0;
-                    if (side == 0) { F0 = make_float2(erff(a.x * kRsqrt2), 0.0f); if (COUNT) ++wk.erfr; }
-                    else { F0 = erf_shift(a.x, a.z); if (COUNT) ++wk.erfc; }
-                    g0 = fmaf(ac, F0.x, as * F0.y);
-                }
-                full = G1 - g0;
+                const float4 x = chord_aux<COUNT>(a, b, side == 1, wk);
+                aux[slot] = x;
+                full = x.x;
             }
-            aux[slot] = make_float4(full, g0, ac, as);
             tot += full;
             const float tm = b.z + (0.5f * (a.x + a.y) - b.w) / b.y;
             atomicAdd(&hist[min(63, max(0, (int)((tm - tlo) * hscale)))], full);
@@ -534,7 +549,7 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
     double tau_tot = tot;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tau_tot += __shfl_xor_sync(FULL, tau_tot, o);
-    if (tau_tot < tstar) {  // escape -> environment
+    if (!PRE && tau_tot < tstar) {  // escape -> environment
         if (lane == 0) R.L[p] += R.beta[p] * R.env_L;
         return;
     }
@@ -759,7 +774,7 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
             continue;
         }
         __syncwarp();
-        ff_resolve<COUNT>(R, p, o, d, tlo, thi, tstar, rec, aux, cap, ng, nb, hist, q, wk);
+        ff_resolve<COUNT, false>(R, p, o, d, tlo, thi, tstar, rec, aux, cap, ng, nb, hist, q, wk);
         __syncwarp();
     }
     if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
@@ -787,6 +802,7 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
     float4* __restrict__ wrec = R.wrec + gw * cap * 2;
     float4* __restrict__ waux = R.waux + gw * cap;
     float4* __restrict__ myrec = wrec + (size_t)lane * lcap * 2;
+    float4* __restrict__ myaux = waux + (size_t)lane * lcap;
     uint32_t* stk = s_stk[wid];
     Work wk;
     uint32_t nray = 0;
@@ -824,8 +840,10 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
             R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
             act = false;
         }
-        // packet traversal: one uniform depth-first walk for the 32 rays
+        // packet traversal: one uniform depth-first walk for the 32 rays; each lane integrates its
+        // own chords as they are found (tau_total), so only colliding rays need the records again
         uint32_t ng = 0, nb = 0;
+        double tau_tot = 0.0;
         auto leaf = [&](uint32_t info, bool mine) {
             const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, g = info & 31u;
             for (uint32_t k = 0; k < cnt; ++k) {
@@ -845,11 +863,15 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
                     float cj = P.d.w * s.ij;
                     if (STOCH) cj *= w[g];
                     const bool gs = s.Om == 0.0f;
+                    const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                    const float4 ra = make_float4(s.u0, s.u1, s.Om, s.phi0), rb = make_float4(amp, s.j, s.tc, s.bp);
+                    const float4 x = chord_aux<COUNT>(ra, rb, !gs, wk);  // all lanes: same primitive type
+                    tau_tot += (double)x.x;
                     if (ng + nb < lcap) {
                         const uint32_t slot = gs ? ng : lcap - 1 - nb;
-                        const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
-                        myrec[2 * slot] = make_float4(s.u0, s.u1, s.Om, s.phi0);
-                        myrec[2 * slot + 1] = make_float4(amp, s.j, s.tc, s.bp);
+                        myrec[2 * slot] = ra;
+                        myrec[2 * slot + 1] = rb;
+                        myaux[slot] = x;
                     }
                     if (gs) ++ng; else ++nb;
                 }
@@ -886,8 +908,12 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
                 __syncwarp();
             }
         }
-        if (act && ng + nb > lcap) {  // record overflow: single-pass fallback
+        if (act && ng + nb > lcap) {  // record overflow: warp-per-ray redo
             R.qO[atomicAdd(R.qcount + kCntO, 1u)] = p;
+            act = false;
+        }
+        if (act && tau_tot < tstar) {  // escape -> environment
+            R.L[p] += R.beta[p] * R.env_L;
             act = false;
         }
         __syncwarp();
@@ -902,8 +928,8 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
             const float tlol = __shfl_sync(FULL, tlo, l), thil = __shfl_sync(FULL, thi, l);
             const double tsl = __shfl_sync(FULL, tstar, l);
             const uint32_t ngl = __shfl_sync(FULL, ng, l), nbl = __shfl_sync(FULL, nb, l);
-            ff_resolve<COUNT>(R, pl, ol, dl, tlol, thil, tsl, wrec + (size_t)l * lcap * 2, waux + (size_t)l * lcap, lcap,
-                              ngl, nbl, s_h[wid], s_e[wid], wk);
+            ff_resolve<COUNT, true>(R, pl, ol, dl, tlol, thil, tsl, wrec + (size_t)l * lcap * 2, waux + (size_t)l * lcap,
+                                    lcap, ngl, nbl, s_h[wid], s_e[wid], wk);
             __syncwarp();
         }
     }
