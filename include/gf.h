@@ -178,7 +178,8 @@ typedef enum { GF_SHARD_NONE = 0, GF_SHARD_TILES = 1, GF_SHARD_SAMPLES = 2 } gf_
  * with right/up pre-scaled by tan(vfov/2) (*aspect), evaluated in fp32 with
  * correctly rounded operations.  jitter = 0 -> pixel centres.
  * TOMOGRAPHY: per sample tau-hat of the camera ray.
- * SCATTER: free flight (Eq. 5, bins + safeguarded Newton, C17), NEE to the
+ * SCATTER: free flight (Eq. 5: exact tau_total for the escape test, then the root of
+ *   tau(t) = tau* over the whole ray by safeguarded Halley/Newton/bisection, C17), NEE to the
  *   directional light (sun_dir towards the light, irradiance sun_E) with the
  *   nee policy, Henyey-Greenstein phase (g), grey albedo, constant env_L on
  *   escape, max_depth vertices (1 = single scattering), no Russian roulette (C19).
