@@ -406,8 +406,8 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
 gf_status gf_render_scratch_bytes(gf_ctx* c, const gf_render_desc* d, size_t* bytes) {
     if (!c || !bytes) return GF_E_INVALID_ARGUMENT;
     if (gf_status s = check_desc(c, d)) return s;
-    *bytes = gf_render_state_bytes(std::min<int64_t>(std::max<int64_t>(render_paths(d), 1), kRenderChunk), nullptr,
-                                   nullptr);
+    *bytes = gf_render_state_bytes(std::min<int64_t>(std::max<int64_t>(render_paths(d), 1), kRenderChunk), c->n,
+                                   nullptr, nullptr, nullptr);
     return GF_OK;
 }
 
@@ -418,13 +418,14 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     if (!c->loaded || !c->built) return fail(c, GF_E_STATE, "render before gf_load_primitives / gf_build_bvh");
     const int64_t np = render_paths(d);
     const int64_t chunk = std::min<int64_t>(std::max<int64_t>(np, 1), kRenderChunk);
-    size_t need = gf_render_state_bytes(chunk, nullptr, nullptr);
+    size_t need = gf_render_state_bytes(chunk, c->n, nullptr, nullptr, nullptr);
     if (scratch_bytes < need || !scratch) return fail(c, GF_E_OUT_OF_MEMORY, "render scratch too small");
     if (!accum && np > 0) return fail(c, GF_E_INVALID_ARGUMENT, "accum required");
     GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
     if (gf_status s = check_sticky(c)) return s;
     RenderDev R{};
-    gf_render_state_bytes(chunk, (char*)scratch, &R);
+    BuildScratch LS;
+    gf_render_state_bytes(chunk, c->n, (char*)scratch, &R, &LS);
     R.rec_cap = std::max(0, std::min(R.rec_cap, env_int("GF_DEBUG_REC_CAP", R.rec_cap)));
     R.nodes = c->nodes;
     R.nodes2 = c->nodes2;
@@ -461,6 +462,27 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.accum = accum;
     R.work = (c->prof & GF_PROFILE_WORK) ? c->d_work : nullptr;
     cudaStream_t st = (cudaStream_t)stream;
+    // NEE light BVH: a second tree over the primitives with boxes in a frame whose third axis is
+    // the light direction (shadow rays become axis-parallel); rebuilt per call, asynchronously
+    R.light = d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 &&
+              env_int("GF_DEBUG_NO_LIGHT_BVH", 0) == 0;
+    if (R.light) {
+        double z[3] = {d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]};
+        const double zn = std::sqrt(z[0] * z[0] + z[1] * z[1] + z[2] * z[2]);
+        for (double& v : z) v /= zn;
+        const double a[3] = {std::fabs(z[0]) < 0.9 ? 1.0 : 0.0, std::fabs(z[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+        double x[3] = {a[1] * z[2] - a[2] * z[1], a[2] * z[0] - a[0] * z[2], a[0] * z[1] - a[1] * z[0]};
+        const double xn = std::sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+        for (double& v : x) v /= xn;
+        const double y[3] = {z[1] * x[2] - z[2] * x[1], z[2] * x[0] - z[0] * x[2], z[0] * x[1] - z[1] * x[0]};
+        for (int k = 0; k < 3; ++k) {
+            R.lf[k] = (float)x[k]; R.lf[3 + k] = (float)y[k]; R.lf[6 + k] = (float)z[k];
+        }
+        GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.lf, R.lnodes, R.lnodes2, R.lprims, R.lperm,
+                                         R.ldepth, st),
+                "light BVH build");
+        c->timer.launches += 7;  // k_bounds, k_keys, k_karras, k_refit, k_layout, k_pair_dev, k_gather (+ CUB sort)
+    }
     for (int32_t k = 0; k < d->spp_count; ++k) {
         const int32_t s = d->spp_begin + k;
         if (d->shard_kind == GF_SHARD_SAMPLES && (s % R.shard_world) != d->shard_rank) continue;

@@ -108,8 +108,16 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
 }
 
-// conservative world AABB of the ellipsoid {mu + R S u : |u| <= E}: half-width_j = E |row_j(R S)|
-__global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cbounds) {
+// Frame of the BVH boxes: rows m[0..2], m[3..5], m[6..8] are the box axes (identity: world AABBs;
+// the NEE light BVH uses a frame whose third axis is the light direction).
+struct Frame {
+    float m[9];
+    int identity;
+};
+
+// conservative AABB (in frame F) of the ellipsoid {mu + R S u : |u| <= E}:
+// half-width along axis a = E |a^T (R S)|
+__global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cbounds, Frame F) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     GPrim P = prims[i];
@@ -119,18 +127,38 @@ __global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cb
     float s1 = 1.0f / (P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
     float s2 = 1.0f / (P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
     float E = sqrtf(P.c.w);
-    float hwx = E * sqrtf(P.b.x * P.b.x * s0 * s0 + P.c.x * P.c.x * s1 * s1 + P.d.x * P.d.x * s2 * s2);
-    float hwy = E * sqrtf(P.b.y * P.b.y * s0 * s0 + P.c.y * P.c.y * s1 * s1 + P.d.y * P.d.y * s2 * s2);
-    float hwz = E * sqrtf(P.b.z * P.b.z * s0 * s0 + P.c.z * P.c.z * s1 * s1 + P.d.z * P.d.z * s2 * s2);
+    float cx = P.a.x, cy = P.a.y, cz = P.a.z, hwx, hwy, hwz;
+    if (F.identity) {
+        hwx = E * sqrtf(P.b.x * P.b.x * s0 * s0 + P.c.x * P.c.x * s1 * s1 + P.d.x * P.d.x * s2 * s2);
+        hwy = E * sqrtf(P.b.y * P.b.y * s0 * s0 + P.c.y * P.c.y * s1 * s1 + P.d.y * P.d.y * s2 * s2);
+        hwz = E * sqrtf(P.b.z * P.b.z * s0 * s0 + P.c.z * P.c.z * s1 * s1 + P.d.z * P.d.z * s2 * s2);
+    } else {
+        const float v[3][3] = {{P.b.x * s0, P.b.y * s0, P.b.z * s0},   // columns of R S
+                               {P.c.x * s1, P.c.y * s1, P.c.z * s1},
+                               {P.d.x * s2, P.d.y * s2, P.d.z * s2}};
+        float hw[3], c[3];
+        for (int a = 0; a < 3; ++a) {
+            const float* f = F.m + 3 * a;
+            float acc = 0.0f;
+            for (int k = 0; k < 3; ++k) {
+                const float dk = f[0] * v[k][0] + f[1] * v[k][1] + f[2] * v[k][2];
+                acc += dk * dk;
+            }
+            hw[a] = E * sqrtf(acc);
+            c[a] = f[0] * P.a.x + f[1] * P.a.y + f[2] * P.a.z;
+        }
+        hwx = hw[0]; hwy = hw[1]; hwz = hw[2];
+        cx = c[0]; cy = c[1]; cz = c[2];
+    }
     // outward padding: relative 1e-4 of the half width + absolute term for the slab rounding
-    float padx = 1e-4f * hwx + 4e-6f * (1.0f + fabsf(P.a.x));
-    float pady = 1e-4f * hwy + 4e-6f * (1.0f + fabsf(P.a.y));
-    float padz = 1e-4f * hwz + 4e-6f * (1.0f + fabsf(P.a.z));
+    float padx = 1e-4f * hwx + 4e-6f * (1.0f + fabsf(cx));
+    float pady = 1e-4f * hwy + 4e-6f * (1.0f + fabsf(cy));
+    float padz = 1e-4f * hwz + 4e-6f * (1.0f + fabsf(cz));
     float* b = box + 6 * i;
-    b[0] = P.a.x - hwx - padx; b[1] = P.a.y - hwy - pady; b[2] = P.a.z - hwz - padz;
-    b[3] = P.a.x + hwx + padx; b[4] = P.a.y + hwy + pady; b[5] = P.a.z + hwz + padz;
-    atomicMin(cbounds + 0, f2ord(P.a.x)); atomicMin(cbounds + 1, f2ord(P.a.y)); atomicMin(cbounds + 2, f2ord(P.a.z));
-    atomicMax(cbounds + 3, f2ord(P.a.x)); atomicMax(cbounds + 4, f2ord(P.a.y)); atomicMax(cbounds + 5, f2ord(P.a.z));
+    b[0] = cx - hwx - padx; b[1] = cy - hwy - pady; b[2] = cz - hwz - padz;
+    b[3] = cx + hwx + padx; b[4] = cy + hwy + pady; b[5] = cz + hwz + padz;
+    atomicMin(cbounds + 0, f2ord(cx)); atomicMin(cbounds + 1, f2ord(cy)); atomicMin(cbounds + 2, f2ord(cz));
+    atomicMax(cbounds + 3, f2ord(cx)); atomicMax(cbounds + 4, f2ord(cy)); atomicMax(cbounds + 5, f2ord(cz));
 }
 
 __device__ __forceinline__ uint64_t expand3(uint32_t x) {
@@ -144,13 +172,15 @@ __device__ __forceinline__ uint64_t expand3(uint32_t x) {
 }
 
 __global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, const uint32_t* cbounds, uint64_t* keys,
-                       uint32_t* vals) {
+                       uint32_t* vals, Frame F) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     GPrim P = prims[i];
     float lo[3] = {ord2f(cbounds[0]), ord2f(cbounds[1]), ord2f(cbounds[2])};
     float hi[3] = {ord2f(cbounds[3]), ord2f(cbounds[4]), ord2f(cbounds[5])};
     float c[3] = {P.a.x, P.a.y, P.a.z};
+    if (!F.identity)
+        for (int a = 0; a < 3; ++a) c[a] = F.m[3 * a] * P.a.x + F.m[3 * a + 1] * P.a.y + F.m[3 * a + 2] * P.a.z;
     uint32_t q[3];
     for (int k = 0; k < 3; ++k) {
         float ext = hi[k] - lo[k];
@@ -312,6 +342,25 @@ __global__ void k_pair(const GNode* __restrict__ nodes, uint32_t total, GNode2* 
     out[i] = o;
 }
 
+// as k_pair, node count read on the device (asynchronous light-BVH build)
+__global__ void k_pair_dev(const GNode* __restrict__ nodes, const uint32_t* __restrict__ total, int64_t bound,
+                           GNode2* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= bound || i >= (int64_t)*total) return;
+    const uint32_t sk = __float_as_uint(nodes[i].lo.w);
+    if (sk & kLeafBit) return;
+    const uint32_t c0 = (uint32_t)i + 1;
+    const GNode a = nodes[c0];
+    const uint32_t c1 = __float_as_uint(a.lo.w) & ~kLeafBit;
+    const GNode b = nodes[c1];
+    GNode2 o;
+    o.lo0 = make_float4(a.lo.x, a.lo.y, a.lo.z, __uint_as_float((__float_as_uint(a.lo.w) & kLeafBit) ? kLeafBit : c0));
+    o.hi0 = a.hi;
+    o.lo1 = make_float4(b.lo.x, b.lo.y, b.lo.z, __uint_as_float((__float_as_uint(b.lo.w) & kLeafBit) ? kLeafBit : c1));
+    o.hi1 = b.hi;
+    out[i] = o;
+}
+
 __global__ void k_gather(const GPrim* in, const int32_t* perm, int64_t n, GPrim* out, int32_t* perm_out) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -379,8 +428,9 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
     if (n == 0) return cudaSuccess;
     uint32_t init[8] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u, 0u};
     if ((e = cudaMemcpyAsync(S.cbounds, init, sizeof(init), cudaMemcpyHostToDevice, st))) return e;
-    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds);
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in);
+    Frame I{{1, 0, 0, 0, 1, 0, 0, 0, 1}, 1};
+    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, I);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, I);
     size_t tb = S.sort_temp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
                                              0, 64, st)))
@@ -405,5 +455,40 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
     if ((e = cudaMemcpyAsync(max_depth, S.cbounds, sizeof(uint32_t), cudaMemcpyDeviceToHost, st))) return e;
     if ((e = cudaStreamSynchronize(st))) return e;
     *n_nodes = total;
+    return cudaGetLastError();
+}
+
+// Asynchronous build in frame F (host rows): same kernels, no host synchronisation; the node count
+// stays on the device (S.nsize[0]) and the tree depth is written to *depth (device).
+cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S,
+                                  const float* F, void* nodes_v, void* nodes2_v, void* sorted_v, int32_t* perm,
+                                  uint32_t* depth, cudaStream_t st) {
+    const GPrim* prims = (const GPrim*)prims_v;
+    GNode* nodes = (GNode*)nodes_v;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(depth, 0, sizeof(uint32_t), st))) return e;
+    if (n == 0) return cudaSuccess;
+    Frame Fr{};
+    for (int k = 0; k < 9; ++k) Fr.m[k] = F[k];
+    Fr.identity = 0;
+    if ((e = cudaMemsetAsync(S.cbounds, 0xFF, sizeof(uint32_t) * 3, st))) return e;
+    if ((e = cudaMemsetAsync(S.cbounds + 3, 0, sizeof(uint32_t) * 3, st))) return e;
+    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, Fr);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, Fr);
+    size_t tb = S.sort_temp_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
+                                             0, 64, st)))
+        return e;
+    if (n > 1) {
+        k_karras<<<nblk(n - 1, 256), 256, 0, st>>>(S.keys_out, n, S.left, S.right, S.parent, S.rlo, S.rhi);
+        if ((e = cudaMemsetAsync(S.flags, 0, sizeof(uint32_t) * n, st))) return e;
+    }
+    RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, group, S.nbox, S.nmask, S.ncount,
+                S.nsize, S.flags};
+    k_refit<<<nblk(n, 256), 256, 0, st>>>(R);
+    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, 0, depth};
+    k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
+    k_pair_dev<<<nblk(2 * n - 1, 256), 256, 0, st>>>(nodes, S.nsize, 2 * n - 1, (GNode2*)nodes2_v);
+    k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
     return cudaGetLastError();
 }

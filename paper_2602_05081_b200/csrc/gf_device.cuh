@@ -698,10 +698,10 @@ struct WarpTrav {
 };
 constexpr uint32_t kRefIdx = 0x07FFFFFFu;
 
-template <bool COUNT, class OnPrims>
-__device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
-                                              uint32_t n_nodes, int stk_limit, const RayDev& r, float t0, float t1,
-                                              uint32_t mask, WarpTrav& sm, Work& wk, OnPrims&& on_prims) {
+template <bool COUNT, class OnPrims, class BoxHit>
+__device__ __forceinline__ void warp_traverse_b(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
+                                                uint32_t n_nodes, int stk_limit, uint32_t mask, WarpTrav& sm, Work& wk,
+                                                OnPrims&& on_prims, BoxHit&& boxhit) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -711,7 +711,7 @@ __device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, c
         const float4 lo = __ldg(&nodes[0].lo), hi = __ldg(&nodes[0].hi);
         const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
         if (COUNT && lane == 0) ++wk.nodes;
-        if (!((node_mask(sk, info) & mask) && slab(r, lo, hi, t0, t1))) return;
+        if (!((node_mask(sk, info) & mask) && boxhit(lo, hi))) return;
         if (sk & kLeafBit) {
             const int cnt = (int)((info >> 5) & 7u);
             if (lane < cnt) sm.prm[lane] = ((info >> 8) + lane) | ((info & 31u) << 27);
@@ -743,8 +743,8 @@ __device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, c
                 const float4 lo0 = __ldg(&q->lo0), hi0 = __ldg(&q->hi0), lo1 = __ldg(&q->lo1), hi1 = __ldg(&q->hi1);
                 ref0 = __float_as_uint(lo0.w); inf0 = __float_as_uint(hi0.w);
                 ref1 = __float_as_uint(lo1.w); inf1 = __float_as_uint(hi1.w);
-                h0 = (node_mask(ref0, inf0) & mask) && slab(r, lo0, hi0, t0, t1);
-                h1 = (node_mask(ref1, inf1) & mask) && slab(r, lo1, hi1, t0, t1);
+                h0 = (node_mask(ref0, inf0) & mask) && boxhit(lo0, hi0);
+                h1 = (node_mask(ref1, inf1) & mask) && boxhit(lo1, hi1);
                 if (COUNT) wk.nodes += 2;
             }
             const bool i0 = h0 && !(ref0 & kLeafBit), i1 = h1 && !(ref1 & kLeafBit);
@@ -778,6 +778,15 @@ __device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, c
     }
 }
 
+// world-frame boxes: slab test of ray r over [t0, t1]
+template <bool COUNT, class OnPrims>
+__device__ __forceinline__ void warp_traverse(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
+                                              uint32_t n_nodes, int stk_limit, const RayDev& r, float t0, float t1,
+                                              uint32_t mask, WarpTrav& sm, Work& wk, OnPrims&& on_prims) {
+    warp_traverse_b<COUNT>(nodes, n2, n_nodes, stk_limit, mask, sm, wk, on_prims,
+                           [&](float4 lo, float4 hi) { return slab(r, lo, hi, t0, t1); });
+}
+
 // Endpoint queues of the warp integrator: a hit's integral is Re{e^{i phi0} [F(u1) - F(u0)]} amp
 // (seg_J), i.e. one or two erf endpoints, each queued as (u, Omega, A, B) with the contribution
 // A Re F(u) + B Im F(u): symmetric full chord (F(h) - F(-h) = 2 Re F(h)): (h, Om, 2 amp cos phi0, 0);
@@ -791,11 +800,11 @@ struct WarpEnd {
 
 // tau of one ray (all 32 lanes call; the result is returned on every lane).  Weights w[g] apply
 // when STOCH (stochastic LOD masks).
-template <bool STOCH, bool COUNT>
-__device__ __forceinline__ double warp_tau(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
-                                           uint32_t n_nodes, int stk_limit, const GPrim* __restrict__ prims,
-                                           const RayDev& r, float t0, float t1, uint32_t mask, const float* w,
-                                           WarpTrav& sm, WarpEnd& q, Work& wk) {
+template <bool STOCH, bool COUNT, class BoxHit>
+__device__ __forceinline__ double warp_tau_b(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
+                                             uint32_t n_nodes, int stk_limit, const GPrim* __restrict__ prims,
+                                             const RayDev& r, float t0, float t1, uint32_t mask, const float* w,
+                                             WarpTrav& sm, WarpEnd& q, Work& wk, BoxHit&& boxhit) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -820,7 +829,7 @@ __device__ __forceinline__ double warp_tau(const GNode* __restrict__ nodes, cons
             }
         }
     };
-    warp_traverse<COUNT>(nodes, n2, n_nodes, stk_limit, r, t0, t1, mask, sm, wk, [&](bool valid, uint32_t ref) {
+    warp_traverse_b<COUNT>(nodes, n2, n_nodes, stk_limit, mask, sm, wk, [&](bool valid, uint32_t ref) {
         int ne = 0;
         bool real = false;
         float4 e0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), e1 = e0;
@@ -872,12 +881,21 @@ __device__ __forceinline__ double warp_tau(const GNode* __restrict__ nodes, cons
                 while (nq >= 32) run(t, 32);
             }
         }
-    });
+    }, boxhit);
     while (nq0 > 0) run(0, min(nq0, 32));
     while (nq1 > 0) run(1, min(nq1, 32));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
     return acc;
+}
+
+template <bool STOCH, bool COUNT>
+__device__ __forceinline__ double warp_tau(const GNode* __restrict__ nodes, const GNode2* __restrict__ n2,
+                                           uint32_t n_nodes, int stk_limit, const GPrim* __restrict__ prims,
+                                           const RayDev& r, float t0, float t1, uint32_t mask, const float* w,
+                                           WarpTrav& sm, WarpEnd& q, Work& wk) {
+    return warp_tau_b<STOCH, COUNT>(nodes, n2, n_nodes, stk_limit, prims, r, t0, t1, mask, w, sm, q, wk,
+                                    [&](float4 lo, float4 hi) { return slab(r, lo, hi, t0, t1); });
 }
 
 }  // namespace gfk

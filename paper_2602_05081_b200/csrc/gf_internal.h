@@ -104,6 +104,14 @@ struct RenderDev {
     int32_t rec_cap;
     uint32_t* qO;    // record-overflow paths (k_ff redo after k_ff_pkt, else single-pass k_ffA)
     uint32_t* qO2;   // record-overflow paths of the k_ff redo (single-pass k_ffA)
+    // light BVH for NEE (built per gf_render call in the frame lf: rows x', y', z' = light direction)
+    int32_t light;
+    float lf[9];
+    gfk::GNode* lnodes;
+    gfk::GNode2* lnodes2;
+    gfk::GPrim* lprims;
+    int32_t* lperm;
+    uint32_t* ldepth;
     uint32_t* qB2;   // record-overflow paths after single-pass ffA (per-thread ffB)
     // queues
     uint32_t *qA, *qB, *qNext;
@@ -119,8 +127,11 @@ BuildScratch gf_scratch_layout(int64_t n, char* base);
 cudaError_t gf_launch_build(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes,
                             void* nodes2, void* sorted, int32_t* perm, uint32_t* n_nodes, uint32_t* max_depth,
                             float* root_box, cudaStream_t st);
+cudaError_t gf_launch_build_frame(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S,
+                                  const float* F, void* nodes, void* nodes2, void* sorted, int32_t* perm,
+                                  uint32_t* depth, cudaStream_t st);
 cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
 cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
-size_t gf_render_state_bytes(int64_t n_paths, char* base, RenderDev* R);
+size_t gf_render_state_bytes(int64_t n_paths, int64_t n_prims, char* base, RenderDev* R, BuildScratch* light_scratch);
 cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t sample_slot, cudaStream_t st,
                                   StageTimer& T);

@@ -1190,12 +1190,16 @@ __global__ void __launch_bounds__(128) k_nee_rt(RenderDev R, int32_t sample, int
 
 // NEE, one warp per path (warp_tau): shadow-ray transmittance, HG phase sampling of the next
 // direction.  Replaces the per-lane k_nee on the production path.
-template <bool STOCH, bool COUNT>
+// LIGHT: traverse the light BVH (boxes in a frame whose third axis is the light direction, built
+// per gf_render call by gf_launch_build_frame): the shadow ray is axis-parallel there, so a box test
+// is two interval tests and one compare, and the boxes are tight across the rays' direction.
+template <bool STOCH, bool COUNT, bool LIGHT>
 __global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int32_t depth) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t count = R.qcount[1];
+    const int lstk = LIGHT ? max(1, kWStk - 34 - (int)*R.ldepth) : 0;
     Work wk;
     uint32_t nray = 0;
     while (true) {
@@ -1212,9 +1216,22 @@ __global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int3
         const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                  ST_NEE, 0, w)
                                     : R.nee.static_mask;
-        const double tau = warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims,
-                                                  make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask, w,
-                                                  s_t[wid], s_e[wid], wk);
+        double tau;
+        if (LIGHT) {
+            const float3 xp = make_float3(fmaf(R.lf[0], x.x, fmaf(R.lf[1], x.y, R.lf[2] * x.z)),
+                                          fmaf(R.lf[3], x.x, fmaf(R.lf[4], x.y, R.lf[5] * x.z)),
+                                          fmaf(R.lf[6], x.x, fmaf(R.lf[7], x.y, R.lf[8] * x.z)));
+            tau = warp_tau_b<STOCH, COUNT>(R.lnodes, R.lnodes2, R.n_nodes, lstk, R.lprims,
+                                           make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask, w, s_t[wid],
+                                           s_e[wid], wk, [&](float4 lo, float4 hi) {
+                                               return lo.x <= xp.x && xp.x <= hi.x && lo.y <= xp.y && xp.y <= hi.y &&
+                                                      hi.z >= xp.z;
+                                           });
+        } else {
+            tau = warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims,
+                                         make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask, w, s_t[wid],
+                                         s_e[wid], wk);
+        }
         if (lane == 0) {
             const float3 d = ld3(R.dx, R.dy, R.dz, p);
             const float beta = R.beta[p];
@@ -1316,7 +1333,7 @@ static unsigned ff_grid(int64_t n_paths) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (n_paths + 3) / 4));
 }
 
-size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
+size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* R, BuildScratch* LS) {
     size_t off = 0;
     auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += (bytes + 255) & ~(size_t)255; return p; };
     const size_t nf = sizeof(float) * (size_t)n, nu = sizeof(uint32_t) * (size_t)n;
@@ -1332,11 +1349,22 @@ size_t gf_render_state_bytes(int64_t n, char* base, RenderDev* R) {
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
     uint32_t* qO = (uint32_t*)take(nu); uint32_t* qB2 = (uint32_t*)take(nu); uint32_t* qO2 = (uint32_t*)take(nu);
     uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
+    // light BVH (NEE): nodes, child pairs, primitives in its leaf order, permutation, depth, build scratch
+    const size_t np1 = (size_t)std::max<int64_t>(n_prims, 1);
+    GNode* lnodes = (GNode*)take(sizeof(GNode) * 2 * np1);
+    GNode2* lnodes2 = (GNode2*)take(sizeof(GNode2) * 2 * np1);
+    GPrim* lprims = (GPrim*)take(sizeof(GPrim) * np1);
+    int32_t* lperm = (int32_t*)take(sizeof(int32_t) * np1);
+    uint32_t* ldepth = (uint32_t*)take(sizeof(uint32_t) * 4);
+    const size_t lsb = gf_scratch_layout(n_prims, nullptr).total_bytes;
+    char* lscratch = (char*)take(lsb);
+    if (LS) *LS = gf_scratch_layout(n_prims, lscratch);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
         R->cum = cum; R->bin = bin; R->pix = pix; R->nhit = nhit; R->hits = hits; R->hit_cap = kHitCap;
         R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qO = qO; R->qB2 = qB2; R->qO2 = qO2; R->qcount = qc;
+        R->lnodes = lnodes; R->lnodes2 = lnodes2; R->lprims = lprims; R->lperm = lperm; R->ldepth = ldepth;
     }
     return off;
 }
@@ -1370,9 +1398,12 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
     if (R.estimator == 1) {  // ratio tracking uses the k_ff record buffers (same grid)
         if (stoch_nee) k_nee_rt<true, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
         else k_nee_rt<false, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    } else if (R.light) {
+        if (stoch_nee) k_nee_w<true, C, true><<<wgrid, 128, 0, st>>>(R, sample, d);
+        else k_nee_w<false, C, true><<<wgrid, 128, 0, st>>>(R, sample, d);
     } else {
-        if (stoch_nee) k_nee_w<true, C><<<wgrid, 128, 0, st>>>(R, sample, d);
-        else k_nee_w<false, C><<<wgrid, 128, 0, st>>>(R, sample, d);
+        if (stoch_nee) k_nee_w<true, C, false><<<wgrid, 128, 0, st>>>(R, sample, d);
+        else k_nee_w<false, C, false><<<wgrid, 128, 0, st>>>(R, sample, d);
     }
     T.post(STAGE_NEE, st, e);
 }

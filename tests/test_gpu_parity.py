@@ -356,6 +356,32 @@ def test_column_more_hits_than_record_buffer(gfm, orc, monkeypatch, rec_cap):
     _probe_compare(gfm, orc, sc, desc, probes, 8, "column free flight", frac_tol=0.05)
 
 
+@pytest.mark.parametrize("stoch", [False, True])
+def test_nee_light_bvh_same_hits(gfm, monkeypatch, stoch):
+    """NEE traverses a second BVH whose boxes live in the light's frame (axis-parallel shadow rays).
+    It must find exactly the shadow-ray hits of the world BVH: same hit count, same image."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    desc = I.render_desc_cfg2(3, 64, 64)
+    desc.update(max_depth=3, albedo=0.9, hg_g=0.3)
+    if stoch:
+        desc.update(ext=I.policy(level_strategy=5, beta=0.2, orient_strategy=3),
+                    nee=I.policy(level_strategy=2, beta=0.5, orient_strategy=2))
+        f.load_primitives(sc, group_f0=I.group_f0(sc))
+        f.build_bvh()
+    out = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("GF_DEBUG_NO_LIGHT_BVH", off)
+        f.set_profiling(work=True)
+        acc, _ = f.render(desc, 0, 2)
+        st = f.stats(reset=True)
+        f.set_profiling()
+        out.append((acc.cpu().numpy(), st["work"]["nee"]))
+    assert out[0][1]["hits"] == out[1][1]["hits"] > 0
+    assert out[0][1]["paths"] == out[1][1]["paths"]
+    np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-4, atol=1e-5)
+
+
 def test_warp_traversal_depth_first_mode(gfm, orc, monkeypatch):
     """The warp traversal pops one node per step above its stack threshold (bounded stack);
     forcing that mode everywhere gives the same hits and transmittance."""
