@@ -237,10 +237,11 @@ struct RefitArgs {
     float* nbox;           // 2n-1 nodes x 6
     uint32_t *nmask, *ncount, *nsize;
     uint32_t* flags;
+    uint32_t leafmax;
 };
 
-__device__ __forceinline__ bool collapsed(uint32_t count, uint32_t mask) {
-    return count <= (uint32_t)kLeafMax && __popc(mask) == 1;
+__device__ __forceinline__ bool collapsed(uint32_t count, uint32_t mask, uint32_t leafmax) {
+    return count <= leafmax && __popc(mask) == 1;
 }
 
 __global__ void k_refit(RefitArgs A) {
@@ -269,7 +270,7 @@ __global__ void k_refit(RefitArgs A) {
         uint32_t cnt = ((volatile uint32_t*)A.ncount)[L] + ((volatile uint32_t*)A.ncount)[R];
         A.nmask[p] = m;
         A.ncount[p] = cnt;
-        A.nsize[p] = collapsed(cnt, m) ? 1u : 1u + ((volatile uint32_t*)A.nsize)[L] + ((volatile uint32_t*)A.nsize)[R];
+        A.nsize[p] = collapsed(cnt, m, A.leafmax) ? 1u : 1u + ((volatile uint32_t*)A.nsize)[L] + ((volatile uint32_t*)A.nsize)[R];
         __threadfence();
         x = p;
     }
@@ -283,6 +284,7 @@ struct LayoutArgs {
     GNode* out;
     uint32_t total;
     uint32_t* max_depth;
+    uint32_t leafmax;
 };
 
 __global__ void k_layout(LayoutArgs A) {
@@ -292,7 +294,7 @@ __global__ void k_layout(LayoutArgs A) {
     int64_t root = 0;
     if (x != root) {
         int32_t p = A.parent[x];
-        if (collapsed(A.ncount[p], A.nmask[p])) return;  // inside a collapsed leaf
+        if (collapsed(A.ncount[p], A.nmask[p], A.leafmax)) return;  // inside a collapsed leaf
     }
     // pre-order index: walk to the root
     uint32_t idx = 0, depth = 0;
@@ -306,7 +308,7 @@ __global__ void k_layout(LayoutArgs A) {
     }
     atomicMax(A.max_depth, depth);
     uint32_t cnt = A.ncount[x], m = A.nmask[x];
-    bool leaf = collapsed(cnt, m);
+    bool leaf = collapsed(cnt, m, A.leafmax);
     uint32_t skip = idx + A.nsize[x];
     uint32_t info;
     if (leaf) {
@@ -440,14 +442,15 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
         if ((e = cudaMemsetAsync(S.flags, 0, sizeof(uint32_t) * n, st))) return e;
     }
     RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, group, S.nbox, S.nmask, S.ncount,
-                S.nsize, S.flags};
+                S.nsize, S.flags, (uint32_t)kLeafMax};
     k_refit<<<nblk(n, 256), 256, 0, st>>>(R);
     // root (node 0 = internal root, or leaf 0 when n == 1 stored at n-1+0 = 0)
     uint32_t total = 0;
     if ((e = cudaMemcpyAsync(&total, S.nsize, sizeof(uint32_t), cudaMemcpyDeviceToHost, st))) return e;
     if ((e = cudaStreamSynchronize(st))) return e;
     if ((e = cudaMemsetAsync(S.cbounds, 0, sizeof(uint32_t), st))) return e;  // reused: max depth
-    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, total, S.cbounds};
+    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, total, S.cbounds,
+                 (uint32_t)kLeafMax};
     k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
     k_pair<<<nblk(total, 256), 256, 0, st>>>(nodes, total, (GNode2*)nodes2_v);
     k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
@@ -458,6 +461,10 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
     return cudaGetLastError();
 }
 
+#ifndef GF_LIGHT_LEAFMAX
+#define GF_LIGHT_LEAFMAX 4  // primitives per leaf of the NEE light BVH (measured: 1/2/3 slower)
+#endif
+static_assert(GF_LIGHT_LEAFMAX >= 1 && GF_LIGHT_LEAFMAX <= kLeafMax, "warp traversal buffers hold kLeafMax per leaf");
 // Asynchronous build in frame F (host rows): same kernels, no host synchronisation; the node count
 // stays on the device (S.nsize[0]) and the tree depth is written to *depth (device).
 cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S,
@@ -484,9 +491,10 @@ cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int
         if ((e = cudaMemsetAsync(S.flags, 0, sizeof(uint32_t) * n, st))) return e;
     }
     RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, group, S.nbox, S.nmask, S.ncount,
-                S.nsize, S.flags};
+                S.nsize, S.flags, (uint32_t)GF_LIGHT_LEAFMAX};
     k_refit<<<nblk(n, 256), 256, 0, st>>>(R);
-    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, 0, depth};
+    LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, 0, depth,
+                 (uint32_t)GF_LIGHT_LEAFMAX};
     k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
     k_pair_dev<<<nblk(2 * n - 1, 256), 256, 0, st>>>(nodes, S.nsize, 2 * n - 1, (GNode2*)nodes2_v);
     k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
