@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 2
+#define GF_ABI_VERSION 3
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -205,6 +205,8 @@ typedef struct {
     float albedo, hg_g, sun_dir[3], sun_E, env_L;
     uint64_t seed;
     int32_t estimator;          /* gf_estimator (SCATTER) */
+    int32_t reuse_accel;        /* 1: reuse the light / camera BVHs left in scratch by the previous
+                                   call (see gf_render); 0: rebuild them */
 } gf_render_desc;
 
 /* Device scratch needed by gf_render for `desc`. */
@@ -216,7 +218,13 @@ gf_status gf_render_scratch_bytes(gf_ctx *ctx, const gf_render_desc *desc, size_
  *     (only the shard's pixels/samples are touched; caller zeroes it);
  *   probes: n_probe * spp_count, accum[i*spp_count + k] = estimate of sample
  *     spp_begin + k at probe i (overwritten).
- * ray_counts: device uint64[2] or NULL, += (camera+extension rays, NEE rays). */
+ * ray_counts: device uint64[2] or NULL, += (camera+extension rays, NEE rays).
+ * scratch also holds two acceleration structures gf_render builds on the stream: the light BVH
+ *   (boxes in the light's frame, for NEE) and, for static camera masks, the camera BVH
+ *   (projective boxes at the eye, for the camera rays).  With desc->reuse_accel = 1 they are
+ *   reused when this call has the same scratch pointer, scene (no gf_load_primitives /
+ *   gf_build_bvh in between), light and camera as the one that built them: the caller
+ *   guarantees that scratch was not written in between. */
 gf_status gf_render(gf_ctx *ctx, const gf_render_desc *desc, float *accum, void *scratch, size_t scratch_bytes,
                     uint64_t *ray_counts, gf_stream stream);
 

@@ -40,7 +40,25 @@ struct gf_ctx {
     StageTimer timer;
     unsigned long long* d_work = nullptr;  // [8 stages][kWorkSlots]
     double stage_ms[N_STAGES] = {};
+    // scene generation (bumped by load/build) and the frame BVHs gf_render left in a scratch buffer
+    uint64_t gen = 0;
+    struct FrameCache {
+        const void* where = nullptr;  // node array inside the scratch
+        uint64_t gen = ~0ull;
+        float key[12] = {};
+    } light_cache, cam_cache;
 };
+
+// true if the frame BVH (node array at `where`, scene generation, key floats) is already there;
+// otherwise records it as built now
+static bool frame_cached(gf_ctx::FrameCache& fc, const void* where, uint64_t gen, const float* key, int nkey) {
+    bool same = fc.where == where && fc.gen == gen;
+    for (int k = 0; k < nkey && same; ++k) same = fc.key[k] == key[k];
+    fc.where = where;
+    fc.gen = gen;
+    for (int k = 0; k < nkey; ++k) fc.key[k] = key[k];
+    return same;
+}
 
 cudaEvent_t StageTimer::ev() {
     if (pool_used == pool.size()) {
@@ -260,6 +278,7 @@ gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_p
     c->dext = make_policy_dev(c->ext, P);
     c->dnee = make_policy_dev(c->nee, P);
     c->loaded = true;
+    ++c->gen;
     return GF_OK;
 }
 
@@ -292,6 +311,7 @@ gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch,
     c->max_depth = md;
     c->stk_limit = kWStk - 34 - (int)md;
     c->built = true;
+    ++c->gen;
     return GF_OK;
 }
 
@@ -478,10 +498,31 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         for (int k = 0; k < 3; ++k) {
             R.lf[k] = (float)x[k]; R.lf[3 + k] = (float)y[k]; R.lf[6 + k] = (float)z[k];
         }
-        GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.lf, R.lnodes, R.lnodes2, R.lprims, R.lperm,
-                                         R.ldepth, st),
-                "light BVH build");
-        c->timer.launches += 7;  // k_bounds, k_keys, k_karras, k_refit, k_layout, k_pair_dev, k_gather (+ CUB sort)
+        if (!frame_cached(c->light_cache, R.lnodes, c->gen, R.lf, 9) || !d->reuse_accel) {
+            GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.lf, nullptr, R.lnodes, R.lnodes2,
+                                             R.lprims, R.lperm, R.ldepth, st),
+                    "light BVH build");
+            c->timer.launches += 7;  // k_bounds, k_keys, k_karras, k_refit, k_layout, k_pair_dev, k_gather (+ CUB)
+        }
+    }
+    // camera BVH for the depth-0 packet kernel (static ext mask, analytic): projective boxes at the eye
+    if (d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 && c->ext.level_strategy == 0 &&
+        c->ext.orient_strategy == 0) {
+        const float* axes[3] = {d->cam_right, d->cam_up, d->cam_fwd};
+        for (int a = 0; a < 3; ++a) {
+            const double nn = std::sqrt((double)axes[a][0] * axes[a][0] + (double)axes[a][1] * axes[a][1] +
+                                        (double)axes[a][2] * axes[a][2]);
+            for (int k = 0; k < 3; ++k) R.cb[3 * a + k] = (float)(axes[a][k] / nn);
+        }
+        float key[12];
+        for (int k = 0; k < 9; ++k) key[k] = R.cb[k];
+        for (int k = 0; k < 3; ++k) key[9 + k] = d->cam_pos[k];
+        if (!frame_cached(c->cam_cache, R.cnodes, c->gen, key, 12) || !d->reuse_accel) {
+            GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.cb, d->cam_pos, R.cnodes, R.cnodes2,
+                                             R.cprims, R.cperm, R.cdepth, st),
+                    "camera BVH build");
+            c->timer.launches += 7;
+        }
     }
     for (int32_t k = 0; k < d->spp_count; ++k) {
         const int32_t s = d->spp_begin + k;

@@ -112,12 +112,55 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
 // the NEE light BVH uses a frame whose third axis is the light direction).
 struct Frame {
     float m[9];
-    int identity;
+    int identity;  // 1: world AABBs; 0: AABBs in the rotated frame m; 2: camera-projective boxes
+    float eye[3];  // camera mode: eye; m rows = r, u, f (any basis; rays use the same floats)
 };
+
+// Camera-projective box of the ellipsoid for rays from the eye: q = x - eye, the ray through
+// (a, b) is {q : q.r = a q.f, q.u = b q.f, q.f >= 0}.  a-range: the two planes q.(r - a f) = 0
+// through the eye tangent to the ellipsoid, roots of (cf^2 - E^2 Mff) a^2 - 2 (cr cf - E^2 Mrf) a
+// + (cr^2 - E^2 Mrr) = 0 (M = (R S)(R S)^T in the basis); the same for b; depth range q.f in
+// cf -+ E sqrt(Mff).  Ellipsoids reaching the eye plane get unbounded a, b.  fp64, padded outward.
+__device__ inline void camera_box(const GPrim& P, float s0, float s1, float s2, float E, const Frame& F, float* b,
+                                  float* center) {
+    const double v[3][3] = {{(double)P.b.x * s0, (double)P.b.y * s0, (double)P.b.z * s0},
+                            {(double)P.c.x * s1, (double)P.c.y * s1, (double)P.c.z * s1},
+                            {(double)P.d.x * s2, (double)P.d.y * s2, (double)P.d.z * s2}};
+    const double c[3] = {(double)P.a.x - F.eye[0], (double)P.a.y - F.eye[1], (double)P.a.z - F.eye[2]};
+    double cm[3], A[3][3];
+    for (int a = 0; a < 3; ++a) {  // a = 0 r, 1 u, 2 f
+        const float* f = F.m + 3 * a;
+        cm[a] = f[0] * c[0] + f[1] * c[1] + f[2] * c[2];
+        for (int k = 0; k < 3; ++k) A[a][k] = f[0] * v[k][0] + f[1] * v[k][1] + f[2] * v[k][2];
+    }
+    auto dotk = [&](int x, int y) { return A[x][0] * A[y][0] + A[x][1] * A[y][1] + A[x][2] * A[y][2]; };
+    const double E2 = (double)E * E, Mff = dotk(2, 2), cf = cm[2];
+    const double hf = sqrt(E2 * Mff);
+    const double padf = 1e-4 * hf + 4e-6 * (1.0 + fabs(cf));
+    b[2] = (float)(cf - hf - padf);
+    b[5] = (float)(cf + hf + padf);
+    center[2] = (float)cf;
+    const double den = cf * cf - E2 * Mff;
+    for (int a = 0; a < 2; ++a) {
+        if (cf - hf > 0.0 && den > 0.0) {
+            const double ca = cm[a], Maa = dotk(a, a), Maf = dotk(a, 2);
+            const double disc = fmax(0.0, cf * cf * Maa - 2.0 * ca * cf * Maf + ca * ca * Mff - E2 * (Mff * Maa - Maf * Maf));
+            const double mid = (ca * cf - E2 * Maf) / den, half = sqrt(E2 * disc) / den;
+            const double pad = 1e-5 * (fabs(mid) + half) + 1e-7;
+            b[a] = (float)(mid - half - pad);
+            b[3 + a] = (float)(mid + half + pad);
+            center[a] = (float)mid;
+        } else {
+            b[a] = -1e30f;
+            b[3 + a] = 1e30f;
+            center[a] = 0.0f;
+        }
+    }
+}
 
 // conservative AABB (in frame F) of the ellipsoid {mu + R S u : |u| <= E}:
 // half-width along axis a = E |a^T (R S)|
-__global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cbounds, Frame F) {
+__global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cbounds, Frame F, float* center) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     GPrim P = prims[i];
@@ -128,6 +171,12 @@ __global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cb
     float s2 = 1.0f / (P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
     float E = sqrtf(P.c.w);
     float cx = P.a.x, cy = P.a.y, cz = P.a.z, hwx, hwy, hwz;
+    float* b = box + 6 * i;
+    if (F.identity == 2) {
+        float cc[3];
+        camera_box(P, s0, s1, s2, E, F, b, cc);
+        cx = cc[0]; cy = cc[1]; cz = cc[2];
+    } else {
     if (F.identity) {
         hwx = E * sqrtf(P.b.x * P.b.x * s0 * s0 + P.c.x * P.c.x * s1 * s1 + P.d.x * P.d.x * s2 * s2);
         hwy = E * sqrtf(P.b.y * P.b.y * s0 * s0 + P.c.y * P.c.y * s1 * s1 + P.d.y * P.d.y * s2 * s2);
@@ -154,9 +203,10 @@ __global__ void k_bounds(const GPrim* prims, int64_t n, float* box, uint32_t* cb
     float padx = 1e-4f * hwx + 4e-6f * (1.0f + fabsf(cx));
     float pady = 1e-4f * hwy + 4e-6f * (1.0f + fabsf(cy));
     float padz = 1e-4f * hwz + 4e-6f * (1.0f + fabsf(cz));
-    float* b = box + 6 * i;
     b[0] = cx - hwx - padx; b[1] = cy - hwy - pady; b[2] = cz - hwz - padz;
     b[3] = cx + hwx + padx; b[4] = cy + hwy + pady; b[5] = cz + hwz + padz;
+    }
+    center[3 * i] = cx; center[3 * i + 1] = cy; center[3 * i + 2] = cz;
     atomicMin(cbounds + 0, f2ord(cx)); atomicMin(cbounds + 1, f2ord(cy)); atomicMin(cbounds + 2, f2ord(cz));
     atomicMax(cbounds + 3, f2ord(cx)); atomicMax(cbounds + 4, f2ord(cy)); atomicMax(cbounds + 5, f2ord(cz));
 }
@@ -172,15 +222,15 @@ __device__ __forceinline__ uint64_t expand3(uint32_t x) {
 }
 
 __global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, const uint32_t* cbounds, uint64_t* keys,
-                       uint32_t* vals, Frame F) {
+                       uint32_t* vals, Frame F, const float* center) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     GPrim P = prims[i];
     float lo[3] = {ord2f(cbounds[0]), ord2f(cbounds[1]), ord2f(cbounds[2])};
     float hi[3] = {ord2f(cbounds[3]), ord2f(cbounds[4]), ord2f(cbounds[5])};
     float c[3] = {P.a.x, P.a.y, P.a.z};
-    if (!F.identity)
-        for (int a = 0; a < 3; ++a) c[a] = F.m[3 * a] * P.a.x + F.m[3 * a + 1] * P.a.y + F.m[3 * a + 2] * P.a.z;
+    if (F.identity != 1)
+        for (int a = 0; a < 3; ++a) c[a] = center[3 * i + a];
     uint32_t q[3];
     for (int k = 0; k < 3; ++k) {
         float ext = hi[k] - lo[k];
@@ -397,6 +447,7 @@ BuildScratch gf_scratch_layout(int64_t n, char* base) {
     auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += (bytes + 255) & ~(size_t)255; return p; };
     int64_t nn = n > 0 ? 2 * n - 1 : 1;
     s.pbox = (float*)take(sizeof(float) * 6 * (n > 0 ? n : 1));
+    s.center = (float*)take(sizeof(float) * 3 * (n > 0 ? n : 1));
     s.cbounds = (uint32_t*)take(sizeof(uint32_t) * 8);
     s.keys_in = (uint64_t*)take(sizeof(uint64_t) * (n > 0 ? n : 1));
     s.keys_out = (uint64_t*)take(sizeof(uint64_t) * (n > 0 ? n : 1));
@@ -430,9 +481,9 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
     if (n == 0) return cudaSuccess;
     uint32_t init[8] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u, 0u, 0u};
     if ((e = cudaMemcpyAsync(S.cbounds, init, sizeof(init), cudaMemcpyHostToDevice, st))) return e;
-    Frame I{{1, 0, 0, 0, 1, 0, 0, 0, 1}, 1};
-    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, I);
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, I);
+    Frame I{{1, 0, 0, 0, 1, 0, 0, 0, 1}, 1, {0, 0, 0}};
+    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, I, S.center);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, I, S.center);
     size_t tb = S.sort_temp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
                                              0, 64, st)))
@@ -468,8 +519,8 @@ static_assert(GF_LIGHT_LEAFMAX >= 1 && GF_LIGHT_LEAFMAX <= kLeafMax, "warp trave
 // Asynchronous build in frame F (host rows): same kernels, no host synchronisation; the node count
 // stays on the device (S.nsize[0]) and the tree depth is written to *depth (device).
 cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S,
-                                  const float* F, void* nodes_v, void* nodes2_v, void* sorted_v, int32_t* perm,
-                                  uint32_t* depth, cudaStream_t st) {
+                                  const float* F, const float* eye, void* nodes_v, void* nodes2_v, void* sorted_v,
+                                  int32_t* perm, uint32_t* depth, cudaStream_t st) {
     const GPrim* prims = (const GPrim*)prims_v;
     GNode* nodes = (GNode*)nodes_v;
     cudaError_t e;
@@ -477,11 +528,12 @@ cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int
     if (n == 0) return cudaSuccess;
     Frame Fr{};
     for (int k = 0; k < 9; ++k) Fr.m[k] = F[k];
-    Fr.identity = 0;
+    Fr.identity = eye ? 2 : 0;
+    for (int k = 0; k < 3; ++k) Fr.eye[k] = eye ? eye[k] : 0.0f;
     if ((e = cudaMemsetAsync(S.cbounds, 0xFF, sizeof(uint32_t) * 3, st))) return e;
     if ((e = cudaMemsetAsync(S.cbounds + 3, 0, sizeof(uint32_t) * 3, st))) return e;
-    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, Fr);
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, Fr);
+    k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, Fr, S.center);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, Fr, S.center);
     size_t tb = S.sort_temp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
                                              0, 64, st)))

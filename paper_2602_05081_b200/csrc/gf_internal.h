@@ -18,6 +18,7 @@ struct LoadArgs {
 
 struct BuildScratch {
     float* pbox;
+    float* center;  // key centre per primitive (frame builds)
     uint32_t* cbounds;
     uint64_t *keys_in, *keys_out;
     uint32_t *vals_in, *vals_out;
@@ -112,6 +113,13 @@ struct RenderDev {
     gfk::GPrim* lprims;
     int32_t* lperm;
     uint32_t* ldepth;
+    // camera BVH for depth-0 packets: projective boxes, basis rows r, u, f (cb) at the eye
+    float cb[9];
+    gfk::GNode* cnodes;
+    gfk::GNode2* cnodes2;
+    gfk::GPrim* cprims;
+    int32_t* cperm;
+    uint32_t* cdepth;
     uint32_t* qB2;   // record-overflow paths after single-pass ffA (per-thread ffB)
     // queues
     uint32_t *qA, *qB, *qNext;
@@ -128,8 +136,8 @@ cudaError_t gf_launch_build(const void* prims, const uint8_t* group, int64_t n, 
                             void* nodes2, void* sorted, int32_t* perm, uint32_t* n_nodes, uint32_t* max_depth,
                             float* root_box, cudaStream_t st);
 cudaError_t gf_launch_build_frame(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S,
-                                  const float* F, void* nodes, void* nodes2, void* sorted, int32_t* perm,
-                                  uint32_t* depth, cudaStream_t st);
+                                  const float* F, const float* eye, void* nodes, void* nodes2, void* sorted,
+                                  int32_t* perm, uint32_t* depth, cudaStream_t st);
 cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
 cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
 size_t gf_render_state_bytes(int64_t n_paths, int64_t n_prims, char* base, RenderDev* R, BuildScratch* light_scratch);

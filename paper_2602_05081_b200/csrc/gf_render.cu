@@ -184,6 +184,9 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #ifndef GF_BATCH
 #define GF_BATCH 0
 #endif
+#ifndef GF_CAM_BVH
+#define GF_CAM_BVH 1  // k_ff_pkt traverses the camera BVH (projective boxes, built per gf_render call)
+#endif
 #ifndef GF_PACKET
 #define GF_PACKET 1  // depth-0 (camera) free flight with packet traversal (k_ff_pkt)
 #endif
@@ -840,6 +843,17 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
             R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
             act = false;
         }
+        // box test: camera BVH (projective boxes: the ray is the point (a, b) = (d.r, d.u) / d.f with depth
+        // q.f = t d.f in [tlo, thi] d.f) or world slabs
+        const float dfw = fmaf(d.x, R.cb[6], fmaf(d.y, R.cb[7], d.z * R.cb[8]));
+        const float pa = fmaf(d.x, R.cb[0], fmaf(d.y, R.cb[1], d.z * R.cb[2])) / dfw;
+        const float pb = fmaf(d.x, R.cb[3], fmaf(d.y, R.cb[4], d.z * R.cb[5])) / dfw;
+        const float qlo = tlo * dfw, qhi = thi * dfw;
+        auto boxhit = [&](float4 lo, float4 hi) {
+            if (GF_CAM_BVH)
+                return lo.x <= pa && pa <= hi.x && lo.y <= pb && pb <= hi.y && hi.z >= qlo && lo.z <= qhi;
+            return slab(r, lo, hi, tlo, thi);
+        };
         // packet traversal: one uniform depth-first walk for the 32 rays; each lane integrates its
         // own chords as they are found (tau_total), so only colliding rays need the records again
         uint32_t ng = 0, nb = 0;
@@ -847,7 +861,7 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
         auto leaf = [&](uint32_t info, bool mine) {
             const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, g = info & 31u;
             for (uint32_t k = 0; k < cnt; ++k) {
-                const GPrim* pp = R.prims + first + k;
+                const GPrim* pp = (GF_CAM_BVH ? R.cprims : R.prims) + first + k;
                 GPrim P;
                 P.a = __ldg(&pp->a);
                 bool pass = false;
@@ -879,23 +893,24 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
         };
         if (__any_sync(FULL, act)) {
             int ns = 0;
-            const float4 lo = __ldg(&R.nodes[0].lo), hi = __ldg(&R.nodes[0].hi);
+            const GNode* nd0 = GF_CAM_BVH ? R.cnodes : R.nodes;
+            const float4 lo = __ldg(&nd0[0].lo), hi = __ldg(&nd0[0].hi);
             const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
             if (COUNT && act) ++wk.nodes;
-            const bool hr = act && (node_mask(sk, info) & mask) && slab(r, lo, hi, tlo, thi);
+            const bool hr = act && (node_mask(sk, info) & mask) && boxhit(lo, hi);
             if (__any_sync(FULL, hr)) {
                 if (sk & kLeafBit) leaf(info, hr);
                 else { stk[0] = 0; ns = 1; }
             }
             while (ns > 0) {
                 const uint32_t i = stk[--ns];
-                const GNode2* q = R.nodes2 + i;
+                const GNode2* q = (GF_CAM_BVH ? R.cnodes2 : R.nodes2) + i;
                 const float4 lo0 = __ldg(&q->lo0), hi0 = __ldg(&q->hi0), lo1 = __ldg(&q->lo1), hi1 = __ldg(&q->hi1);
                 const uint32_t ref0 = __float_as_uint(lo0.w), inf0 = __float_as_uint(hi0.w);
                 const uint32_t ref1 = __float_as_uint(lo1.w), inf1 = __float_as_uint(hi1.w);
                 if (COUNT && act) wk.nodes += 2;
-                const bool h0 = act && (node_mask(ref0, inf0) & mask) && slab(r, lo0, hi0, tlo, thi);
-                const bool h1 = act && (node_mask(ref1, inf1) & mask) && slab(r, lo1, hi1, tlo, thi);
+                const bool h0 = act && (node_mask(ref0, inf0) & mask) && boxhit(lo0, hi0);
+                const bool h1 = act && (node_mask(ref1, inf1) & mask) && boxhit(lo1, hi1);
                 const bool a0 = __any_sync(FULL, h0), a1 = __any_sync(FULL, h1);
                 if (a1) {
                     if (ref1 & kLeafBit) leaf(inf1, h1);
@@ -1356,6 +1371,11 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     GPrim* lprims = (GPrim*)take(sizeof(GPrim) * np1);
     int32_t* lperm = (int32_t*)take(sizeof(int32_t) * np1);
     uint32_t* ldepth = (uint32_t*)take(sizeof(uint32_t) * 4);
+    GNode* cnodes = (GNode*)take(sizeof(GNode) * 2 * np1);  // camera BVH (depth-0 packets)
+    GNode2* cnodes2 = (GNode2*)take(sizeof(GNode2) * 2 * np1);
+    GPrim* cprims = (GPrim*)take(sizeof(GPrim) * np1);
+    int32_t* cperm = (int32_t*)take(sizeof(int32_t) * np1);
+    uint32_t* cdepth = (uint32_t*)take(sizeof(uint32_t) * 4);
     const size_t lsb = gf_scratch_layout(n_prims, nullptr).total_bytes;
     char* lscratch = (char*)take(lsb);
     if (LS) *LS = gf_scratch_layout(n_prims, lscratch);
@@ -1365,6 +1385,7 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
         R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qO = qO; R->qB2 = qB2; R->qO2 = qO2; R->qcount = qc;
         R->lnodes = lnodes; R->lnodes2 = lnodes2; R->lprims = lprims; R->lperm = lperm; R->ldepth = ldepth;
+        R->cnodes = cnodes; R->cnodes2 = cnodes2; R->cprims = cprims; R->cperm = cperm; R->cdepth = cdepth;
     }
     return off;
 }

@@ -60,7 +60,7 @@ class RenderDesc(ctypes.Structure):
                 ("cam_pos", ctypes.c_float * 3), ("cam_fwd", ctypes.c_float * 3), ("cam_right", ctypes.c_float * 3),
                 ("cam_up", ctypes.c_float * 3), ("albedo", ctypes.c_float), ("hg_g", ctypes.c_float),
                 ("sun_dir", ctypes.c_float * 3), ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float),
-                ("seed", ctypes.c_uint64), ("estimator", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("estimator", ctypes.c_int32), ("reuse_accel", ctypes.c_int32)]
 
 
 def header_symbols():
@@ -239,6 +239,7 @@ class GaborField:
         d.sun_E, d.env_L = desc.get("sun_E", 0.0), desc.get("env_L", 0.0)
         d.seed = desc["seed"] & 0xFFFFFFFFFFFFFFFF
         d.estimator = int(desc.get("estimator", 0))
+        d.reuse_accel = int(desc.get("reuse_accel", 0))
         return d
 
     def render(self, desc, spp_begin=0, spp_count=1, shard=(SHARD_NONE, 0, 1), probes=None, accum=None,

@@ -382,6 +382,23 @@ def test_nee_light_bvh_same_hits(gfm, monkeypatch, stoch):
     np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-4, atol=1e-5)
 
 
+def test_reused_view_bvhs(gfm):
+    """gf_render reuse_accel: the light / camera BVHs kept in scratch are reused only for the same
+    scene, light and camera; results equal those of fresh builds, also after a camera change."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    d1 = I.render_desc_cfg2(3, 64, 64)
+    d2 = dict(d1, **I.camera((0.3, 0.2, 3.0), (0, 0.05, 0), (0, 1, 0), 40.0, 64, 64))
+    scratch = f.render_scratch(d1, 1)
+    ref1, _ = f.render(d1, 0, 1)
+    ref2, _ = f.render(d2, 0, 1)
+    a1, _ = f.render(dict(d1, reuse_accel=1), 0, 1, scratch=scratch)
+    b1, _ = f.render(dict(d1, reuse_accel=1), 0, 1, scratch=scratch)
+    a2, _ = f.render(dict(d2, reuse_accel=1), 0, 1, scratch=scratch)
+    for x, y in ((a1, ref1), (b1, ref1), (a2, ref2)):
+        assert torch.equal(x, y)
+
+
 def test_warp_traversal_depth_first_mode(gfm, orc, monkeypatch):
     """The warp traversal pops one node per step above its stack threshold (bounded stack);
     forcing that mode everywhere gives the same hits and transmittance."""
