@@ -506,8 +506,9 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         }
     }
     // camera BVH for the depth-0 packet kernel (static ext mask, analytic): projective boxes at the eye
-    if (d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 && c->ext.level_strategy == 0 &&
-        c->ext.orient_strategy == 0) {
+    R.camb = d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 &&
+             env_int("GF_DEBUG_NO_CAMERA_BVH", 0) == 0;
+    if (R.camb) {
         const float* axes[3] = {d->cam_right, d->cam_up, d->cam_fwd};
         for (int a = 0; a < 3; ++a) {
             const double nn = std::sqrt((double)axes[a][0] * axes[a][0] + (double)axes[a][1] * axes[a][1] +

@@ -113,7 +113,8 @@ struct RenderDev {
     gfk::GPrim* lprims;
     int32_t* lperm;
     uint32_t* ldepth;
-    // camera BVH for depth-0 packets: projective boxes, basis rows r, u, f (cb) at the eye
+    // camera BVH for depth-0 rays: projective boxes, basis rows r, u, f (cb) at the eye
+    int32_t camb;  // camera BVH built for this call
     float cb[9];
     gfk::GNode* cnodes;
     gfk::GNode2* cnodes2;

@@ -695,7 +695,8 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
 //     so no erf is spent on chords that t has passed or not reached.
 // The buffer (rec_cap records per warp) stays L2-resident between the three phases; a path with
 // more records than rec_cap goes to the single-pass fallback (k_ffA + k_ffB).
-template <bool STOCH, bool COUNT>
+// CAM: depth-0 rays from the eye traverse the camera BVH (projective boxes, see k_ff_pkt)
+template <bool STOCH, bool COUNT, bool CAM>
 __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t depth,
                                             const uint32_t* __restrict__ q_in, int cnt_slot, int cur_slot,
                                             uint32_t* __restrict__ q_over, int over_slot) {
@@ -741,13 +742,19 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
         }
         // 1. records
         uint32_t ng = 0, nb = 0;
-        warp_traverse<COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, r, tlo, thi, mask, s_t[wid], wk,
+        const float dfw = fmaf(d.x, R.cb[6], fmaf(d.y, R.cb[7], d.z * R.cb[8]));
+        const float pa = fmaf(d.x, R.cb[0], fmaf(d.y, R.cb[1], d.z * R.cb[2])) / dfw;
+        const float pb = fmaf(d.x, R.cb[3], fmaf(d.y, R.cb[4], d.z * R.cb[5])) / dfw;
+        const float qlo = tlo * dfw, qhi = thi * dfw;
+        const GPrim* __restrict__ prims = CAM ? R.cprims : R.prims;
+        warp_traverse_b<COUNT>(CAM ? R.cnodes : R.nodes, CAM ? R.cnodes2 : R.nodes2, R.n_nodes,
+                               CAM ? max(1, kWStk - 34 - (int)*R.cdepth) : R.stk_limit, mask, s_t[wid], wk,
                              [&](bool valid, uint32_t ref) {
             bool hit = false;
             Setup s;
             float cj = 0.0f;
             if (valid) {
-                const GPrim* pp = R.prims + (ref & kRefIdx);
+                const GPrim* pp = prims + (ref & kRefIdx);
                 GPrim P;
                 P.a = __ldg(&pp->a);
                 if (COUNT) ++wk.tests;
@@ -771,6 +778,9 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
             }
             ng += __popc(mg);
             nb += __popc(mb);
+        }, [&](float4 lo, float4 hi) {
+            if (CAM) return lo.x <= pa && pa <= hi.x && lo.y <= pb && pb <= hi.y && hi.z >= qlo && lo.z <= qhi;
+            return slab(r, lo, hi, tlo, thi);
         });
         if (ng + nb > cap) {  // record overflow: single-pass fallback
             if (lane == 0) q_over[atomicAdd(R.qcount + over_slot, 1u)] = p;
@@ -1341,7 +1351,7 @@ template <bool S, bool C>
 static unsigned ff_grid(int64_t n_paths) {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ff<S, C>, 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ff<S, C, false>, 128, 0);
         occ = std::max(1, std::min(occ, 8));
     }
     const int64_t blocks = (int64_t)(persist_blocks() / 16) * occ;
@@ -1397,15 +1407,20 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
                          bool stoch_nee) {
     cudaEvent_t e;
     // coherent camera rays under one static mask: packet traversal
-    const bool packet = GF_PACKET && d == 0 && !S && R.estimator == 0;
+    const bool packet = GF_PACKET && d == 0 && !S && R.estimator == 0 && R.camb;  // (k_ff_pkt needs the camera BVH)
     T.pre(STAGE_FFA, st, e);
     if (R.estimator == 1) k_ff_trk<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
     else if (packet) k_ff_pkt<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
-    else k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qA, 0, kWorkAT, R.qO, kCntO);
+    else if (d == 0 && R.camb)
+        k_ff<S, C, true><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qA, 0, kWorkAT, R.qO, kCntO);
+    else k_ff<S, C, false><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qA, 0, kWorkAT, R.qO, kCntO);
     T.post(STAGE_FFA, st, e);
     if (packet) {  // rays with more records than a packet lane holds: warp-per-ray k_ff (larger buffer),
         T.pre(STAGE_FFB, st, e);  // timed with the fallbacks (stage "ff_fallback")
-        k_ff<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkRO, R.qO2, kCntO2);
+        if (R.camb)
+            k_ff<S, C, true><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkRO, R.qO2, kCntO2);
+        else
+            k_ff<S, C, false><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkRO, R.qO2, kCntO2);
         T.post(STAGE_FFB, st, e);
     }
     T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")

@@ -356,27 +356,28 @@ def test_column_more_hits_than_record_buffer(gfm, orc, monkeypatch, rec_cap):
     _probe_compare(gfm, orc, sc, desc, probes, 8, "column free flight", frac_tol=0.05)
 
 
+@pytest.mark.parametrize("which", ["LIGHT", "CAMERA"])
 @pytest.mark.parametrize("stoch", [False, True])
-def test_nee_light_bvh_same_hits(gfm, monkeypatch, stoch):
-    """NEE traverses a second BVH whose boxes live in the light's frame (axis-parallel shadow rays).
-    It must find exactly the shadow-ray hits of the world BVH: same hit count, same image."""
+def test_view_bvhs_same_hits(gfm, monkeypatch, stoch, which):
+    """NEE traverses the light BVH (boxes in the light's frame), the camera rays the camera BVH
+    (projective boxes at the eye).  Each must find exactly the hits of the world BVH: same hit
+    counts, same image (static masks: packet kernel; stochastic: warp-per-ray kernels)."""
     sc = I.scene_cfg2()
-    f = field(gfm, sc)
+    f = field(gfm, sc, group_f0=I.group_f0(sc))
     desc = I.render_desc_cfg2(3, 64, 64)
     desc.update(max_depth=3, albedo=0.9, hg_g=0.3)
     if stoch:
         desc.update(ext=I.policy(level_strategy=5, beta=0.2, orient_strategy=3),
                     nee=I.policy(level_strategy=2, beta=0.5, orient_strategy=2))
-        f.load_primitives(sc, group_f0=I.group_f0(sc))
-        f.build_bvh()
+    stage = "nee" if which == "LIGHT" else "ff"
     out = []
     for off in ("0", "1"):
-        monkeypatch.setenv("GF_DEBUG_NO_LIGHT_BVH", off)
+        monkeypatch.setenv(f"GF_DEBUG_NO_{which}_BVH", off)
         f.set_profiling(work=True)
         acc, _ = f.render(desc, 0, 2)
         st = f.stats(reset=True)
         f.set_profiling()
-        out.append((acc.cpu().numpy(), st["work"]["nee"]))
+        out.append((acc.cpu().numpy(), st["work"][stage]))
     assert out[0][1]["hits"] == out[1][1]["hits"] > 0
     assert out[0][1]["paths"] == out[1][1]["paths"]
     np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-4, atol=1e-5)
