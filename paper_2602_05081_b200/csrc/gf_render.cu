@@ -535,17 +535,19 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
     for (int side = 0; side < 2; ++side) {
         for (uint32_t i = lane; i < nside[side]; i += 32) {
             const uint32_t slot = side == 0 ? i : cap - 1 - i;
-            const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
-            float full;
-            if (PRE) {
-                full = aux[slot].x;
+            float full, tm;
+            if (PRE) {  // aux = (t_a, t_b, full, amp G(u0)): the records themselves are not read
+                const float4 x = aux[slot];
+                full = x.z;
+                tm = 0.5f * (x.x + x.y);
             } else {
+                const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
                 const float4 x = chord_aux<COUNT>(a, b, side == 1, wk);
                 aux[slot] = x;
                 full = x.x;
+                tm = b.z + (0.5f * (a.x + a.y) - b.w) / b.y;
             }
             tot += full;
-            const float tm = b.z + (0.5f * (a.x + a.y) - b.w) / b.y;
             atomicAdd(&hist[min(63, max(0, (int)((tm - tlo) * hscale)))], full);
         }
     }
@@ -590,7 +592,33 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
                 const uint32_t i = base + lane;
                 bool push = false;
                 float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                if (i < n) {
+                if (PRE && i < n) {  // aux = (t_a, t_b, full, amp G(u0)); records read only for straddlers
+                    const uint32_t slot = side == 0 ? i : cap - 1 - i;
+                    const float4 x = aux[slot];
+                    if (t >= x.y) {
+                        part += x.z;
+                    } else if (t > x.x) {
+                        const float4 a = rec[2 * slot], b = rec[2 * slot + 1];
+                        const float ut = fminf(fmaxf(fmaf(b.y, t - b.z, b.w), a.x), a.y);
+                        float sp, cp;
+                        sincos_red(fmaf(a.z, ut, a.w), &sp, &cp);
+                        const float kk = b.x * b.y * 0.79788456080286536f * __expf(0.5f * (a.z * a.z - ut * ut));
+                        kap += kk * cp;
+                        dkap -= kk * b.y * fmaf(ut, cp, a.z * sp);
+                        if (x.w != x.w) {  // special record: lane-local partial integral
+                            Setup s;
+                            s.r2 = 0.0f; s.h = INFINITY; s.bp = b.w; s.j = b.y; s.ij = 1.0f / b.y; s.tc = b.z;
+                            s.Om = a.z; s.phi0 = a.w;
+                            part += 2.0f * b.x * __expf(0.5f * a.z * a.z) * seg_J(s, a.x, ut, wk);
+                        } else {
+                            float s0 = 0.0f, c0 = 1.0f;
+                            if (side == 1 || a.w != 0.0f) sincos_red(a.w, &s0, &c0);
+                            part -= x.w;
+                            push = true;
+                            e = make_float4(ut, a.z, b.x * c0, -b.x * s0);
+                        }
+                    }
+                } else if (!PRE && i < n) {
                     const uint32_t slot = side == 0 ? i : cap - 1 - i;
                     const float4 a = rec[2 * slot], b = rec[2 * slot + 1], x = aux[slot];
                     const float ut = fmaf(b.y, t - b.z, b.w);
@@ -889,8 +917,10 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
                     const bool gs = s.Om == 0.0f;
                     const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
                     const float4 ra = make_float4(s.u0, s.u1, s.Om, s.phi0), rb = make_float4(amp, s.j, s.tc, s.bp);
-                    const float4 x = chord_aux<COUNT>(ra, rb, !gs, wk);  // all lanes: same primitive type
-                    tau_tot += (double)x.x;
+                    const float4 xc = chord_aux<COUNT>(ra, rb, !gs, wk);  // all lanes: same primitive type
+                    tau_tot += (double)xc.x;
+                    // resolve layout: chord t-interval, full integral, amp G(u0)
+                    const float4 x = make_float4(fmaf(s.u0 - s.bp, s.ij, s.tc), fmaf(s.u1 - s.bp, s.ij, s.tc), xc.x, xc.y);
                     if (ng + nb < lcap) {
                         const uint32_t slot = gs ? ng : lcap - 1 - nb;
                         myrec[2 * slot] = ra;
