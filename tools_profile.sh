@@ -13,3 +13,11 @@ if [ $rc = 0 ]; then
   timeout 1200 ncu --set full --clock-control none --import-source on -k k_nee_w -s 4 -c 4 -f -o gpurun_out/prof_nee \
     python bench.py --profile-pass --steps 1 --warmup 1 > gpurun_out/ncu3.log 2>&1; echo "ncu nee rc=$?"
 fi
+# export on the box (keeps gpurun_out under the 64 MiB copy-back limit)
+for f in prof_ff prof_nee; do
+  if [ -f gpurun_out/$f.ncu-rep ]; then
+    ncu -i gpurun_out/$f.ncu-rep --page raw --csv > gpurun_out/${f}_raw.csv 2>/dev/null
+    ncu -i gpurun_out/$f.ncu-rep --page source --csv --print-source sass > gpurun_out/${f}_sass.csv 2>/dev/null
+    rm -f gpurun_out/$f.ncu-rep
+  fi
+done
