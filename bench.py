@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--estimator", default="analytic", choices=["analytic", "tracking"],
                     help="scatter estimator: closed-form tau + root (default) or delta/ratio tracking")
+    ap.add_argument("--foveation", action="store_true",
+                    help="foveated rendering variant: gaze at the image centre, all levels in the fovea, "
+                         "threshold falling linearly to 0 at eccentricity 0.7 (jitter 0.2)")
     ap.add_argument("--profile-pass", action="store_true", help="only run warmup+steps (for ncu launch lists)")
     args = ap.parse_args()
     rank, local, world = dist_env()
@@ -203,6 +206,12 @@ def main():
     descs = [dict(d, reuse_accel=1) for d in descs]
     if args.estimator == "tracking":
         descs = [dict(d, estimator=1) for d in descs]
+    if args.foveation:
+        lf = I.level_fmax(sc)
+        f0 = float(lf.max()) * 1.05
+        descs = [dict(d, foveation=I.foveation(sc, (d["width"] / 2, d["height"] / 2), f0, f0 / 0.7, 0.2))
+                 for d in descs]
+        name += " [foveated: gaze centre, threshold 1.05 max level frequency, zero at eccentricity 0.7]"
         name += " [delta/ratio tracking estimator]"
     f = gf.GaborField(local)
     f.load_primitives(sc, group_f0=I.group_f0(sc))

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 3
+#define GF_ABI_VERSION 4
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -207,6 +207,16 @@ typedef struct {
     int32_t estimator;          /* gf_estimator (SCATTER) */
     int32_t reuse_accel;        /* 1: reuse the light / camera BVHs left in scratch by the previous
                                    call (see gf_render); 0: rebuild them */
+    /* Foveated rendering (readings F1-F5): foveation = 1
+     * gives every path of pixel (px, py) the frequency threshold
+     *   f_max = max(0, fov_f0 - fov_slope e) (1 + fov_jitter (2u - 1)),
+     *   e = |(px + 0.5, py + 0.5) - fov_gaze| / max(W, H),  u = uniform of stream 6, k = 0, depth 0;
+     * Gabor levels l with fov_level_fmax[l] > f_max are masked (level 0 never), and a primitive
+     * whose frequency along the ray |omega_vec . d| exceeds f_max is not integrated. */
+    int32_t foveation;
+    float fov_gaze[2];          /* gaze point in pixels */
+    float fov_f0, fov_slope, fov_jitter;
+    float fov_level_fmax[8];    /* maximum world frequency |omega_vec| of each level (index 0 unused) */
 } gf_render_desc;
 
 /* Device scratch needed by gf_render for `desc`. */

@@ -43,7 +43,9 @@ class RenderDesc(ctypes.Structure):
                 ("cam_right", ctypes.c_float * 3), ("cam_up", ctypes.c_float * 3),
                 ("albedo", ctypes.c_float), ("hg_g", ctypes.c_float), ("sun_dir", ctypes.c_float * 3),
                 ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float), ("seed", ctypes.c_uint64),
-                ("ext", Policy), ("nee", Policy), ("group_f0", ctypes.c_void_p)]
+                ("ext", Policy), ("nee", Policy), ("group_f0", ctypes.c_void_p),
+                ("foveation", ctypes.c_int32), ("fov_gaze", ctypes.c_float * 2), ("fov_f0", ctypes.c_float),
+                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8)]
 
 
 def lib():
@@ -234,6 +236,14 @@ def make_render_desc(desc):
     d.seed = desc["seed"] & 0xFFFFFFFFFFFFFFFF
     d.ext = make_policy(**desc.get("ext", {}))
     d.nee = make_policy(**desc.get("nee", desc.get("ext", {})))
+    fov = desc.get("foveation")
+    if fov:
+        d.foveation = 1
+        d.fov_gaze[:] = [float(x) for x in np.asarray(fov["gaze"], np.float32)]
+        d.fov_f0, d.fov_slope = float(np.float32(fov["f0"])), float(np.float32(fov["slope"]))
+        d.fov_jitter = float(np.float32(fov.get("jitter", 0.0)))
+        lf = [float(x) for x in np.asarray(fov["level_fmax"], np.float32)] + [0.0] * 8
+        d.fov_level_fmax[:] = lf[:8]
     f0 = desc.get("group_f0")
     keep = None
     if f0 is not None:

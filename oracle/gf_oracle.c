@@ -286,8 +286,18 @@ static void neum_add(neum *n, double x) {
 static double neum_get(const neum *n) { return n->s + n->c; }
 
 /* tau = sum over visible i of w_g(i) alpha_i int K_i ; also A = sum |.| and per-group tau */
+/* fmax: foveation (reading F4): a primitive whose frequency along the ray |omega_vec . v|
+   exceeds fmax is not integrated (INFINITY: off) */
+static double trace_one_f(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
+                          uint32_t mask, const float *wts, double fmax, double *abs_out, double *grp_out,
+                          int *nhits);
 static double trace_one(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
                         uint32_t mask, const float *wts, double *abs_out, double *grp_out, int *nhits) {
+    return trace_one_f(s, o, v, t0, t1, mask, wts, INFINITY, abs_out, grp_out, nhits);
+}
+static double trace_one_f(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
+                          uint32_t mask, const float *wts, double fmax, double *abs_out, double *grp_out,
+                          int *nhits) {
     neum tau = {0, 0}, A = {0, 0};
     neum grp[OR_MAXG];
     memset(grp, 0, sizeof(grp));
@@ -298,6 +308,7 @@ static double trace_one(const or_scene *s, const double o[3], const double v[3],
         or_pair p;
         pair_setup(s, i, o, v, t0, t1, &p);
         if (!p.hit) continue;
+        if (fabs(p.B) > fmax) continue;  /* foveation: frequency along the ray above the threshold */
         ++nh;
         double w = wts ? (double)wts[g] : 1.0;
         double ti = w * s->alpha[i] * seg_integral(s, i, &p, p.tin, p.tout);
@@ -583,8 +594,14 @@ static double active_sum(const or_scene *s, const or_active *act, const int *on,
 
 /* returns 1 and *t_out on collision, 0 on escape; *tau_total = tau over the
    whole ray if escaped (for diagnostics). */
+static int free_flight_f(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
+                         uint32_t mask, const float *wts, double xi, double fmax, double *t_out);
 int or_free_flight(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
                    uint32_t mask, const float *wts, double xi, double *t_out) {
+    return free_flight_f(s, o, v, t0, t1, mask, wts, xi, INFINITY, t_out);
+}
+static int free_flight_f(const or_scene *s, const double o[3], const double v[3], double t0, double t1,
+                         uint32_t mask, const float *wts, double xi, double fmax, double *t_out) {
     double tstar = -log1p(-xi);  /* tau* = -ln(1 - xi)  (Eq. 5) */
     if (tstar <= 0.0) { *t_out = t0; return 1; }
     int cap = 64, nact = 0;
@@ -595,6 +612,7 @@ int or_free_flight(const or_scene *s, const double o[3], const double v[3], doub
         or_pair p;
         pair_setup(s, i, o, v, t0, t1, &p);
         if (!p.hit) continue;
+        if (fabs(p.B) > fmax) continue;  /* foveation (F4) */
         if (nact == cap) { cap *= 2; act = realloc(act, sizeof(or_active) * cap); }
         act[nact].idx = i; act[nact].p = p; act[nact].w = wts ? wts[g] : 1.0;
         ++nact;
@@ -649,7 +667,41 @@ typedef struct {
     uint64_t seed;
     or_policy ext, nee;
     const float *group_f0;  /* G floats (C12), may be NULL */
+    int32_t foveation;      /* foveated rendering */
+    float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_level_fmax[8];
 } or_render_desc;
+
+/* Foveation threshold of a pixel ("a linear relationship between eccentricity and the
+   frequency threshold", readings F1-F3, F5): e = |(px+0.5, py+0.5) - gaze| / max(W, H),
+   f_max = max(0, f0 - slope e), stochastic smoothing f_max (1 + jitter (2u - 1)) with u of stream 6.
+   fp32, one rounding per operation (the GPU evaluates the same expression bit for bit). */
+#define ST_FOV 6u
+static float fov_fmax(const or_render_desc *d, uint32_t pix, uint32_t smp) {
+    float px = (float)(pix % (uint32_t)d->width), py = (float)(pix / (uint32_t)d->width);
+    volatile float dx = (px + 0.5f) - d->fov_gaze[0], dy = (py + 0.5f) - d->fov_gaze[1];
+    volatile float dd = dx * dx;
+    volatile float ee = dy * dy;
+    float e = sqrtf(dd + ee) / (float)(d->width > d->height ? d->width : d->height);
+    volatile float se = d->fov_slope * e;
+    float fm = d->fov_f0 - se;
+    if (!(fm > 0.0f)) fm = 0.0f;
+    if (d->fov_jitter > 0.0f) {
+        float u = or_uniform(d->seed, pix, smp, 0, ST_FOV, 0);
+        volatile float tu = 2.0f * u;
+        volatile float j = d->fov_jitter * (tu - 1.0f);
+        fm = fm * (1.0f + j);
+    }
+    return fm;
+}
+/* Level masking ("discard all levels that contain Gabor primitives with frequencies above
+   the threshold", reading F3): level l >= 1 kept iff its maximum frequency <= f_max; level 0 kept */
+static uint32_t fov_mask(const or_scene *s, const or_render_desc *d, float fm) {
+    uint32_t m = 1u;
+    for (int l = 1; l < s->P; ++l)
+        if (d->fov_level_fmax[l] <= fm)
+            for (int b = 0; b < s->K; ++b) m |= 1u << (1 + (l - 1) * s->K + b);
+    return m;
+}
 
 /* camera ray in fp32 with explicit fused ops (bit-identical to the GPU) */
 static void camera_ray(const or_render_desc *d, int px, int py, float jx, float jy, float o[3], float v[3]) {
@@ -703,10 +755,14 @@ double or_path(const or_scene *s, const or_render_desc *d, uint32_t pix, uint32_
     int nr = 0;
     uint32_t mask;
     float w[OR_MAXG];
+    /* foveation: one threshold per (pixel, sample) for every ray of the path */
+    const float fmx = d->foveation ? fov_fmax(d, pix, smp) : INFINITY;
+    const uint32_t fovm = d->foveation ? fov_mask(s, d, fmx) : 0xFFFFFFFFu;
     if (d->mode == 0) {  /* tomography: tau-hat of the camera ray */
         eval_pol(s, d, &d->ext, vf, pix, smp, 0, ST_EXT, 1, &mask, w);
+        mask &= fovm;
         double o[3] = {of[0], of[1], of[2]}, v[3] = {vf[0], vf[1], vf[2]};
-        double tau = trace_one(s, o, v, 0.0, INFINITY, mask, w, NULL, NULL, NULL);
+        double tau = trace_one_f(s, o, v, 0.0, INFINITY, mask, w, fmx, NULL, NULL, NULL);
         if (nrays) *nrays = 1;
         return tau;
     }
@@ -716,10 +772,11 @@ double or_path(const or_scene *s, const or_render_desc *d, uint32_t pix, uint32_
     for (int dep = 0; dep < d->max_depth; ++dep) {
         float vfl[3] = {(float)v[0], (float)v[1], (float)v[2]};
         eval_pol(s, d, &d->ext, vfl, pix, smp, dep, ST_EXT, 1, &mask, w);
+        mask &= fovm;
         double xi = or_uniform(d->seed, pix, smp, dep, ST_EXT, 0);
         double tstar;
         ++nr;
-        if (!or_free_flight(s, o, v, 0.0, INFINITY, mask, w, xi, &tstar)) {
+        if (!free_flight_f(s, o, v, 0.0, INFINITY, mask, w, xi, fmx, &tstar)) {
             L += beta * d->env_L;  /* escape -> environment */
             break;
         }
@@ -728,7 +785,8 @@ double or_path(const or_scene *s, const or_render_desc *d, uint32_t pix, uint32_
         uint32_t mn;
         float wn[OR_MAXG];
         eval_pol(s, d, &d->nee, d->sun_dir, pix, smp, dep, ST_NEE, 0, &mn, wn);
-        double tn = trace_one(s, x, sun, 0.0, INFINITY, mn, wn, NULL, NULL, NULL);
+        mn &= fovm;
+        double tn = trace_one_f(s, x, sun, 0.0, INFINITY, mn, wn, fmx, NULL, NULL, NULL);
         ++nr;
         double cost = v[0] * sun[0] + v[1] * sun[1] + v[2] * sun[2];
         L += beta * d->albedo * hg_eval(d->hg_g, cost) * exp(-tn) * d->sun_E;

@@ -420,6 +420,8 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
     if (!(d->hg_g > -1.0f && d->hg_g < 1.0f)) return fail(c, GF_E_INVALID_ARGUMENT, "hg_g must be in (-1,1)");
     if (d->estimator != GF_EST_ANALYTIC && d->estimator != GF_EST_TRACKING)
         return fail(c, GF_E_INVALID_ARGUMENT, "bad estimator");
+    if (d->foveation && !(d->fov_f0 >= 0.0f && d->fov_slope >= 0.0f && d->fov_jitter >= 0.0f && d->fov_jitter < 1.0f))
+        return fail(c, GF_E_INVALID_ARGUMENT, "foveation: f0, slope >= 0 and jitter in [0,1)");
     return GF_OK;
 }
 
@@ -467,6 +469,10 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.max_depth = d->mode == GF_MODE_SCATTER ? d->max_depth : 1;
     R.jitter = d->jitter;
     R.estimator = d->estimator;
+    R.fov = d->foveation != 0;
+    R.fov_gaze[0] = d->fov_gaze[0]; R.fov_gaze[1] = d->fov_gaze[1];
+    R.fov_f0 = d->fov_f0; R.fov_slope = d->fov_slope; R.fov_jitter = d->fov_jitter;
+    for (int k = 0; k < 8; ++k) R.fov_lfmax[k] = d->fov_level_fmax[k];
     R.albedo = d->albedo; R.hg_g = d->hg_g; R.sun_E = d->sun_E; R.env_L = d->env_L;
     R.sun = make_float3(d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]);
     R.seed = d->seed;

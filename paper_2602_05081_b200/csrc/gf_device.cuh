@@ -65,7 +65,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     }
     return c;
 }
-enum { ST_EXT = 0, ST_NEE = 1, ST_SCAT = 2, ST_CAM = 3, ST_TRK = 4, ST_TRK_NEE = 5 };
+enum { ST_EXT = 0, ST_NEE = 1, ST_SCAT = 2, ST_CAM = 3, ST_TRK = 4, ST_TRK_NEE = 5, ST_FOV = 6 };
 // 4 uniforms k0..k0+3 of a stream (k0 multiple of 4) -- one Philox call
 __device__ __forceinline__ uint4 stream_block(uint64_t seed, uint32_t pix, uint32_t smp, uint32_t d, uint32_t st,
                                               uint32_t k0) {
@@ -262,13 +262,14 @@ __host__ __device__ inline int32_t shard_path_pixel(int64_t p, int32_t W, int32_
 struct RayDev {
     float3 o, d, inv, oinv;
     float tmin, tmax;
+    float fmax;  // foveation: primitives with |omega_vec . d| > fmax are skipped (INFINITY: off)
 };
 __device__ __forceinline__ float safe_inv(float x) {
     return 1.0f / (fabsf(x) > 1e-20f ? x : copysignf(1e-20f, x));
 }
-__device__ __forceinline__ RayDev make_ray(float3 o, float3 d, float tmin, float tmax) {
+__device__ __forceinline__ RayDev make_ray(float3 o, float3 d, float tmin, float tmax, float fmax = INFINITY) {
     RayDev r;
-    r.o = o; r.d = d; r.tmin = tmin; r.tmax = tmax;
+    r.o = o; r.d = d; r.tmin = tmin; r.tmax = tmax; r.fmax = fmax;
     r.inv = make_float3(safe_inv(d.x), safe_inv(d.y), safe_inv(d.z));
     r.oinv = make_float3(o.x * r.inv.x, o.y * r.inv.y, o.z * r.inv.z);
     return r;
@@ -341,6 +342,8 @@ __device__ __forceinline__ bool prim_setup(const GPrim& P, const RayDev& r, floa
     float wx = fmaf(P.b.x, r.d.x, fmaf(P.b.y, r.d.y, P.b.z * r.d.z));
     float wy = fmaf(P.c.x, r.d.x, fmaf(P.c.y, r.d.y, P.c.z * r.d.z));
     float wz = fmaf(P.d.x, r.d.x, fmaf(P.d.y, r.d.y, P.d.z * r.d.z));
+    // foveation (continuous masking): frequency along the ray omega_vec . d = omega (W d).(1,1,1)
+    if (fabsf(P.b.w * (wx + wy + wz)) > r.fmax) return false;
     float jj = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
     float ij = rsqrtf(jj);
     float vx = wx * ij, vy = wy * ij, vz = wz * ij;

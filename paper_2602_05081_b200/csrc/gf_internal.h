@@ -81,6 +81,8 @@ struct RenderDev {
     gfk::CamDev cam;
     float4 root_lo, root_hi;
     int32_t mode, max_depth, jitter, estimator;
+    int32_t fov;  // foveated rendering (gf_render_desc.foveation)
+    float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_lfmax[8];
     float albedo, hg_g, sun_E, env_L;
     float3 sun;
     uint64_t seed;

@@ -97,6 +97,36 @@ __device__ __forceinline__ float3 ld3(const float* x, const float* y, const floa
     return make_float3(x[p], y[p], z[p]);
 }
 
+// Foveated rendering (readings F1-F5 in DESIGN.md §3): per pixel a
+// frequency threshold linear in the eccentricity, f_max = max(0, f_fovea - slope e), e = |pixel centre -
+// gaze| / max(W, H), jittered by (1 + sigma (2u - 1)) (u: stream 6, k = 0, per pixel and sample);
+// levels whose maximum frequency exceeds f_max are masked for every ray of the path, and a remaining
+// primitive is skipped when its frequency along the ray |omega_vec . d| exceeds f_max (prim_setup).
+// Correctly rounded fp32 ops: the oracle computes the same f_max bit for bit.
+template <bool FOV>
+__device__ __forceinline__ float fov_fmax(const RenderDev& R, uint32_t pix, uint32_t sample) {
+    if (!FOV || !R.fov) return INFINITY;
+    const float px = (float)(pix % (uint32_t)R.cam.W), py = (float)(pix / (uint32_t)R.cam.W);
+    const float dx = __fsub_rn(__fadd_rn(px, 0.5f), R.fov_gaze[0]), dy = __fsub_rn(__fadd_rn(py, 0.5f), R.fov_gaze[1]);
+    const float e = __fdiv_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy))),
+                              (float)max(R.cam.W, R.cam.H));
+    float fm = fmaxf(0.0f, __fsub_rn(R.fov_f0, __fmul_rn(R.fov_slope, e)));
+    if (R.fov_jitter > 0.0f) {
+        const float u = stream_u(R.seed, pix, sample, 0, ST_FOV, 0);
+        fm = __fmul_rn(fm, __fadd_rn(1.0f, __fmul_rn(R.fov_jitter, __fsub_rn(__fmul_rn(2.0f, u), 1.0f))));
+    }
+    return fm;
+}
+template <bool FOV>
+__device__ __forceinline__ uint32_t fov_mask(const RenderDev& R, float fm) {
+    if (!FOV || !R.fov) return 0xFFFFFFFFu;
+    uint32_t m = 1u;  // level 0 (Gaussians, frequency 0) always
+    for (int l = 1; l < R.sc.P; ++l)
+        if (R.fov_lfmax[l] <= fm)
+            for (int b = 0; b < R.sc.K; ++b) m |= 1u << (1 + (l - 1) * R.sc.K + b);
+    return m;
+}
+
 // tau of a ray through the masked, weighted field (NEE, tomography, ffB overflow)
 template <bool STOCH, bool COUNT>
 __device__ __forceinline__ double trace_tau(const RenderDev& R, const RayDev& r, float t0, float t1, uint32_t mask,
@@ -241,13 +271,14 @@ __global__ void __launch_bounds__(128, GF_MINB_FFA) k_ffA(RenderDev R, int32_t s
             if (COUNT) ++wk.paths;
             const uint32_t pix = R.pix[p];
             const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
-            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+            const float fmx = fov_fmax<true>(R, (uint32_t)pix, (uint32_t)sample);
+            const uint32_t mask = fov_mask<true>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                      ST_EXT, 1, w)
-                                        : R.ext.static_mask;
+                                        : R.ext.static_mask);
             const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
             tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
             if (tstar <= 0.0) { finish(-1, 0.0, 0.0, 0); return false; }
-            const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+            const RayDev r = make_ray(o, d, 0.0f, INFINITY, fmx);
             float thi;
             if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
                 finish(-2, 0.0, 0.0, 0);
@@ -353,10 +384,11 @@ __global__ void __launch_bounds__(128) k_ffB(RenderDev R, int32_t sample, int32_
             const int32_t bin = binw & 0xFFFF;
             const uint32_t pix = R.pix[p];
             float w[kMaxGroups];
-            const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+            const float fmx = fov_fmax<true>(R, (uint32_t)pix, (uint32_t)sample);
+            const uint32_t mask = fov_mask<true>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                      ST_EXT, 1, w)
-                                        : R.ext.static_mask;
-            const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+                                        : R.ext.static_mask);
+            const RayDev r = make_ray(o, d, 0.0f, INFINITY, fmx);
             float tlo, thi;
             slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi);
             const float bw = (thi - tlo) * (1.0f / kBins);
@@ -724,7 +756,7 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
 // The buffer (rec_cap records per warp) stays L2-resident between the three phases; a path with
 // more records than rec_cap goes to the single-pass fallback (k_ffA + k_ffB).
 // CAM: depth-0 rays from the eye traverse the camera BVH (projective boxes, see k_ff_pkt)
-template <bool STOCH, bool COUNT, bool CAM>
+template <bool STOCH, bool COUNT, bool CAM, bool FOV>
 __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t depth,
                                             const uint32_t* __restrict__ q_in, int cnt_slot, int cur_slot,
                                             uint32_t* __restrict__ q_over, int over_slot) {
@@ -753,16 +785,17 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
         const uint32_t pix = R.pix[p];
         const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
         float w[kMaxGroups];
-        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+        const float fmx = fov_fmax<FOV>(R, (uint32_t)pix, (uint32_t)sample);
+        const uint32_t mask = fov_mask<FOV>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                  ST_EXT, 1, w)
-                                    : R.ext.static_mask;
+                                    : R.ext.static_mask);
         const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
         const double tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
         if (tstar <= 0.0) {  // collision at the origin
             if (lane == 0) R.qB[atomicAdd(R.qcount + 1, 1u)] = p;
             continue;
         }
-        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY, fmx);
         float tlo, thi;
         if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
             if (lane == 0) R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
@@ -831,8 +864,8 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
 // writes its ray's hit records into its own region of the warp's buffer; then the warp resolves
 // the rays one after another with ff_resolve (chord integrals, escape test, root).
 constexpr int kPStk = 512;
-template <bool STOCH, bool COUNT>
-__global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int32_t depth) {
+template <bool STOCH, bool COUNT, bool FOV>
+__global__ void __launch_bounds__(128, 7) k_ff_pkt(RenderDev R, int32_t sample, int32_t depth) {
     __shared__ uint32_t s_stk[4][kPStk];
     __shared__ WarpEnd s_e[4];
     __shared__ float s_h[4][64];
@@ -857,6 +890,7 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
         const uint32_t p = valid ? R.qA[idx] : 0u;
         bool act = valid;
         uint32_t pix = 0, mask = 0;
+        float fmx = INFINITY;
         float3 o = make_float3(0.0f, 0.0f, 0.0f), d = make_float3(0.0f, 0.0f, 1.0f);
         double tstar = 0.0;
         float w[kMaxGroups];
@@ -866,8 +900,10 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
             pix = R.pix[p];
             o = ld3(R.ox, R.oy, R.oz, p);
             d = ld3(R.dx, R.dy, R.dz, p);
-            mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 1, w)
-                         : R.ext.static_mask;
+            fmx = fov_fmax<FOV>(R, pix, (uint32_t)sample);
+            mask = fov_mask<FOV>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+                                                          ST_EXT, 1, w)
+                                             : R.ext.static_mask);
             const float xi = stream_u(R.seed, pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
             tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
             if (tstar <= 0.0) {  // collision at the origin
@@ -875,7 +911,7 @@ __global__ void __launch_bounds__(128) k_ff_pkt(RenderDev R, int32_t sample, int
                 act = false;
             }
         }
-        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY, fmx);
         float tlo = 0.0f, thi = 0.0f;
         if (act && (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi))) {
             R.L[p] += R.beta[p] * R.env_L;  // escape -> environment
@@ -1138,10 +1174,11 @@ __global__ void __launch_bounds__(128) k_ff_trk(RenderDev R, int32_t sample, int
         const uint32_t pix = R.pix[p];
         const float3 o = ld3(R.ox, R.oy, R.oz, p), d = ld3(R.dx, R.dy, R.dz, p);
         float w[kMaxGroups];
-        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+        const float fmx = fov_fmax<true>(R, (uint32_t)pix, (uint32_t)sample);
+        const uint32_t mask = fov_mask<true>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                  ST_EXT, 1, w)
-                                    : R.ext.static_mask;
-        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+                                    : R.ext.static_mask);
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY, fmx);
         float tlo, thi;
         if (R.n_nodes == 0 || !slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
             if (lane == 0) R.L[p] += R.beta[p] * R.env_L;
@@ -1202,10 +1239,11 @@ __global__ void __launch_bounds__(128) k_nee_rt(RenderDev R, int32_t sample, int
         ++nray;
         const float3 x = ld3(R.ox, R.oy, R.oz, p);
         float w[kMaxGroups];
-        const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+        const float fmx = fov_fmax<true>(R, (uint32_t)pix, (uint32_t)sample);
+        const uint32_t mask = fov_mask<true>(R, fmx) & (STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                  ST_NEE, 0, w)
-                                    : R.nee.static_mask;
-        const RayDev r = make_ray(x, R.sun, 0.0f, INFINITY);
+                                    : R.nee.static_mask);
+        const RayDev r = make_ray(x, R.sun, 0.0f, INFINITY, fmx);
         float T = 1.0f, tlo, thi;
         if (R.n_nodes > 0 && slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi)) {
             uint32_t ng, nb;
@@ -1248,7 +1286,7 @@ __global__ void __launch_bounds__(128) k_nee_rt(RenderDev R, int32_t sample, int
 // LIGHT: traverse the light BVH (boxes in a frame whose third axis is the light direction, built
 // per gf_render call by gf_launch_build_frame): the shadow ray is axis-parallel there, so a box test
 // is two interval tests and one compare, and the boxes are tight across the rays' direction.
-template <bool STOCH, bool COUNT, bool LIGHT>
+template <bool STOCH, bool COUNT, bool LIGHT, bool FOV>
 __global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int32_t depth) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];
@@ -1268,23 +1306,24 @@ __global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int3
         ++nray;
         const float3 x = ld3(R.ox, R.oy, R.oz, p);
         float w[kMaxGroups];
-        const uint32_t mask = STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
+        const float fmx = fov_fmax<FOV>(R, (uint32_t)pix, (uint32_t)sample);
+        const uint32_t mask = fov_mask<FOV>(R, fmx) & (STOCH ? policy_for(R.nee, R.sc, R.sun, R.seed, pix, (uint32_t)sample, (uint32_t)depth,
                                                  ST_NEE, 0, w)
-                                    : R.nee.static_mask;
+                                    : R.nee.static_mask);
         double tau;
         if (LIGHT) {
             const float3 xp = make_float3(fmaf(R.lf[0], x.x, fmaf(R.lf[1], x.y, R.lf[2] * x.z)),
                                           fmaf(R.lf[3], x.x, fmaf(R.lf[4], x.y, R.lf[5] * x.z)),
                                           fmaf(R.lf[6], x.x, fmaf(R.lf[7], x.y, R.lf[8] * x.z)));
             tau = warp_tau_b<STOCH, COUNT>(R.lnodes, R.lnodes2, R.n_nodes, lstk, R.lprims,
-                                           make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask, w, s_t[wid],
+                                           make_ray(x, R.sun, 0.0f, INFINITY, fmx), 0.0f, INFINITY, mask, w, s_t[wid],
                                            s_e[wid], wk, [&](float4 lo, float4 hi) {
                                                return lo.x <= xp.x && xp.x <= hi.x && lo.y <= xp.y && xp.y <= hi.y &&
                                                       hi.z >= xp.z;
                                            });
         } else {
             tau = warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims,
-                                         make_ray(x, R.sun, 0.0f, INFINITY), 0.0f, INFINITY, mask, w, s_t[wid],
+                                         make_ray(x, R.sun, 0.0f, INFINITY, fmx), 0.0f, INFINITY, mask, w, s_t[wid],
                                          s_e[wid], wk);
         }
         if (lane == 0) {
@@ -1306,7 +1345,7 @@ __global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int3
 }
 
 // tomography (mode 0), one warp per pixel: L = tau of the camera ray
-template <bool STOCH, bool COUNT>
+template <bool STOCH, bool COUNT, bool FOV>
 __global__ void __launch_bounds__(128) k_tomo_w(RenderDev R, int32_t sample) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];
@@ -1324,12 +1363,13 @@ __global__ void __launch_bounds__(128) k_tomo_w(RenderDev R, int32_t sample) {
         float3 o, d;
         camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
         float w[kMaxGroups];
-        const uint32_t mask = STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_EXT, 1, w)
-                                    : R.ext.static_mask;
+        const float fmx = fov_fmax<FOV>(R, (uint32_t)pix, (uint32_t)sample);
+        const uint32_t mask = fov_mask<FOV>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_EXT, 1, w)
+                                    : R.ext.static_mask);
         if (COUNT && lane == 0) ++wk.paths;
         ++nray;
         const double tau = warp_tau<STOCH, COUNT>(R.nodes, R.nodes2, R.n_nodes, R.stk_limit, R.prims,
-                                                  make_ray(o, d, 0.0f, INFINITY), 0.0f, INFINITY, mask, w, s_t[wid],
+                                                  make_ray(o, d, 0.0f, INFINITY, fmx), 0.0f, INFINITY, mask, w, s_t[wid],
                                                   s_e[wid], wk);
         if (lane == 0) R.L[p] = (float)tau;
     }
@@ -1381,7 +1421,7 @@ template <bool S, bool C>
 static unsigned ff_grid(int64_t n_paths) {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ff<S, C, false>, 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ff<S, C, false, false>, 128, 0);
         occ = std::max(1, std::min(occ, 8));
     }
     const int64_t blocks = (int64_t)(persist_blocks() / 16) * occ;
@@ -1432,6 +1472,19 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
 
 
 template <bool S, bool C>
+static void launch_ff(RenderDev& R, int32_t sample, int d, bool cam, const uint32_t* q_in, int cnt_slot, int cur_slot,
+                      uint32_t* q_over, int over_slot, cudaStream_t st) {
+    const unsigned g = ff_grid<S, C>(R.n_paths);
+    if (R.fov) {
+        if (cam) k_ff<S, C, true, true><<<g, 128, 0, st>>>(R, sample, d, q_in, cnt_slot, cur_slot, q_over, over_slot);
+        else k_ff<S, C, false, true><<<g, 128, 0, st>>>(R, sample, d, q_in, cnt_slot, cur_slot, q_over, over_slot);
+    } else {
+        if (cam) k_ff<S, C, true, false><<<g, 128, 0, st>>>(R, sample, d, q_in, cnt_slot, cur_slot, q_over, over_slot);
+        else k_ff<S, C, false, false><<<g, 128, 0, st>>>(R, sample, d, q_in, cnt_slot, cur_slot, q_over, over_slot);
+    }
+}
+
+template <bool S, bool C>
 static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, unsigned wgrid, cudaStream_t st,
                          StageTimer& T,
                          bool stoch_nee) {
@@ -1440,17 +1493,16 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
     const bool packet = GF_PACKET && d == 0 && !S && R.estimator == 0 && R.camb;  // (k_ff_pkt needs the camera BVH)
     T.pre(STAGE_FFA, st, e);
     if (R.estimator == 1) k_ff_trk<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
-    else if (packet) k_ff_pkt<S, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
-    else if (d == 0 && R.camb)
-        k_ff<S, C, true><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qA, 0, kWorkAT, R.qO, kCntO);
-    else k_ff<S, C, false><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qA, 0, kWorkAT, R.qO, kCntO);
+    else if (packet) {
+        if (R.fov) k_ff_pkt<S, C, true><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+        else k_ff_pkt<S, C, false><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
+    } else {
+        launch_ff<S, C>(R, sample, d, d == 0 && R.camb, R.qA, 0, kWorkAT, R.qO, kCntO, st);
+    }
     T.post(STAGE_FFA, st, e);
     if (packet) {  // rays with more records than a packet lane holds: warp-per-ray k_ff (larger buffer),
         T.pre(STAGE_FFB, st, e);  // timed with the fallbacks (stage "ff_fallback")
-        if (R.camb)
-            k_ff<S, C, true><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkRO, R.qO2, kCntO2);
-        else
-            k_ff<S, C, false><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d, R.qO, kCntO, kWorkRO, R.qO2, kCntO2);
+        launch_ff<S, C>(R, sample, d, R.camb, R.qO, kCntO, kWorkRO, R.qO2, kCntO2, st);
         T.post(STAGE_FFB, st, e);
     }
     T.pre(STAGE_FFB, st, e);  // record-overflow paths: single-pass kernels (stage "ffB")
@@ -1464,12 +1516,16 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, unsigned pgrid, un
     if (R.estimator == 1) {  // ratio tracking uses the k_ff record buffers (same grid)
         if (stoch_nee) k_nee_rt<true, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
         else k_nee_rt<false, C><<<ff_grid<S, C>(R.n_paths), 128, 0, st>>>(R, sample, d);
-    } else if (R.light) {
-        if (stoch_nee) k_nee_w<true, C, true><<<wgrid, 128, 0, st>>>(R, sample, d);
-        else k_nee_w<false, C, true><<<wgrid, 128, 0, st>>>(R, sample, d);
     } else {
-        if (stoch_nee) k_nee_w<true, C, false><<<wgrid, 128, 0, st>>>(R, sample, d);
-        else k_nee_w<false, C, false><<<wgrid, 128, 0, st>>>(R, sample, d);
+#define GF_NEE(SN, L, F) k_nee_w<SN, C, L, F><<<wgrid, 128, 0, st>>>(R, sample, d)
+        if (R.fov) {
+            if (R.light) { if (stoch_nee) GF_NEE(true, true, true); else GF_NEE(false, true, true); }
+            else { if (stoch_nee) GF_NEE(true, false, true); else GF_NEE(false, false, true); }
+        } else {
+            if (R.light) { if (stoch_nee) GF_NEE(true, true, false); else GF_NEE(false, true, false); }
+            else { if (stoch_nee) GF_NEE(true, false, false); else GF_NEE(false, false, false); }
+        }
+#undef GF_NEE
     }
     T.post(STAGE_NEE, st, e);
 }
@@ -1487,13 +1543,15 @@ cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cu
     cudaEvent_t ev;
     if (R.mode == 0) {
         T.pre(STAGE_TOMO, st, ev);
-        if (stoch_ext) {
-            if (cnt) k_tomo_w<true, true><<<wgrid, 128, 0, st>>>(R, sample);
-            else k_tomo_w<true, false><<<wgrid, 128, 0, st>>>(R, sample);
+#define GF_TOMO(S_, C_, F_) k_tomo_w<S_, C_, F_><<<wgrid, 128, 0, st>>>(R, sample)
+        if (R.fov) {
+            if (stoch_ext) { if (cnt) GF_TOMO(true, true, true); else GF_TOMO(true, false, true); }
+            else { if (cnt) GF_TOMO(false, true, true); else GF_TOMO(false, false, true); }
         } else {
-            if (cnt) k_tomo_w<false, true><<<wgrid, 128, 0, st>>>(R, sample);
-            else k_tomo_w<false, false><<<wgrid, 128, 0, st>>>(R, sample);
+            if (stoch_ext) { if (cnt) GF_TOMO(true, true, false); else GF_TOMO(true, false, false); }
+            else { if (cnt) GF_TOMO(false, true, false); else GF_TOMO(false, false, false); }
         }
+#undef GF_TOMO
         T.post(STAGE_TOMO, st, ev);
     } else {
         T.pre(STAGE_GEN, st, ev);

@@ -60,7 +60,9 @@ class RenderDesc(ctypes.Structure):
                 ("cam_pos", ctypes.c_float * 3), ("cam_fwd", ctypes.c_float * 3), ("cam_right", ctypes.c_float * 3),
                 ("cam_up", ctypes.c_float * 3), ("albedo", ctypes.c_float), ("hg_g", ctypes.c_float),
                 ("sun_dir", ctypes.c_float * 3), ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float),
-                ("seed", ctypes.c_uint64), ("estimator", ctypes.c_int32), ("reuse_accel", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("estimator", ctypes.c_int32), ("reuse_accel", ctypes.c_int32),
+                ("foveation", ctypes.c_int32), ("fov_gaze", ctypes.c_float * 2), ("fov_f0", ctypes.c_float),
+                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8)]
 
 
 def header_symbols():
@@ -240,6 +242,13 @@ class GaborField:
         d.seed = desc["seed"] & 0xFFFFFFFFFFFFFFFF
         d.estimator = int(desc.get("estimator", 0))
         d.reuse_accel = int(desc.get("reuse_accel", 0))
+        fov = desc.get("foveation")
+        if fov:
+            d.foveation = 1
+            d.fov_gaze[:] = [float(x) for x in fov["gaze"]]
+            d.fov_f0, d.fov_slope, d.fov_jitter = float(fov["f0"]), float(fov["slope"]), float(fov.get("jitter", 0.0))
+            lf = list(np.asarray(fov["level_fmax"], np.float32)) + [0.0] * 8
+            d.fov_level_fmax[:] = [float(x) for x in lf[:8]]
         return d
 
     def render(self, desc, spp_begin=0, spp_count=1, shard=(SHARD_NONE, 0, 1), probes=None, accum=None,

@@ -291,6 +291,26 @@ def scene_column(seed=SCENE_SEED + 9, n=1500, density=0.02):
     return _finish(mu, random_quats(rng, n), scale, peak, omega, level, name="column")
 
 
+def level_fmax(scene):
+    """Maximum world frequency |omega_vec| = omega |S^-1 (1,1,1)| of each pyramid level
+    (index 0: Gaussians, 0): the per-level bound the foveation policy compares with f_max."""
+    P = scene["P"]
+    s = scene["scale"].astype(np.float64)
+    f = scene["omega"].astype(np.float64) * np.linalg.norm(1.0 / s, axis=1)
+    out = np.zeros(8, np.float32)
+    for l in range(1, P):
+        sel = scene["level"] == l
+        if sel.any():
+            out[l] = np.float32(f[sel].max())
+    return out
+
+
+def foveation(scene, gaze, f0, slope, jitter=0.0):
+    """Foveated-rendering parameters (gf_render_desc foveation fields) for `scene`."""
+    return {"gaze": [float(gaze[0]), float(gaze[1])], "f0": float(f0), "slope": float(slope),
+            "jitter": float(jitter), "level_fmax": level_fmax(scene)}
+
+
 def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
     """32-bit group mask selecting whole pyramid levels: level 0 -> bit 0, Gabor level l ->
     bits 1+(l-1)K .. (l)K (the group numbering g(l,b) of DESIGN.md §5; paper V_l = 2^l)."""

@@ -415,6 +415,24 @@ def test_warp_traversal_depth_first_mode(gfm, orc, monkeypatch):
     assert np.array_equal(c1.cpu().numpy()[:, 2], r["nhits"])
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_render_foveation_probes(gfm, orc, mode):
+    """Foveated rendering: per-pixel frequency threshold linear in
+    the eccentricity with stochastic smoothing, level masking and the per-primitive check along the
+    ray; identical Philox streams.  Tomography and multiple scattering vs the oracle."""
+    sc = I.scene_cfg1p() if mode else I.scene_cfg1()
+    lf = I.level_fmax(sc)
+    fov = I.foveation(sc, (10.0, 20.0), float(lf[1:4].max()) * 1.05, float(lf[1:4].max()) * 1.6, 0.3)
+    if mode == 0:
+        desc = dict(I.render_desc_cfg1(32, 32), jitter=1, foveation=fov)
+    else:
+        desc = I.render_desc_cfg2(3, 32, 32)
+        desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 32, 32))
+        desc.update(max_depth=3, albedo=0.9, hg_g=0.3, ext=I.policy(), nee=I.policy(), foveation=fov)
+    probes = np.random.default_rng(8).integers(0, 32 * 32, 40)
+    _probe_compare(gfm, orc, sc, desc, probes, 8, f"foveation mode {mode}", frac_tol=0.03)
+
+
 def test_cfg2_bench_configuration_sampled(gfm, orc):
     """Config 2 at full size in the launch configuration bench.py times (1024^2, 1 spp per LOD
     mask, single scattering): sampled pixels of the full-image render vs the oracle's paths."""

@@ -571,3 +571,54 @@ def test_albedo_zero_and_white_furnace(orc):
     vals, nr = S.render_probes(d, [27, 28, 36], 0, 300)
     assert abs(vals.mean() - 1.0) < 0.02
     assert set(np.unique(vals)) <= {0.0, 1.0}
+
+
+# ---------------------------------------------------------------- foveation
+def test_foveation_limits_reduce_to_plain_renders(orc):
+    """P:L624-L634, readings F1-F5: a threshold above every frequency changes nothing; a threshold of
+    0 keeps exactly level 0 (the Gaussians, frequency 0): both reduce to renders without foveation
+    (static masks all / {0}), sample for sample, for tomography and single scattering."""
+    sc = I.scene_cfg1()
+    S = orc.Scene(sc)
+    pix = list(range(0, 64, 3))
+    for mode in (0, 1):
+        base = _tiny_desc(mode, jitter=1)
+        plain = S.render_probes(base, pix, 0, 6)[0]
+        lvl0 = S.render_probes(dict(base, ext=I.policy(static_mask=1), nee=I.policy(static_mask=1)), pix, 0, 6)[0]
+        hi = S.render_probes(dict(base, foveation=I.foveation(sc, (4, 4), 1e30, 0.0, 0.3)), pix, 0, 6)[0]
+        zero = S.render_probes(dict(base, foveation=I.foveation(sc, (4, 4), 0.0, 0.0, 0.3)), pix, 0, 6)[0]
+        assert np.array_equal(hi, plain)
+        assert np.array_equal(zero, lvl0)
+        assert not np.array_equal(plain, lvl0)
+
+
+def test_foveation_primitive_check_follows_definition(orc):
+    """F4: a primitive is integrated iff its frequency along the ray |omega_vec . d| does not
+    exceed f_max, omega_vec = R S^-1 (omega, omega, omega) computed here independently in
+    numpy from the primitive's quaternion and scales; thresholds 1 % either side of it."""
+    rng = np.random.default_rng(12)
+    n = 1
+    mu = np.zeros((1, 3))
+    quat = I.random_quats(rng, 1)
+    scale = np.array([[0.3, 0.2, 0.25]])
+    sc = I._finish(mu, quat, scale, np.array([1.0]), np.array([1.2]), np.array([1], np.uint8), name="one")
+    S = orc.Scene(sc)
+    d = _tiny_desc(0)
+    x, y, z, w = (float(v) for v in sc["quat"][0])
+    nq = math.sqrt(x * x + y * y + z * z + w * w)
+    x, y, z, w = x / nq, y / nq, z / nq, w / nq
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                  [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                  [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+    wvec = R @ (float(sc["omega"][0]) / sc["scale"][0].astype(np.float64))
+    pix = [27, 28, 35, 36]
+    _, dirs = I.camera_rays_f64(d, np.array(pix) % 8, np.array(pix) // 8)
+    full = S.render_probes(d, pix, 0, 1)[0][:, 0]
+    assert np.all(np.abs(full) > 1e-6)
+    for k, p in enumerate(pix):
+        f = abs(float(dirs[k] @ wvec))
+        lf = I.level_fmax(sc) * 0  # level masking off: every level bound 0 <= f_max
+        above = dict(d, foveation={"gaze": [0, 0], "f0": f * 1.01, "slope": 0.0, "level_fmax": lf})
+        below = dict(d, foveation={"gaze": [0, 0], "f0": f * 0.99, "slope": 0.0, "level_fmax": lf})
+        assert S.render_probes(above, [p], 0, 1)[0][0, 0] == full[k]
+        assert S.render_probes(below, [p], 0, 1)[0][0, 0] == 0.0
