@@ -187,6 +187,9 @@ def main():
     ap.add_argument("--foveation", action="store_true",
                     help="foveated rendering variant: gaze at the image centre, all levels in the fovea, "
                          "threshold falling linearly to 0 at eccentricity 0.7 (jitter 0.2)")
+    ap.add_argument("--motion-blur", choices=["reference", "culled"], default=None,
+                    help="motion-blur variant (direction (1, 0.2, 0), magnitude 0.02): time-sampled reference, "
+                         "or the group-culled approximation (attenuation threshold 0.6)")
     ap.add_argument("--profile-pass", action="store_true", help="only run warmup+steps (for ncu launch lists)")
     args = ap.parse_args()
     rank, local, world = dist_env()
@@ -206,6 +209,15 @@ def main():
     descs = [dict(d, reuse_accel=1) for d in descs]
     if args.estimator == "tracking":
         descs = [dict(d, estimator=1) for d in descs]
+    if args.motion_blur:
+        mdir, mm = (1.0, 0.2, 0.0), 0.02
+        if args.motion_blur == "reference":
+            descs = [dict(d, motion_blur=I.motion_blur(mdir, mm)) for d in descs]
+        else:
+            mask, _ = I.motion_blur_mask(sc, mdir, mm, 0.6)
+            descs = [dict(d, ext=I.policy(static_mask=d["ext"]["static_mask"] & mask),
+                          nee=I.policy(static_mask=d["nee"]["static_mask"] & mask)) for d in descs]
+        name += f" [motion blur {args.motion_blur}: direction (1, 0.2, 0), magnitude 0.02]"
     if args.foveation:
         lf = I.level_fmax(sc)
         f0 = float(lf.max()) * 1.05

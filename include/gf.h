@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 4
+#define GF_ABI_VERSION 5
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -217,6 +217,14 @@ typedef struct {
     float fov_gaze[2];          /* gaze point in pixels */
     float fov_f0, fov_slope, fov_jitter;
     float fov_level_fmax[8];    /* maximum world frequency |omega_vec| of each level (index 0 unused) */
+    /* Motion-blur reference (readings M1-M3):
+     * motion_blur = 1 renders the field moving along mb_dir by mb_m during the exposure, a box
+     * filter of length mb_m: each (pixel, sample) draws u (stream 7, k = 0, depth 0) and the field
+     * is shifted by s = mb_m (u - 1/2) mb_dir, i.e. the camera by -s.  (The accelerated version
+     * culls orientation/frequency groups with inputs.motion_blur_mask -> a static mask.) */
+    int32_t motion_blur;
+    float mb_dir[3];
+    float mb_m;
 } gf_render_desc;
 
 /* Device scratch needed by gf_render for `desc`. */

@@ -45,7 +45,8 @@ class RenderDesc(ctypes.Structure):
                 ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("ext", Policy), ("nee", Policy), ("group_f0", ctypes.c_void_p),
                 ("foveation", ctypes.c_int32), ("fov_gaze", ctypes.c_float * 2), ("fov_f0", ctypes.c_float),
-                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8)]
+                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8),
+                ("motion_blur", ctypes.c_int32), ("mb_dir", ctypes.c_float * 3), ("mb_m", ctypes.c_float)]
 
 
 def lib():
@@ -244,6 +245,11 @@ def make_render_desc(desc):
         d.fov_jitter = float(np.float32(fov.get("jitter", 0.0)))
         lf = [float(x) for x in np.asarray(fov["level_fmax"], np.float32)] + [0.0] * 8
         d.fov_level_fmax[:] = lf[:8]
+    mb = desc.get("motion_blur")
+    if mb:
+        d.motion_blur = 1
+        d.mb_dir[:] = [float(x) for x in np.asarray(mb["dir"], np.float32)]
+        d.mb_m = float(np.float32(mb["m"]))
     f0 = desc.get("group_f0")
     keep = None
     if f0 is not None:

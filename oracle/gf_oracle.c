@@ -669,6 +669,8 @@ typedef struct {
     const float *group_f0;  /* G floats (C12), may be NULL */
     int32_t foveation;      /* foveated rendering */
     float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_level_fmax[8];
+    int32_t motion_blur;    /* motion-blur reference */
+    float mb_dir[3], mb_m;
 } or_render_desc;
 
 /* Foveation threshold of a pixel ("a linear relationship between eccentricity and the
@@ -752,6 +754,17 @@ double or_path(const or_scene *s, const or_render_desc *d, uint32_t pix, uint32_
     if (d->jitter) { jx = or_uniform(d->seed, pix, smp, 0, ST_CAM, 0); jy = or_uniform(d->seed, pix, smp, 0, ST_CAM, 1); }
     float of[3], vf[3];
     camera_ray(d, px, py, jx, jy, of, vf);
+    if (d->motion_blur) {
+        /* P:L656 "a convolution with a 1D box filter oriented in direction d and with size m": the
+           field at exposure time u is shifted by s = m (u - 1/2) d, the same as a camera at -s
+           (readings M1, M2); fp32, one rounding per operation */
+        float u = or_uniform(d->seed, pix, smp, 0, 7u, 0);
+        volatile float sh = d->mb_m * (u - 0.5f);
+        for (int k = 0; k < 3; ++k) {
+            volatile float sk = sh * d->mb_dir[k];
+            of[k] = of[k] - sk;
+        }
+    }
     int nr = 0;
     uint32_t mask;
     float w[OR_MAXG];

@@ -420,6 +420,8 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
     if (!(d->hg_g > -1.0f && d->hg_g < 1.0f)) return fail(c, GF_E_INVALID_ARGUMENT, "hg_g must be in (-1,1)");
     if (d->estimator != GF_EST_ANALYTIC && d->estimator != GF_EST_TRACKING)
         return fail(c, GF_E_INVALID_ARGUMENT, "bad estimator");
+    if (d->motion_blur && !(d->mb_m >= 0.0f && std::isfinite(d->mb_m)))
+        return fail(c, GF_E_INVALID_ARGUMENT, "motion blur: mb_m must be finite and >= 0");
     if (d->foveation && !(d->fov_f0 >= 0.0f && d->fov_slope >= 0.0f && d->fov_jitter >= 0.0f && d->fov_jitter < 1.0f))
         return fail(c, GF_E_INVALID_ARGUMENT, "foveation: f0, slope >= 0 and jitter in [0,1)");
     return GF_OK;
@@ -473,6 +475,9 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.fov_gaze[0] = d->fov_gaze[0]; R.fov_gaze[1] = d->fov_gaze[1];
     R.fov_f0 = d->fov_f0; R.fov_slope = d->fov_slope; R.fov_jitter = d->fov_jitter;
     for (int k = 0; k < 8; ++k) R.fov_lfmax[k] = d->fov_level_fmax[k];
+    R.mb = d->motion_blur != 0;
+    for (int k = 0; k < 3; ++k) R.mb_dir[k] = d->mb_dir[k];
+    R.mb_m = d->mb_m;
     R.albedo = d->albedo; R.hg_g = d->hg_g; R.sun_E = d->sun_E; R.env_L = d->env_L;
     R.sun = make_float3(d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]);
     R.seed = d->seed;
@@ -512,8 +517,8 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         }
     }
     // camera BVH for the depth-0 packet kernel (static ext mask, analytic): projective boxes at the eye
-    R.camb = d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 &&
-             env_int("GF_DEBUG_NO_CAMERA_BVH", 0) == 0;
+    R.camb = d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 && !d->motion_blur &&
+             env_int("GF_DEBUG_NO_CAMERA_BVH", 0) == 0;  // (motion blur moves the eye per sample)
     if (R.camb) {
         const float* axes[3] = {d->cam_right, d->cam_up, d->cam_fwd};
         for (int a = 0; a < 3; ++a) {

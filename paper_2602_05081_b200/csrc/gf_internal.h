@@ -83,6 +83,8 @@ struct RenderDev {
     int32_t mode, max_depth, jitter, estimator;
     int32_t fov;  // foveated rendering (gf_render_desc.foveation)
     float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_lfmax[8];
+    int32_t mb;  // motion-blur reference (gf_render_desc.motion_blur)
+    float mb_dir[3], mb_m;
     float albedo, hg_g, sun_E, env_L;
     float3 sun;
     uint64_t seed;

@@ -143,6 +143,19 @@ __device__ __forceinline__ double trace_tau(const RenderDev& R, const RayDev& r,
     return tau;
 }
 
+// Motion-blur reference (readings M1-M3): the field moves by s = m (u - 1/2) dir during
+// the exposure (a box filter of length m along dir); a sample at time u sees the field shifted by s,
+// i.e. the whole path runs in the static field from the camera origin shifted by -s.  u: stream 7,
+// k = 0, depth 0, per (pixel, sample); correctly rounded fp32 as in the oracle.
+__device__ __forceinline__ void mb_shift(const RenderDev& R, uint32_t pix, uint32_t sample, float3& o) {
+    if (!R.mb) return;
+    const float u = stream_u(R.seed, pix, sample, 0, ST_MB, 0);
+    const float sh = __fmul_rn(R.mb_m, __fsub_rn(u, 0.5f));
+    o.x = __fsub_rn(o.x, __fmul_rn(sh, R.mb_dir[0]));
+    o.y = __fsub_rn(o.y, __fmul_rn(sh, R.mb_dir[1]));
+    o.z = __fsub_rn(o.z, __fmul_rn(sh, R.mb_dir[2]));
+}
+
 __global__ void __launch_bounds__(128) k_gen(RenderDev R, int32_t sample) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // grid covers whole warps
     const int32_t pix = p < R.n_paths ? path_pixel(R, p) : -1;
@@ -155,6 +168,7 @@ __global__ void __launch_bounds__(128) k_gen(RenderDev R, int32_t sample) {
         }
         float3 o, d;
         camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+        mb_shift(R, (uint32_t)pix, (uint32_t)sample, o);
         R.ox[p] = o.x; R.oy[p] = o.y; R.oz[p] = o.z;
         R.dx[p] = d.x; R.dy[p] = d.y; R.dz[p] = d.z;
         R.beta[p] = 1.0f;
@@ -1362,6 +1376,7 @@ __global__ void __launch_bounds__(128) k_tomo_w(RenderDev R, int32_t sample) {
         }
         float3 o, d;
         camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+        mb_shift(R, (uint32_t)pix, (uint32_t)sample, o);
         float w[kMaxGroups];
         const float fmx = fov_fmax<FOV>(R, (uint32_t)pix, (uint32_t)sample);
         const uint32_t mask = fov_mask<FOV>(R, fmx) & (STOCH ? policy_for(R.ext, R.sc, d, R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_EXT, 1, w)

@@ -62,7 +62,8 @@ class RenderDesc(ctypes.Structure):
                 ("sun_dir", ctypes.c_float * 3), ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("estimator", ctypes.c_int32), ("reuse_accel", ctypes.c_int32),
                 ("foveation", ctypes.c_int32), ("fov_gaze", ctypes.c_float * 2), ("fov_f0", ctypes.c_float),
-                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8)]
+                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8),
+                ("motion_blur", ctypes.c_int32), ("mb_dir", ctypes.c_float * 3), ("mb_m", ctypes.c_float)]
 
 
 def header_symbols():
@@ -249,6 +250,11 @@ class GaborField:
             d.fov_f0, d.fov_slope, d.fov_jitter = float(fov["f0"]), float(fov["slope"]), float(fov.get("jitter", 0.0))
             lf = list(np.asarray(fov["level_fmax"], np.float32)) + [0.0] * 8
             d.fov_level_fmax[:] = [float(x) for x in lf[:8]]
+        mb = desc.get("motion_blur")
+        if mb:
+            d.motion_blur = 1
+            d.mb_dir[:] = [float(x) for x in np.asarray(mb["dir"], np.float32)]
+            d.mb_m = float(np.float32(mb["m"]))
         return d
 
     def render(self, desc, spp_begin=0, spp_count=1, shard=(SHARD_NONE, 0, 1), probes=None, accum=None,

@@ -311,6 +311,67 @@ def foveation(scene, gaze, f0, slope, jitter=0.0):
             "jitter": float(jitter), "level_fmax": level_fmax(scene)}
 
 
+def omega_vectors(scene):
+    """World frequency vectors omega_vec = R S^-1 (omega, omega, omega), float64 [n, 3]."""
+    q = scene["quat"].astype(np.float64)
+    x, y, z, w = (q[:, k] / np.linalg.norm(q, axis=1) for k in range(4))
+    R = np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], -1),
+                  np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1),
+                  np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1)], 1)
+    return np.einsum("nij,nj->ni", R, scene["omega"].astype(np.float64)[:, None] / scene["scale"].astype(np.float64))
+
+
+def group_ids(scene):
+    """Group id per primitive (C10/C11): level 0 -> 0; Gabor level l, orientation bin b = argmax_k
+    |omega_hat . axis_k| (ties -> lower k) -> 1 + (l-1) K + b.  Host-side helper for mask policies."""
+    K = scene["K"]
+    lvl = scene["level"].astype(np.int64)
+    if np.all(scene["bin"] != 255):
+        b = scene["bin"].astype(np.int64)
+    else:
+        wv = omega_vectors(scene)
+        nrm = np.linalg.norm(wv, axis=1, keepdims=True)
+        wh = np.divide(wv, nrm, out=np.zeros_like(wv), where=nrm > 0)
+        axes = np.asarray(scene["bin_axes"], np.float64).reshape(K, 3)
+        b = np.argmax(np.abs(wh @ axes.T), axis=1)
+    return np.where(lvl == 0, 0, 1 + (lvl - 1) * K + b)
+
+
+def motion_blur(direction, m):
+    """Motion-blur reference parameters (gf_render_desc motion_blur fields)."""
+    d = np.asarray(direction, np.float64)
+    return {"dir": (d / np.linalg.norm(d)).astype(np.float32).tolist(), "m": float(m)}
+
+
+def motion_blur_mask(scene, direction, m, threshold, groups=None):
+    """Accelerated motion blur (readings M1-M3): cull group g if the box-filter attenuation
+    |sin(m k / 2) / (m k / 2)|, k = |omega_g . d|, of the group's mean frequency vector omega_g (signs
+    aligned with the group's orientation axis before averaging) is below `threshold`.  Level 0 is never
+    culled.  Returns the static mask (32 bits) and the per-group attenuation."""
+    d = np.asarray(direction, np.float64)
+    d = d / np.linalg.norm(d)
+    if groups is None:
+        groups = group_ids(scene)
+    wv = omega_vectors(scene)
+    G = 1 + (scene["P"] - 1) * scene["K"]
+    att = np.ones(G)
+    mask = 0
+    for g in range(G):
+        sel = groups == g
+        if g == 0 or not sel.any():
+            mask |= 1 << g
+            continue
+        v = wv[sel]
+        ref = v[np.argmax(np.linalg.norm(v, axis=1))]
+        v = np.where((v @ ref)[:, None] < 0, -v, v)
+        k = abs(float(v.mean(0) @ d))
+        x = 0.5 * m * k
+        att[g] = 1.0 if x == 0 else abs(np.sin(x) / x)
+        if att[g] >= threshold:
+            mask |= 1 << g
+    return mask, att
+
+
 def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
     """32-bit group mask selecting whole pyramid levels: level 0 -> bit 0, Gabor level l ->
     bits 1+(l-1)K .. (l)K (the group numbering g(l,b) of DESIGN.md §5; paper V_l = 2^l)."""

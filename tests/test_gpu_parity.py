@@ -433,6 +433,27 @@ def test_render_foveation_probes(gfm, orc, mode):
     _probe_compare(gfm, orc, sc, desc, probes, 8, f"foveation mode {mode}", frac_tol=0.03)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_render_motion_blur_reference_probes(gfm, orc, mode):
+    """Motion-blur reference: per-sample exposure time, field shifted
+    along the motion (camera shifted back), identical Philox streams; plus the accelerated version
+    (culled groups) is just a static mask: both vs the oracle."""
+    sc = I.scene_cfg1p() if mode else I.scene_cfg1()
+    mb = I.motion_blur((1.0, 0.2, 0.0), 0.3)
+    if mode == 0:
+        desc = dict(I.render_desc_cfg1(32, 32), jitter=1, motion_blur=mb)
+    else:
+        desc = I.render_desc_cfg2(3, 32, 32)
+        desc.update(**I.camera((0, 0, 4), (0, 0, 0), (0, 1, 0), 40.0, 32, 32))
+        desc.update(max_depth=2, albedo=0.9, hg_g=0.3, ext=I.policy(), nee=I.policy(), motion_blur=mb)
+    probes = np.random.default_rng(9).integers(0, 32 * 32, 40)
+    _probe_compare(gfm, orc, sc, desc, probes, 8, f"motion blur mode {mode}", frac_tol=0.03)
+    mask, _ = I.motion_blur_mask(sc, mb["dir"], mb["m"], 0.6)
+    culled = dict(desc, ext=I.policy(static_mask=mask), nee=I.policy(static_mask=mask))
+    culled.pop("motion_blur")
+    _probe_compare(gfm, orc, sc, culled, probes, 8, f"motion blur culled mode {mode}", frac_tol=0.03)
+
+
 def test_cfg2_bench_configuration_sampled(gfm, orc):
     """Config 2 at full size in the launch configuration bench.py times (1024^2, 1 spp per LOD
     mask, single scattering): sampled pixels of the full-image render vs the oracle's paths."""

@@ -622,3 +622,54 @@ def test_foveation_primitive_check_follows_definition(orc):
         below = dict(d, foveation={"gaze": [0, 0], "f0": f * 0.99, "slope": 0.0, "level_fmax": lf})
         assert S.render_probes(above, [p], 0, 1)[0][0, 0] == full[k]
         assert S.render_probes(below, [p], 0, 1)[0][0, 0] == 0.0
+
+
+# ---------------------------------------------------------------- motion blur
+def test_motion_blur_zero_magnitude_is_plain(orc):
+    """M1: a box filter of length 0 leaves every sample unchanged."""
+    sc = I.scene_cfg1()
+    S = orc.Scene(sc)
+    pix = list(range(0, 64, 5))
+    for mode in (0, 1):
+        base = _tiny_desc(mode, jitter=1)
+        plain = S.render_probes(base, pix, 0, 4)[0]
+        mb = S.render_probes(dict(base, motion_blur=I.motion_blur((1, 2, 0.5), 0.0)), pix, 0, 4)[0]
+        assert np.array_equal(plain, mb)
+
+
+def test_motion_blur_is_the_box_filtered_field(orc):
+    """M1/M2: the estimate over exposure times is the optical depth of the field convolved with
+    a box of length m along d: the sample mean matches the shift average of the closed form computed
+    here by Gauss-Legendre quadrature over the shift (one Gabor, one ray), within 4 SE."""
+    rng = np.random.default_rng(3)
+    sc = I._finish(np.zeros((1, 3)), I.random_quats(rng, 1), np.array([[0.3, 0.2, 0.25]]), np.array([1.0]),
+                   np.array([1.3]), np.array([1], np.uint8), name="one")
+    S = orc.Scene(sc)
+    d = _tiny_desc(0)
+    mdir, m = np.array([0.6, 0.0, 0.8]), 0.4
+    pix = 27
+    o, v = I.camera_rays_f64(d, np.array([pix % 8]), np.array([pix // 8]))
+    xs, ws = np.polynomial.legendre.leggauss(64)
+    ref = 0.0
+    for x, wgt in zip(xs, ws):  # shift s = m (u - 1/2), u = (x + 1) / 2
+        sft = m * 0.5 * x * mdir
+        ray = I.pack_rays(o - sft, v)[0]
+        ref += 0.5 * wgt * float(orc.lib().or_prim_integral(S.h, 0, orc._p(ray[:3]), orc._p(ray[4:7]), 0.0, np.inf))
+    ref *= float(sc["alpha"][0])
+    vals = S.render_probes(dict(d, motion_blur=I.motion_blur(mdir, m)), [pix], 0, 20000)[0][0]
+    se = vals.std() / math.sqrt(vals.size)
+    assert abs(vals.mean() - ref) <= 4 * se + 1e-9, (vals.mean(), ref, se)
+    assert vals.std() > 0
+
+
+def test_motion_blur_mask_attenuation(orc):
+    """M3: a group is culled iff |sin(m k/2)/(m k/2)| of its mean frequency along d is
+    below the threshold; level 0 is never culled; m = 0 culls nothing."""
+    sc = I.scene_cfg1()
+    mask0, att0 = I.motion_blur_mask(sc, (1, 0, 0), 0.0, 0.99)
+    assert mask0 == (1 << 10) - 1 and np.all(att0 == 1.0)
+    mask, att = I.motion_blur_mask(sc, (1, 0, 0), 0.2, 0.6)
+    assert mask & 1
+    for g in range(1, 10):
+        assert bool(mask >> g & 1) == (att[g] >= 0.6)
+    assert 0 < bin(mask).count("1") < 10
