@@ -324,7 +324,8 @@ def main():
         d2h = out_host.numel() * out_host.element_size()
         e2e_ms, e2e_rays, e2e_steps = 0.0, 0, []
         g2 = gf.GaborField(local)
-        for k in range(1 + args.steps):
+        e2e_warm = 2
+        for k in range(e2e_warm + args.steps):
             torch.cuda.synchronize()
             rays.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -342,7 +343,7 @@ def main():
             out_host.copy_(accum, non_blocking=True)
             b.record()
             torch.cuda.synchronize()
-            if k > 0:  # first iteration is warm-up
+            if k >= e2e_warm:  # the first iterations are warm-up
                 e2e_ms += a.elapsed_time(b)
                 e2e_rays += int(rays.sum().item())
                 e2e_steps.append(round(a.elapsed_time(b), 3))
