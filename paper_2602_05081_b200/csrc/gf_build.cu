@@ -515,7 +515,11 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
 #ifndef GF_LIGHT_LEAFMAX
 #define GF_LIGHT_LEAFMAX 4  // primitives per leaf of the NEE light BVH (measured: 1/2/3 slower)
 #endif
+#ifndef GF_CAM_LEAFMAX
+#define GF_CAM_LEAFMAX 4  // primitives per leaf of the camera BVH (measured: 2/3/6 no better)
+#endif
 static_assert(GF_LIGHT_LEAFMAX >= 1 && GF_LIGHT_LEAFMAX <= kLeafMax, "warp traversal buffers hold kLeafMax per leaf");
+static_assert(GF_CAM_LEAFMAX >= 1 && GF_CAM_LEAFMAX <= kLeafMax, "k_ff walks the camera BVH with kLeafMax buffers");
 // Asynchronous build in frame F (host rows): same kernels, no host synchronisation; the node count
 // stays on the device (S.nsize[0]) and the tree depth is written to *depth (device).
 cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S,
@@ -543,10 +547,10 @@ cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int
         if ((e = cudaMemsetAsync(S.flags, 0, sizeof(uint32_t) * n, st))) return e;
     }
     RefitArgs R{n, S.left, S.right, S.parent, (const int32_t*)S.vals_out, S.pbox, group, S.nbox, S.nmask, S.ncount,
-                S.nsize, S.flags, (uint32_t)GF_LIGHT_LEAFMAX};
+                S.nsize, S.flags, (uint32_t)(eye ? GF_CAM_LEAFMAX : GF_LIGHT_LEAFMAX)};
     k_refit<<<nblk(n, 256), 256, 0, st>>>(R);
     LayoutArgs L{n, S.left, S.right, S.parent, S.rlo, S.nbox, S.nmask, S.ncount, S.nsize, nodes, 0, depth,
-                 (uint32_t)GF_LIGHT_LEAFMAX};
+                 (uint32_t)(eye ? GF_CAM_LEAFMAX : GF_LIGHT_LEAFMAX)};
     k_layout<<<nblk(2 * n - 1, 256), 256, 0, st>>>(L);
     k_pair_dev<<<nblk(2 * n - 1, 256), 256, 0, st>>>(nodes, S.nsize, 2 * n - 1, (GNode2*)nodes2_v);
     k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
