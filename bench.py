@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--motion-blur", choices=["reference", "culled"], default=None,
                     help="motion-blur variant (direction (1, 0.2, 0), magnitude 0.02): time-sampled reference, "
                          "or the group-culled approximation (attenuation threshold 0.6)")
+    ap.add_argument("--adaptive-extent", type=float, default=None, metavar="EPS",
+                    help="adaptive clamping variant (Eq. 15): per-primitive extents for threshold EPS")
     ap.add_argument("--profile-pass", action="store_true", help="only run warmup+steps (for ncu launch lists)")
     args = ap.parse_args()
     rank, local, world = dist_env()
@@ -209,6 +211,9 @@ def main():
     descs = [dict(d, reuse_accel=1) for d in descs]
     if args.estimator == "tracking":
         descs = [dict(d, estimator=1) for d in descs]
+    if args.adaptive_extent:
+        sc = dict(sc, extent=I.adaptive_extent(sc, args.adaptive_extent))
+        name += f" [adaptive extents, eps {args.adaptive_extent:g}: mean E {float(np.mean(sc['extent'])):.2f}]"
     if args.motion_blur:
         mdir, mm = (1.0, 0.2, 0.0), 0.02
         if args.motion_blur == "reference":

@@ -372,6 +372,20 @@ def motion_blur_mask(scene, direction, m, threshold, groups=None):
     return mask, att
 
 
+def adaptive_extent(scene, eps):
+    """Adaptive clamping (Eq. 15, reading C8'): per primitive
+    E = min(3, sqrt(max(0, -2 ln(eps 2 pi s1 s2 s3 / (alpha s_max)) - 3 omega^2))), the whitened
+    distance beyond which a ray's untruncated line integral (worst case ||W v|| = 1/s_max, Omega^2 =
+    k_W^2 = 3 omega^2 as in Eq. 15) is below eps.  Non-conservative for rays across the modulation
+    planes (Omega < k_W); returned as the `extent` input of both the kernels and the oracle, floored at
+    1e-3 (the loader requires E > 0; such a primitive keeps a negligible core)."""
+    s = scene["scale"].astype(np.float64)
+    a = scene["alpha"].astype(np.float64)
+    w = scene["omega"].astype(np.float64)
+    arg = -2.0 * np.log(eps * 2.0 * math.pi * s.prod(1) / (np.maximum(a, 1e-30) * s.max(1))) - 3.0 * w * w
+    return np.clip(np.sqrt(np.maximum(arg, 0.0)), 1e-3, 3.0).astype(np.float32)
+
+
 def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
     """32-bit group mask selecting whole pyramid levels: level 0 -> bit 0, Gabor level l ->
     bits 1+(l-1)K .. (l)K (the group numbering g(l,b) of DESIGN.md §5; paper V_l = 2^l)."""

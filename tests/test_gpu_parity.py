@@ -454,6 +454,23 @@ def test_render_motion_blur_reference_probes(gfm, orc, mode):
     _probe_compare(gfm, orc, sc, culled, probes, 8, f"motion blur culled mode {mode}", frac_tol=0.03)
 
 
+def test_adaptive_extent_parity(gfm, orc):
+    """Adaptive clamping (Eq. 15, reading C8'): per-primitive extents are inputs of both sides; the
+    transmittance parity holds and the clamped field is cheaper (fewer hits) than the 3-sigma one."""
+    sc = I.scene_cfg2()
+    sca = dict(sc, extent=I.adaptive_extent(sc, 1e-3))
+    assert np.all(sca["extent"] <= 3.0) and np.mean(sca["extent"]) < 3.0
+    rays = camera_rays(I.render_desc_cfg2(3), 300, seed=31)
+    f = field(gfm, sca)
+    tau, T, cnt = f.trace_transmittance(rays, counters=True)
+    r = orc.Scene(sca).trace(rays)
+    assert_tau_parity(tau.cpu().numpy(), r["tau"], r["A"], T.cpu().numpy(), "adaptive extent")
+    assert np.array_equal(cnt.cpu().numpy()[:, 2], r["nhits"])
+    f3 = field(gfm, sc)
+    _, _, c3 = f3.trace_transmittance(rays, counters=True)
+    assert cnt[:, 2].sum() < c3[:, 2].sum()
+
+
 def test_cfg2_bench_configuration_sampled(gfm, orc):
     """Config 2 at full size in the launch configuration bench.py times (1024^2, 1 spp per LOD
     mask, single scattering): sampled pixels of the full-image render vs the oracle's paths."""
