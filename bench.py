@@ -211,6 +211,7 @@ def main():
     descs = [dict(d, reuse_accel=1) for d in descs]
     if args.estimator == "tracking":
         descs = [dict(d, estimator=1) for d in descs]
+        name += " [delta/ratio tracking estimator]"
     if args.adaptive_extent:
         sc = dict(sc, extent=I.adaptive_extent(sc, args.adaptive_extent))
         name += f" [adaptive extents, eps {args.adaptive_extent:g}: mean E {float(np.mean(sc['extent'])):.2f}]"
@@ -229,7 +230,6 @@ def main():
         descs = [dict(d, foveation=I.foveation(sc, (d["width"] / 2, d["height"] / 2), f0, f0 / 0.7, 0.2))
                  for d in descs]
         name += " [foveated: gaze centre, threshold 1.05 max level frequency, zero at eccentricity 0.7]"
-        name += " [delta/ratio tracking estimator]"
     f = gf.GaborField(local)
     f.load_primitives(sc, group_f0=I.group_f0(sc))
     f.build_bvh()
