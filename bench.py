@@ -192,6 +192,9 @@ def main():
                          "or the group-culled approximation (attenuation threshold 0.6)")
     ap.add_argument("--adaptive-extent", type=float, default=None, metavar="EPS",
                     help="adaptive clamping variant (Eq. 15): per-primitive extents for threshold EPS")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="render the LOD frames of a step on this many CUDA streams, each with its own scratch "
+                         "(default 2: two frames in flight fill each other's kernel tails)")
     ap.add_argument("--profile-pass", action="store_true", help="only run warmup+steps (for ncu launch lists)")
     args = ap.parse_args()
     rank, local, world = dist_env()
@@ -236,15 +239,24 @@ def main():
     H, W = descs[0]["height"], descs[0]["width"]
     shard = (gf.SHARD_SAMPLES, rank, world)
     scratch = f.render_scratch(descs[0], 1, shard)
+    nstr = max(1, min(args.streams, len(descs)))
+    scratches = [scratch] + [f.render_scratch(descs[0], 1, shard) for _ in range(nstr - 1)]
+    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream() for _ in range(nstr - 1)]
     accum = torch.zeros((len(descs), H * W * 2), dtype=torch.float32, device=f.device)
     rays = torch.zeros(2, dtype=torch.int64, device=f.device)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f.device)  # 256 MB > 126 MB L2
 
-    def step(k):
+    def step(k, ns=nstr):
         accum.zero_()
+        main = streams[0]
+        for s_ in streams[1:ns]:
+            s_.wait_stream(main)
         for i, d in enumerate(descs):
-            f.render(d, spp_begin=k * world, spp_count=world, shard=shard, accum=accum[i], ray_counts=rays,
-                     scratch=scratch)
+            with torch.cuda.stream(streams[i % ns]):
+                f.render(d, spp_begin=k * world, spp_count=world, shard=shard, accum=accum[i], ray_counts=rays,
+                         scratch=scratches[i % ns])
+        for s_ in streams[1:ns]:
+            main.wait_stream(s_)
         if world > 1:
             dist.all_reduce(accum)
 
@@ -275,7 +287,16 @@ def main():
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
     st = f.stats(reset=True)
     f.set_profiling()
-    nrays = int(rays.sum().item())
+    nrays = int(rays.sum().item())  # (before any further pass adds to the counter)
+    if nstr > 1:  # per-kernel CUDA-event times for the roofline from a one-stream pass (streams overlap)
+        f.set_profiling(timing=True)
+        for k in range(args.steps):
+            step(args.warmup + k, 1)
+        torch.cuda.synchronize()
+        st_stage = f.stats(reset=True)
+        f.set_profiling()
+    else:
+        st_stage = st
     tt = torch.tensor([t_ms, float(nrays)], dtype=torch.float64, device=f.device)
     if world > 1:
         tmax = tt.clone()
@@ -293,9 +314,9 @@ def main():
     torch.cuda.synchronize()
     sw = f.stats(reset=True)
     f.set_profiling()
-    stage_ms = {k: v for k, v in st["stage_ms"].items() if v > 0}
+    stage_ms = {k: v for k, v in st_stage["stage_ms"].items() if v > 0}
     dom = max(stage_ms, key=stage_ms.get)
-    launches = st["stage_launches"][dom]
+    launches = st_stage["stage_launches"][dom]
     w = sw["work"][dom]
     flops = (FLOP_NODE * w["nodes"] + FLOP_TEST * w["tests"] + FLOP_HIT * w["hits"] + FLOP_ERF * w["erf_complex"]
              + FLOP_ERF_REAL * w["erf_real"] + FLOP_ROOT_EVAL * w["root_evals"])
@@ -375,6 +396,7 @@ def main():
                            "paths_per_step": len(descs) * W * H * world,
                            "rays_per_step": total_rays / args.steps,
                            "l2": "flushed between timed steps (256 MB write, outside the step events)",
+                           "streams": nstr,
                            "accel": "scene BVH built before the timed steps; the per-view light and camera BVHs "
                                     "built by the first warm-up render and reused (reuse_accel); e2e rebuilds all "
                                     "each step",

@@ -46,17 +46,29 @@ struct gf_ctx {
         const void* where = nullptr;  // node array inside the scratch
         uint64_t gen = ~0ull;
         float key[12] = {};
-    } light_cache, cam_cache;
+    } light_cache[4], cam_cache[4];  // per scratch buffer (up to 4 in flight, e.g. one per stream)
 };
 
 // true if the frame BVH (node array at `where`, scene generation, key floats) is already there;
 // otherwise records it as built now
-static bool frame_cached(gf_ctx::FrameCache& fc, const void* where, uint64_t gen, const float* key, int nkey) {
-    bool same = fc.where == where && fc.gen == gen;
-    for (int k = 0; k < nkey && same; ++k) same = fc.key[k] == key[k];
-    fc.where = where;
-    fc.gen = gen;
-    for (int k = 0; k < nkey; ++k) fc.key[k] = key[k];
+static bool frame_cached(gf_ctx::FrameCache* fcs, const void* where, uint64_t gen, const float* key, int nkey) {
+    gf_ctx::FrameCache* fc = nullptr;
+    for (int i = 0; i < 4 && !fc; ++i)
+        if (fcs[i].where == where) fc = fcs + i;
+    if (!fc) {  // new scratch buffer: take a free slot, else the first (round robin)
+        for (int i = 0; i < 4 && !fc; ++i)
+            if (!fcs[i].where) fc = fcs + i;
+        if (!fc) {
+            for (int i = 0; i < 3; ++i) fcs[i] = fcs[i + 1];
+            fc = fcs + 3;
+        }
+        fc->gen = ~0ull;
+    }
+    bool same = fc->where == where && fc->gen == gen;
+    for (int k = 0; k < nkey && same; ++k) same = fc->key[k] == key[k];
+    fc->where = where;
+    fc->gen = gen;
+    for (int k = 0; k < nkey; ++k) fc->key[k] = key[k];
     return same;
 }
 
