@@ -361,9 +361,14 @@ def main():
             g2.load_primitives(scd, group_f0=I.group_f0(sc))
             g2.build_bvh()
             accum.zero_()
-            for i, d in enumerate(descs):
-                g2.render(d, spp_begin=k * world, spp_count=world, shard=shard, accum=accum[i], ray_counts=rays,
-                          scratch=scratch)
+            for s_ in streams[1:]:
+                s_.wait_stream(streams[0])
+            for i, d in enumerate(descs):  # same stream layout as the timed steps
+                with torch.cuda.stream(streams[i % nstr]):
+                    g2.render(d, spp_begin=k * world, spp_count=world, shard=shard, accum=accum[i],
+                              ray_counts=rays, scratch=scratches[i % nstr])
+            for s_ in streams[1:]:
+                streams[0].wait_stream(s_)
             if world > 1:
                 dist.all_reduce(accum)
             out_host.copy_(accum, non_blocking=True)
