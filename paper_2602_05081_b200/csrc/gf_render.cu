@@ -231,6 +231,9 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #ifndef GF_CAM_BVH
 #define GF_CAM_BVH 1  // k_ff_pkt traverses the camera BVH (projective boxes, built per gf_render call)
 #endif
+#ifndef GF_PRE_PF
+#define GF_PRE_PF 1  // packet resolve: load the next chunk's chord data one chunk ahead
+#endif
 #ifndef GF_PACKET
 #define GF_PACKET 1  // depth-0 (camera) free flight with packet traversal (k_ff_pkt)
 #endif
@@ -634,13 +637,33 @@ __device__ __forceinline__ void ff_resolve(const RenderDev& R, uint32_t p, float
 #pragma unroll 1
         for (int side = 0; side < 2; ++side) {
             const uint32_t n = nside[side];
+#if GF_PRE_PF
+            float4 xnext = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (PRE && lane < n) xnext = aux[side == 0 ? lane : cap - 1 - lane];
+#if GF_PRE_PF == 2
+            float4 xnext2 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (PRE && lane + 32 < n) xnext2 = aux[side == 0 ? lane + 32 : cap - 1 - (lane + 32)];
+#endif
+#endif
             for (uint32_t base = 0; base < n; base += 32) {
                 const uint32_t i = base + lane;
                 bool push = false;
                 float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#if GF_PRE_PF == 2
+                const float4 xcur = xnext;  // chord data of this chunk, loaded two chunks ahead
+                xnext = xnext2;
+                if (PRE && i + 64 < n) xnext2 = aux[side == 0 ? i + 64 : cap - 1 - (i + 64)];
+#elif GF_PRE_PF
+                const float4 xcur = xnext;  // chord data of this chunk, loaded one chunk ahead
+                if (PRE && i + 32 < n) xnext = aux[side == 0 ? i + 32 : cap - 1 - (i + 32)];
+#endif
                 if (PRE && i < n) {  // aux = (t_a, t_b, full, amp G(u0)); records read only for straddlers
                     const uint32_t slot = side == 0 ? i : cap - 1 - i;
+#if GF_PRE_PF
+                    const float4 x = xcur;
+#else
                     const float4 x = aux[slot];
+#endif
                     if (t >= x.y) {
                         part += x.z;
                     } else if (t > x.x) {
