@@ -163,6 +163,14 @@ gf_status gf_trace_transmittance(gf_ctx *ctx, const float *rays, int64_t n, uint
 gf_status gf_trace_transmittance_ex(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, uint32_t flags,
                                     float *tau_out, float *T_out, uint32_t *counters_out, gf_stream stream);
 
+/* Backward of the optical depth w.r.t. the opacities (the alpha part of
+ * d tau / d(mu, q, s, alpha, omega); tomographic regression P:L370-L470):
+ *   grad_alpha[i] += sum_r dl_dtau[r] * d tau_r / d alpha_i,  d tau_r / d alpha_i = w_g(i) tau_ri / alpha_i
+ * (tau is linear in alpha).  rays as gf_trace_transmittance (same ext policy and draws); dl_dtau:
+ * device n fp32; grad_alpha: device n_prims fp32 in input order, accumulated (caller zeroes). */
+gf_status gf_trace_grad_alpha(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, const float *dl_dtau,
+                              float *grad_alpha, gf_stream stream);
+
 /* Candidate sets (test path, C21): for each ray, the ORIGINAL indices of the
  * primitives accepted by the fp32 ellipsoid predicate (traversal order),
  * ids[r * capacity + k], count[r] = total (may exceed capacity: truncated). */

@@ -68,6 +68,7 @@ def lib():
         L.or_prim_integral_infinite.restype = dbl
         L.or_prim_integral_infinite.argtypes = [vp, i32, vp, vp]
         L.or_trace.argtypes = [vp, vp, i64, u32, vp, vp, vp, vp, vp, i32]
+        L.or_grad_alpha.argtypes = [vp, vp, i64, u32, vp, vp, vp]
         L.or_candidates.restype = i32
         L.or_candidates.argtypes = [vp, vp, u32, vp, i32, vp]
         L.or_pair_r2_rel.restype = dbl
@@ -164,6 +165,15 @@ class Scene:
         if want_groups:
             out["groups"] = grp
         return out
+
+    def grad_alpha(self, rays, dl_dtau, mask=0xFFFFFFFF, weights=None):
+        """d(sum_r dl[r] tau_r)/d alpha_i for every primitive (input order)."""
+        rays = _f32(rays).reshape(-1, 8)
+        dl = np.ascontiguousarray(dl_dtau, np.float64)
+        g = np.zeros(self.n, np.float64)
+        w = _f32(weights)
+        lib().or_grad_alpha(self.h, _p(rays), rays.shape[0], mask & 0xFFFFFFFF, _p(w), _p(dl), _p(g))
+        return g
 
     def candidates(self, ray, mask=0xFFFFFFFF):
         ray = _f32(ray).reshape(8)

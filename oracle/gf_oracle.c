@@ -375,6 +375,28 @@ void or_trace(const or_scene *s, const float *rays, long n, uint32_t mask, const
     run_parallel(trace_work, &c, n, nthreads);
 }
 
+/* Backward of tau w.r.t. the opacities (the alpha part):
+   tau_r = sum_i w_g(i) alpha_i I_i(r) is linear in alpha, so
+   grad[i] = sum_r dl[r] w_g(i) I_i(r), I_i the closed-form integral of kernel i with alpha = 1 (App. A).
+   Plain double loops over rays and primitives (no BVH). */
+void or_grad_alpha(const or_scene *s, const float *rays, long n, uint32_t mask, const float *wts,
+                   const double *dl, double *grad) {
+    for (int i = 0; i < s->n; ++i) grad[i] = 0.0;
+    for (long r = 0; r < n; ++r) {
+        const float *ray = rays + 8 * r;
+        double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};
+        for (int i = 0; i < s->n; ++i) {
+            int g = s->group[i];
+            if (!((mask >> g) & 1u)) continue;
+            or_pair p;
+            pair_setup(s, i, o, v, ray[3], ray[7], &p);
+            if (!p.hit) continue;
+            double w = wts ? (double)wts[g] : 1.0;
+            grad[i] += dl[r] * w * seg_integral(s, i, &p, p.tin, p.tout);
+        }
+    }
+}
+
 /* candidate set of one ray (prims whose clipped chord has positive length) */
 int or_candidates(const or_scene *s, const float *ray, uint32_t mask, int *ids, int cap, double *r2_out) {
     double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};

@@ -388,6 +388,17 @@ gf_status gf_trace_transmittance(gf_ctx* c, const float* rays, int64_t n, uint64
     return gf_trace_transmittance_ex(c, rays, n, seed, 0u, tau_out, T_out, counters, stream);
 }
 
+gf_status gf_trace_grad_alpha(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, const float* dl_dtau,
+                              float* grad_alpha, gf_stream stream) {
+    TraceArgs A;
+    if (gf_status s = trace_common(c, rays, n, A, 0u)) return s;
+    if (!c->built) return fail(c, GF_E_STATE, "gf_trace_grad_alpha before gf_build_bvh");
+    if (n > 0 && (!dl_dtau || !grad_alpha)) return fail(c, GF_E_INVALID_ARGUMENT, "null gradient buffers");
+    A.seed = seed;
+    GF_CUDA(c, gf_launch_grad_alpha(A, dl_dtau, grad_alpha, (cudaStream_t)stream), "k_grad_alpha");
+    return GF_OK;
+}
+
 gf_status gf_trace_candidates(gf_ctx* c, const float* rays, int64_t n, uint32_t flags, int32_t* ids,
                               int32_t capacity, int32_t* count, gf_stream stream) {
     TraceArgs A;

@@ -137,6 +137,48 @@ __global__ void __launch_bounds__(128) k_trace_w(TraceArgs A) {
     if (COUNT && A.work) flush_work(A.work + kWorkSlots * STAGE_TRACE, tot);
 }
 
+// Backward of tau w.r.t. the opacities (alpha part): tau is linear in alpha,
+// d tau_r / d alpha_i = w_g c_i/alpha_i (1/j) J_i with c_i / alpha_i = 1 / (2 pi s1 s2 s3) =
+// |W0| |W1| |W2| / (2 pi).  One warp per ray over the BVH; each hit's integral lane-local (seg_J),
+// scattered into grad[perm[k]] (input order) with atomics.
+template <bool STOCH>
+__global__ void __launch_bounds__(128) k_grad_alpha(TraceArgs A, const float* __restrict__ dl,
+                                                    float* __restrict__ grad) {
+    __shared__ WarpTrav s_t[4];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Work wk;
+    for (int64_t i = (int64_t)blockIdx.x * 4 + wid; i < A.n; i += (int64_t)gridDim.x * 4) {
+        const float4 r0 = __ldg((const float4*)A.rays + 2 * i);
+        const float4 r1 = __ldg((const float4*)A.rays + 2 * i + 1);
+        const float3 o = make_float3(r0.x, r0.y, r0.z), d = make_float3(r1.x, r1.y, r1.z);
+        const RayDev r = make_ray(o, d, r0.w, r1.w);
+        float w[kMaxGroups];
+        uint32_t mask;
+        if (STOCH) mask = policy_for(A.pol, A.sc, d, A.seed, (uint32_t)i, 0, 0, ST_EXT, 1, w);
+        else mask = A.pol.static_mask;
+        const float g = __ldg(dl + i);
+        if (g == 0.0f) continue;
+        warp_traverse<false>(A.nodes, A.nodes2, A.n_nodes, A.stk_limit, r, r.tmin, r.tmax, mask, s_t[wid], wk,
+                             [&](bool valid, uint32_t ref) {
+            if (!valid) return;
+            const uint32_t k = ref & kRefIdx;
+            const GPrim* pp = A.prims + k;
+            GPrim P;
+            P.a = __ldg(&pp->a);
+            if (!sphere_pretest(P.a, r, r.tmin, r.tmax)) return;
+            P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+            Setup s;
+            if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
+            const float nb = sqrtf(P.b.x * P.b.x + P.b.y * P.b.y + P.b.z * P.b.z);
+            const float nc = sqrtf(P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
+            const float nd = sqrtf(P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
+            float v = nb * nc * nd * 0.15915494309189535f * s.ij * seg_J(s, s.u0, s.u1, wk);
+            if (STOCH) v *= w[ref >> 27];
+            atomicAdd(grad + A.perm[k], g * v);
+        });
+    }
+}
+
 template <bool BRUTE>
 __global__ void __launch_bounds__(128) k_candidates(TraceArgs A) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -189,6 +231,17 @@ cudaError_t gf_launch_trace(const TraceArgs& A, bool brute_force, bool count, cu
         }
     }
 #undef GF_T
+    return cudaGetLastError();
+}
+
+cudaError_t gf_launch_grad_alpha(const TraceArgs& A, const float* dl, float* grad, cudaStream_t st) {
+    if (A.n == 0 || A.n_nodes == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned wgrid = (unsigned)std::min<int64_t>((A.n + 3) / 4, (int64_t)sms * 16);
+    if (!(A.pol.ls == 0 && A.pol.os == 0)) k_grad_alpha<true><<<wgrid, 128, 0, st>>>(A, dl, grad);
+    else k_grad_alpha<false><<<wgrid, 128, 0, st>>>(A, dl, grad);
     return cudaGetLastError();
 }
 

@@ -97,6 +97,7 @@ def lib():
     L.gf_trace_transmittance.argtypes = [vp, vp, i64, u64, vp, vp, vp, vp]
     L.gf_trace_transmittance_ex.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp, vp]
     L.gf_trace_candidates.argtypes = [vp, vp, i64, u32, vp, i32, vp, vp]
+    L.gf_trace_grad_alpha.argtypes = [vp, vp, i64, u64, vp, vp, vp]
     L.gf_render_scratch_bytes.argtypes = [vp, ctypes.POINTER(RenderDesc), ctypes.POINTER(sz)]
     L.gf_render.argtypes = [vp, ctypes.POINTER(RenderDesc), vp, vp, sz, vp, vp]
     L.gf_set_profiling.argtypes = [vp, u32]
@@ -214,6 +215,16 @@ class GaborField:
         self._check(self.L.gf_trace_transmittance_ex(self.ctx, _ptr(rays), n, seed & 0xFFFFFFFFFFFFFFFF, flags,
                                                      _ptr(tau), _ptr(T), _ptr(cnt), _stream()))
         return tau, T, cnt
+
+    def trace_grad_alpha(self, rays, dl_dtau, seed=0, out=None):
+        """d(sum_r dl_dtau[r] tau_r) / d alpha (input order, fp32)."""
+        torch = self.torch
+        rays = torch.as_tensor(rays).to(device=self.device, dtype=torch.float32).contiguous().view(-1, 8)
+        dl = torch.as_tensor(dl_dtau).to(device=self.device, dtype=torch.float32).contiguous()
+        grad = out if out is not None else torch.zeros(self.n, dtype=torch.float32, device=self.device)
+        self._check(self.L.gf_trace_grad_alpha(self.ctx, _ptr(rays), rays.shape[0], seed,
+                                               _ptr(dl), _ptr(grad), _stream()))
+        return grad
 
     def trace_candidates(self, rays, capacity=2048, brute_force=False):
         torch = self.torch

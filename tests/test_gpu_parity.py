@@ -471,6 +471,33 @@ def test_adaptive_extent_parity(gfm, orc):
     assert cnt[:, 2].sum() < c3[:, 2].sum()
 
 
+@pytest.mark.parametrize("stoch", [False, True])
+def test_grad_alpha_parity(gfm, orc, stoch):
+    """Opacity gradient (the alpha part) vs the oracle's plain double loops:
+    per primitive within 1e-4 relative + 1e-6 of the largest |gradient|."""
+    sc = I.scene_cfg1(seed=21)
+    f = field(gfm, sc, group_f0=I.group_f0(sc))
+    pol = I.policy(level_strategy=5, beta=0.2, orient_strategy=3) if stoch else I.policy(static_mask=I.level_mask([0, 2, 3]))
+    f.set_lod_mask(pol)
+    rays = I.rays_through_box(4, 500)
+    dl = np.random.default_rng(7).normal(size=500).astype(np.float32)
+    g = f.trace_grad_alpha(rays, dl, seed=5).cpu().numpy().astype(np.float64)
+    S = orc.Scene(sc)
+    if stoch:
+        go = np.zeros(sc["n"])
+        f0 = I.group_f0(sc)
+        for r in range(len(rays)):  # per-ray masks and weights (same draws as gf_trace_transmittance)
+            ul = orc.uniform(5, r, 0, 0, 0, 1)
+            uo = [orc.uniform(5, r, 0, 0, 0, 2 + l) for l in range(sc["P"] - 1)]
+            m, w = S.policy_eval(dict(I.policy(), **pol), rays[r, 4:7], ul, uo, f0)
+            go += S.grad_alpha(rays[r:r + 1], dl[r:r + 1].astype(np.float64), m, w)
+    else:
+        go = S.grad_alpha(rays, dl.astype(np.float64), pol["static_mask"])
+    tol = 1e-4 * np.abs(go) + 1e-6 * np.abs(go).max()
+    assert np.all(np.abs(g - go) <= tol), np.max(np.abs(g - go) - tol)
+    assert np.count_nonzero(go) > 100
+
+
 def test_cfg2_bench_configuration_sampled(gfm, orc):
     """Config 2 at full size in the launch configuration bench.py times (1024^2, 1 spp per LOD
     mask, single scattering): sampled pixels of the full-image render vs the oracle's paths."""

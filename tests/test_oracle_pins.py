@@ -673,3 +673,21 @@ def test_motion_blur_mask_attenuation(orc):
     for g in range(1, 10):
         assert bool(mask >> g & 1) == (att[g] >= 0.6)
     assert 0 < bin(mask).count("1") < 10
+
+
+# ---------------------------------------------------------------- backward (alpha part)
+def test_grad_alpha_matches_finite_differences(orc):
+    """tau is linear in the opacities (Eq. 1-2), so the opacity gradient of sum_r dl_r tau_r equals the
+    finite difference of the oracle's own forward trace (one primitive's alpha doubled), to rounding."""
+    sc = I.scene_cfg1(n=60, seed=5)
+    S = orc.Scene(sc)
+    rays = I.rays_through_box(3, 40)
+    dl = np.random.default_rng(2).normal(size=40)
+    g = S.grad_alpha(rays, dl)
+    base = S.trace(rays)["tau"]
+    for i in (0, 7, 33, 59):
+        sc2 = dict(sc, alpha=sc["alpha"].copy())
+        sc2["alpha"][i] *= 2.0
+        d = (orc.Scene(sc2).trace(rays)["tau"] - base) @ dl / float(sc["alpha"][i])
+        assert abs(d - g[i]) <= 1e-9 * (1 + abs(g[i])), (i, d, g[i])
+    assert np.count_nonzero(g) > 10
