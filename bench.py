@@ -192,6 +192,8 @@ def main():
                          "or the group-culled approximation (attenuation threshold 0.6)")
     ap.add_argument("--adaptive-extent", type=float, default=None, metavar="EPS",
                     help="adaptive clamping variant (Eq. 15): per-primitive extents for threshold EPS")
+    ap.add_argument("--tomography", action="store_true",
+                    help="tomography variant: the config's scene and views, primary-ray transmittance only (mode 0)")
     ap.add_argument("--streams", type=int, default=2,
                     help="render the LOD frames of a step on this many CUDA streams, each with its own scratch "
                          "(default 2: two frames in flight fill each other's kernel tails)")
@@ -212,6 +214,9 @@ def main():
     # the per-view light / camera BVHs live in the one scratch buffer the steps share (gf_render
     # reuse_accel): built in the first warm-up render, like the scene BVH; e2e rebuilds everything
     descs = [dict(d, reuse_accel=1) for d in descs]
+    if args.tomography:
+        descs = [dict(d, mode=0, max_depth=1) for d in descs]
+        name += " [tomography: primary-ray transmittance only]"
     if args.estimator == "tracking":
         descs = [dict(d, estimator=1) for d in descs]
         name += " [delta/ratio tracking estimator]"
@@ -329,7 +334,7 @@ def main():
     peak = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
     clocks = clk.summary()
     tr_kernel, traffic = load_traffic(args.config, dom)
-    kernel = tr_kernel or {"ff": "k_ff_pkt (depth 0, static masks) / k_ff", "nee": "k_nee_w", "tomo": "k_tomo_w",
+    kernel = tr_kernel or {"ff": "k_ff_pkt (depth 0, static masks) / k_ff", "nee": "k_nee_w", "tomo": "k_tomo_pkt (static masks) / k_tomo_w",
                            "ff_fallback": "k_ffA+k_ffB"}.get(dom, dom)
     roofline = {"bound": "alu", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,

@@ -540,8 +540,10 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         }
     }
     // camera BVH for the depth-0 packet kernel (static ext mask, analytic): projective boxes at the eye
-    R.camb = d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 && !d->motion_blur &&
+    R.camb = (d->mode == GF_MODE_TOMOGRAPHY || d->estimator == GF_EST_ANALYTIC) && c->n > 0 && !d->motion_blur &&
              env_int("GF_DEBUG_NO_CAMERA_BVH", 0) == 0;  // (motion blur moves the eye per sample)
+    // packets pay off once the chunk fills the GPU (small images: one warp per pixel, k_tomo_w)
+    R.tomo_pkt_min = env_int("GF_DEBUG_TOMO_PKT_MIN", 1 << 16);
     if (R.camb) {
         const float* axes[3] = {d->cam_right, d->cam_up, d->cam_fwd};
         for (int a = 0; a < 3; ++a) {

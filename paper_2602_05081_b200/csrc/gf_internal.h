@@ -119,6 +119,7 @@ struct RenderDev {
     uint32_t* ldepth;
     // camera BVH for depth-0 rays: projective boxes, basis rows r, u, f (cb) at the eye
     int32_t camb;  // camera BVH built for this call
+    int64_t tomo_pkt_min;  // tomography chunks with at least this many paths take k_tomo_pkt
     float cb[9];
     gfk::GNode* cnodes;
     gfk::GNode2* cnodes2;

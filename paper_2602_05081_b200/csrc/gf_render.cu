@@ -1415,6 +1415,104 @@ __global__ void __launch_bounds__(128) k_tomo_w(RenderDev R, int32_t sample) {
     if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
 }
 
+// Tomography of coherent camera rays (static mask, no foveation / motion blur): the packet walk of
+// k_ff_pkt over the camera BVH for 32 consecutive pixels (one 8x4 block), each lane integrating its
+// own hits lane-locally (seg_J; all lanes test the same primitive, so the erf type is uniform).
+template <bool COUNT>
+__global__ void __launch_bounds__(128) k_tomo_pkt(RenderDev R, int32_t sample) {
+    __shared__ uint32_t s_stk[4][kPStk];
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* stk = s_stk[wid];
+    const uint32_t mask = R.ext.static_mask;
+    Work wk;
+    uint32_t nray = 0;
+    for (int64_t base = ((int64_t)blockIdx.x * 4 + wid) * 32; base < R.n_paths; base += (int64_t)gridDim.x * 128) {
+        const int64_t p = base + lane;
+        const int32_t pix = p < R.n_paths ? path_pixel(R, p) : -1;
+        const bool act0 = pix >= 0;
+        float3 o = make_float3(0.0f, 0.0f, 0.0f), d = make_float3(0.0f, 0.0f, 1.0f);
+        if (act0) {
+            float jx = 0.5f, jy = 0.5f;
+            if (R.jitter) {
+                uint4 b = stream_block(R.seed, (uint32_t)pix, (uint32_t)sample, 0, ST_CAM, 0);
+                jx = u01(b.x); jy = u01(b.y);
+            }
+            camera_ray(R.cam, pix % R.cam.W, pix / R.cam.W, jx, jy, o, d);
+            ++nray;
+            if (COUNT) ++wk.paths;
+        }
+        const RayDev r = make_ray(o, d, 0.0f, INFINITY);
+        float tlo = 0.0f, thi = 0.0f;
+        const bool act = act0 && R.n_nodes > 0 && slab_range(r, R.root_lo, R.root_hi, 0.0f, INFINITY, tlo, thi);
+        const float dfw = fmaf(d.x, R.cb[6], fmaf(d.y, R.cb[7], d.z * R.cb[8]));
+        const float pa = fmaf(d.x, R.cb[0], fmaf(d.y, R.cb[1], d.z * R.cb[2])) / dfw;
+        const float pb = fmaf(d.x, R.cb[3], fmaf(d.y, R.cb[4], d.z * R.cb[5])) / dfw;
+        const float qlo = tlo * dfw, qhi = thi * dfw;
+        auto boxhit = [&](float4 lo, float4 hi) {
+            return lo.x <= pa && pa <= hi.x && lo.y <= pb && pb <= hi.y && hi.z >= qlo && lo.z <= qhi;
+        };
+        double tau = 0.0;
+        auto leaf = [&](uint32_t info, bool mine) {
+            const uint32_t first = info >> 8, cnt = (info >> 5) & 7u;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const GPrim* pp = R.cprims + first + k;
+                GPrim P;
+                P.a = __ldg(&pp->a);
+                bool pass = false;
+                if (mine) {
+                    if (COUNT) ++wk.tests;
+                    pass = sphere_pretest(P.a, r, tlo, thi);
+                }
+                if (!__any_sync(FULL, pass)) continue;
+                P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                Setup s;
+                if (pass && prim_setup(P, r, tlo, thi, s)) {
+                    if (COUNT) ++wk.hits;
+                    tau += (double)(P.d.w * s.ij * seg_J(s, s.u0, s.u1, wk));
+                }
+            }
+        };
+        if (__any_sync(FULL, act)) {
+            int ns = 0;
+            const float4 lo = __ldg(&R.cnodes[0].lo), hi = __ldg(&R.cnodes[0].hi);
+            const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+            if (COUNT && act) ++wk.nodes;
+            const bool hr = act && (node_mask(sk, info) & mask) && boxhit(lo, hi);
+            if (__any_sync(FULL, hr)) {
+                if (sk & kLeafBit) leaf(info, hr);
+                else { stk[0] = 0; ns = 1; }
+            }
+            while (ns > 0) {
+                const uint32_t i = stk[--ns];
+                const GNode2* q = R.cnodes2 + i;
+                const float4 lo0 = __ldg(&q->lo0), hi0 = __ldg(&q->hi0), lo1 = __ldg(&q->lo1), hi1 = __ldg(&q->hi1);
+                const uint32_t ref0 = __float_as_uint(lo0.w), inf0 = __float_as_uint(hi0.w);
+                const uint32_t ref1 = __float_as_uint(lo1.w), inf1 = __float_as_uint(hi1.w);
+                if (COUNT && act) wk.nodes += 2;
+                const bool h0 = act && (node_mask(ref0, inf0) & mask) && boxhit(lo0, hi0);
+                const bool h1 = act && (node_mask(ref1, inf1) & mask) && boxhit(lo1, hi1);
+                const bool a0 = __any_sync(FULL, h0), a1 = __any_sync(FULL, h1);
+                if (a1) {
+                    if (ref1 & kLeafBit) leaf(inf1, h1);
+                    else stk[ns++] = ref1;
+                }
+                if (a0) {
+                    if (ref0 & kLeafBit) leaf(inf0, h0);
+                    else stk[ns++] = ref0;
+                }
+                __syncwarp();
+            }
+        }
+        if (act0) R.L[p] = (float)tau;
+        __syncwarp();
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) nray += __shfl_xor_sync(FULL, nray, off);
+    if (lane == 0 && nray) atomicAdd(R.rays + 0, (unsigned long long)nray);
+    if (COUNT) flush_work(R.work + kWorkSlots * STAGE_TOMO, wk);
+}
+
 __global__ void k_rotate(uint32_t* qc) {
     qc[0] = qc[2];
     qc[1] = 0; qc[2] = 0;
@@ -1582,7 +1680,11 @@ cudaError_t gf_launch_render_pass(RenderDev& R, int32_t sample, int32_t slot, cu
     if (R.mode == 0) {
         T.pre(STAGE_TOMO, st, ev);
 #define GF_TOMO(S_, C_, F_) k_tomo_w<S_, C_, F_><<<wgrid, 128, 0, st>>>(R, sample)
-        if (R.fov) {
+        if (R.camb && !stoch_ext && !R.fov && GF_PACKET && R.n_paths >= R.tomo_pkt_min) {  // coherent camera rays: packets
+            const unsigned tg = (unsigned)std::min<int64_t>((int64_t)persist_blocks(), (R.n_paths + 127) / 128);
+            if (cnt) k_tomo_pkt<true><<<tg, 128, 0, st>>>(R, sample);
+            else k_tomo_pkt<false><<<tg, 128, 0, st>>>(R, sample);
+        } else if (R.fov) {
             if (stoch_ext) { if (cnt) GF_TOMO(true, true, true); else GF_TOMO(true, false, true); }
             else { if (cnt) GF_TOMO(false, true, true); else GF_TOMO(false, false, true); }
         } else {

@@ -236,6 +236,48 @@ def test_render_tomography_cfg1_full_image(gfm, orc):
     assert int(rc[0]) == 64 * 64
 
 
+@pytest.mark.parametrize("wh", [(37, 29), (64, 64)])
+def test_render_tomography_packets_forced(gfm, orc, monkeypatch, wh):
+    """k_tomo_pkt (camera-BVH packets, lane-local integrals) forced on small images, a ragged
+    37x29 one included (last packet partly empty): every pixel against the oracle."""
+    monkeypatch.setenv("GF_DEBUG_TOMO_PKT_MIN", "0")
+    sc = I.scene_cfg1()
+    W, H = wh
+    desc = I.render_desc_cfg1(W, H)
+    f = field(gfm, sc)
+    acc, rc = f.render(desc)
+    acc = acc.view(-1, 2).cpu().numpy()
+    S = orc.Scene(sc)
+    vals, _ = S.render_probes(desc, np.arange(W * H), 0, 1)
+    r = S.trace(camera_rays(desc))
+    assert_tau_parity(acc[:, 0], vals[:, 0], r["A"], None, f"packet tomo {wh}")
+    assert int(rc[0]) == W * H
+    # incoherent packets (random probe pixels) and an empty mask
+    probes = np.random.default_rng(9).integers(0, W * H, 77).astype(np.int32)
+    vg, _ = f.render(desc, probes=probes)
+    assert_tau_parity(vg.cpu().numpy().reshape(-1), vals[probes, 0], r["A"][probes], None, "packet tomo probes")
+    acc0, _ = f.render(dict(desc, ext=I.policy(static_mask=0)))
+    assert np.all(acc0.view(-1, 2).cpu().numpy()[:, 0] == 0.0)
+
+
+def test_render_tomography_cfg2_full_size_sampled(gfm, orc):
+    """The bench's --tomography variant of config 2 (1024x1024, jittered, 4 LOD masks) in its launch
+    configuration (k_tomo_pkt): 256 sampled pixels per mask against the oracle."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    S = orc.Scene(sc)
+    rng = np.random.default_rng(10)
+    for i in range(4):
+        desc = dict(I.render_desc_cfg2(i), mode=0, max_depth=1)
+        acc, rc = f.render(desc)
+        acc = acc.view(-1, 2).cpu().numpy()
+        assert int(rc[0]) == 1024 * 1024
+        pix = rng.integers(0, 1024 * 1024, 256).astype(np.int32)
+        vo, _ = S.render_probes(desc, pix, 0, 1)
+        d = np.abs(acc[pix, 0] - vo[:, 0])
+        assert np.all(d <= 1e-4 * np.maximum(1.0, np.abs(vo[:, 0]))), (i, d.max())
+
+
 def _probe_compare(gfm, orc, sc, desc, probes, spp, what, frac_tol=0.02, f0=None):
     f = field(gfm, sc, group_f0=f0)
     if f0 is not None:
