@@ -69,6 +69,7 @@ def lib():
         L.or_prim_integral_infinite.argtypes = [vp, i32, vp, vp]
         L.or_trace.argtypes = [vp, vp, i64, u32, vp, vp, vp, vp, vp, i32]
         L.or_grad_alpha.argtypes = [vp, vp, i64, u32, vp, vp, vp]
+        L.or_grad_params.argtypes = [vp, vp, vp, i64, u32, vp, vp, vp, vp, i32]
         L.or_candidates.restype = i32
         L.or_candidates.argtypes = [vp, vp, u32, vp, i32, vp]
         L.or_pair_r2_rel.restype = dbl
@@ -174,6 +175,23 @@ class Scene:
         w = _f32(weights)
         lib().or_grad_alpha(self.h, _p(rays), rays.shape[0], mask & 0xFFFFFFFF, _p(w), _p(dl), _p(g))
         return g
+
+    def grad_params(self, rays, dl_dtau, mask=0xFFFFFFFF, weights=None, nthreads=None):
+        """d(sum_r dl[r] tau_r)/d theta_i, theta = (mu[3], q[4], s[3], omega, alpha) per primitive
+        (input order), by Richardson central differences of the closed form (or_grad_params).
+        Returns (grad, gabs): n x 12 each, gabs the sum of |per-ray terms| (a tolerance scale)."""
+        rays = _f32(rays).reshape(-1, 8)
+        dl = np.ascontiguousarray(dl_dtau, np.float64)
+        k = self._keep
+        theta = np.ascontiguousarray(np.concatenate(
+            [k[0].reshape(-1, 3), k[1].reshape(-1, 4), k[2].reshape(-1, 3), k[4].reshape(-1, 1),
+             k[3].reshape(-1, 1)], axis=1), np.float32)
+        g = np.zeros((self.n, 12), np.float64)
+        ga = np.zeros((self.n, 12), np.float64)
+        w = _f32(weights)
+        lib().or_grad_params(self.h, _p(theta), _p(rays), rays.shape[0], mask & 0xFFFFFFFF, _p(w), _p(dl), _p(g),
+                             _p(ga), nthreads or default_threads())
+        return g, ga
 
     def candidates(self, ray, mask=0xFFFFFFFF):
         ray = _f32(ray).reshape(8)

@@ -691,3 +691,105 @@ def test_grad_alpha_matches_finite_differences(orc):
         d = (orc.Scene(sc2).trace(rays)["tau"] - base) @ dl / float(sc["alpha"][i])
         assert abs(d - g[i]) <= 1e-9 * (1 + abs(g[i])), (i, d, g[i])
     assert np.count_nonzero(g) > 10
+
+
+# ---------------------------------------------------------------- parameter gradient (§8(f) rank 4)
+def _R_of_q(q):
+    """rotation matrix of the quaternion (x, y, z, w), normalised; complex-safe (complex-step pins)."""
+    x, y, z, w = q / np.sqrt(np.sum(q * q))
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def _tau_full_line(th, o, v):
+    """App. A boxed infinite-limit integral times alpha, written out here:
+    alpha (8 pi^3 |S|)^-1/2 sqrt(2 pi / a) e^{-(gamma - beta^2/a)/2} e^{-B^2/2a} cos(delta - beta B / a)."""
+    mu, q, s, om, al = th[0:3], th[3:7], th[7:10], th[10], th[11]
+    R = _R_of_q(q)
+    Si = R @ np.diag(1.0 / s ** 2) @ R.T
+    wv = R @ (om / s)
+    d = o - mu
+    a, b, g = v @ Si @ v, v @ Si @ d, d @ Si @ d
+    B, dl = wv @ v, wv @ d
+    norm = 1.0 / np.sqrt(8 * np.pi ** 3 * np.prod(s) ** 2)
+    return al * norm * np.sqrt(2 * np.pi / a) * np.exp(-0.5 * (g - b * b / a)) * np.exp(-B * B / (2 * a)) * \
+        np.cos(dl - b * B / a)
+
+
+def _one_prim_scene(th, E):
+    return make_scene([(th[0:3], th[3:7], th[7:10], th[10], th[11], E)])
+
+
+@pytest.mark.parametrize("omega", [0.0, 0.8])
+def test_grad_params_full_line_complex_step(orc, omega):
+    """d tau / d(mu, q, s, omega, alpha) of one primitive whose truncation is negligible (E = 6:
+    e^{-18}) on a ray covering its whole chord, against the complex-step derivative (exact to
+    rounding) of the full-line closed form written out above -- pins the oracle's finite
+    differences, its parameter order and its q/s/omega chain (a transposed R or a wrong s power
+    fails)."""
+    rng = np.random.default_rng(11)
+    for trial in range(4):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        th = np.concatenate([rng.uniform(-0.3, 0.3, 3), q, rng.uniform(0.15, 0.35, 3), [omega], [0.7]])
+        th = th.astype(np.float32).astype(np.float64)
+        o = np.array([-2.0, rng.uniform(-0.1, 0.1), rng.uniform(-0.1, 0.1)])
+        v = np.array([1.0, 0.1 * rng.normal(), 0.1 * rng.normal()])
+        v /= np.linalg.norm(v)
+        ray = np.array([*o, -20.0, *v, 20.0], np.float32)
+        o, v = ray[0:3].astype(np.float64), ray[4:7].astype(np.float64)
+        S = orc.Scene(_one_prim_scene(th, 6.0))
+        g, _ = S.grad_params(ray[None, :], np.array([1.0]))
+        ref = np.array([(_tau_full_line(th + 1e-30j * np.eye(12)[k], o, v)).imag / 1e-30 for k in range(12)])
+        scale = np.abs(ref).max()
+        assert np.all(np.abs(g[0] - ref) <= 1e-6 * scale), (trial, g[0], ref)
+        # alpha enters linearly; q's norm does not matter (gradient orthogonal to q)
+        assert abs(g[0, 11] * th[11] - _tau_full_line(th, o, v)) <= 1e-7 * abs(g[0, 11] * th[11]) + 1e-12
+        assert abs(g[0, 3:7] @ th[3:7]) <= 1e-6 * scale
+
+
+def test_grad_params_truncated_leibniz(orc):
+    """Truncated kernel (E = 3, C7), chord strictly inside the ray's range: d tau / d mu and d tau /
+    d omega by Leibniz's rule written out here -- adaptive quadrature (scipy) of dg/dmu, dg/domega
+    of Eq. 6 along the chord plus the moving-endpoint terms g(x_e) dt_e/dmu, dt_e/dmu =
+    S^-1 d_e / (v . S^-1 d_e) -- against the oracle's finite differences; and the translation
+    invariance v . d tau / d mu = 0."""
+    from scipy import integrate
+    rng = np.random.default_rng(12)
+    for trial in range(4):
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        th = np.concatenate([rng.uniform(-0.2, 0.2, 3), q, rng.uniform(0.15, 0.35, 3), [1.1], [0.9]])
+        th = th.astype(np.float32).astype(np.float64)
+        ray = np.array([-2.0, 0.05 * rng.normal(), 0.05 * rng.normal(), 0.0, 1.0, 0.0, 0.0, 10.0], np.float32)
+        o, v = ray[0:3].astype(np.float64), ray[4:7].astype(np.float64)
+        S = orc.Scene(_one_prim_scene(th, 3.0))
+        g, _ = S.grad_params(ray[None, :], np.array([1.0]))
+        mu, R, s, om, al = th[0:3], _R_of_q(th[3:7]), th[7:10], th[10], th[11]
+        Si = R @ np.diag(1.0 / s ** 2) @ R.T
+        wv = R @ (om / s)
+        norm = 1.0 / np.sqrt(8 * np.pi ** 3 * np.prod(s) ** 2)
+        d0 = o - mu
+        a, b, c = v @ Si @ v, v @ Si @ d0, d0 @ Si @ d0 - 9.0
+        disc = b * b - a * c
+        assert disc > 0.05 * b * b
+        t0, t1 = (-b - np.sqrt(disc)) / a, (-b + np.sqrt(disc)) / a
+
+        def gk(t):
+            d = o + t * v - mu
+            return norm * np.exp(-0.5 * d @ Si @ d), d
+
+        dmu = np.zeros(3)
+        for k in range(3):
+            f = lambda t: (lambda e, d: e * ((Si @ d)[k] * np.cos(wv @ d) + wv[k] * np.sin(wv @ d)))(*gk(t))
+            dmu[k] = al * integrate.quad(f, t0, t1, epsabs=1e-13, epsrel=1e-10, limit=200)[0]
+        for te, sgn in ((t1, 1.0), (t0, -1.0)):
+            e, d = gk(te)
+            dmu += sgn * al * e * np.cos(wv @ d) * (Si @ d) / (v @ Si @ d)
+        fo = lambda t: (lambda e, d: -e * np.sin(wv @ d) * (wv @ d) / om)(*gk(t))
+        dom = al * integrate.quad(fo, t0, t1, epsabs=1e-13, epsrel=1e-10, limit=200)[0]
+        scale = np.abs(dmu).max()
+        assert np.all(np.abs(g[0, 0:3] - dmu) <= 1e-6 * scale), (trial, g[0, 0:3], dmu)
+        assert abs(g[0, 10] - dom) <= 1e-6 * max(abs(dom), scale), (trial, g[0, 10], dom)
+        assert abs(g[0, 0:3] @ v) <= 1e-6 * scale
