@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 5
+#define GF_ABI_VERSION 6
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -170,6 +170,27 @@ gf_status gf_trace_transmittance_ex(gf_ctx *ctx, const float *rays, int64_t n, u
  * device n fp32; grad_alpha: device n_prims fp32 in input order, accumulated (caller zeroes). */
 gf_status gf_trace_grad_alpha(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, const float *dl_dtau,
                               float *grad_alpha, gf_stream stream);
+
+/* Backward of the optical depth w.r.t. every primitive parameter (SURVEY §8(f) rank 4:
+ * d tau / d(mu, q, s, alpha, omega)), in two calls.
+ *
+ * gf_trace_grad_params accumulates, per primitive, the derivative of sum_r dl_dtau[r] tau_r
+ * w.r.t. the primitive's mean, whitening matrix W = S^-1 R^T, omega and alpha,
+ * each hit in closed form (the App. A moments J0..J2 by integration by parts, plus the terms of the
+ * chord ends that move with the ellipsoid, C7) -- rays, policy and draws as
+ * gf_trace_transmittance.  accum: device n_prims x 16 fp32, input order, caller-zeroed,
+ * accumulated across calls: [0..2] d/dmu, [3..11] d/dW (row-major), [12] d/domega, [13] d/dalpha,
+ * [14] sum dl tau_ri (the |det W| part), [15] unused.
+ *
+ * gf_grad_params_finish converts accum to the load parameters by the chain rule through
+ * W = S^-1 R(q / |q|)^T and |det W| = 1/(s_x s_y s_z): grad: device n_prims x 12 fp32
+ * (mu_x, mu_y, mu_z, q_x, q_y, q_z, q_w, s_x, s_y, s_z, omega, alpha), overwritten.  quat: the
+ * device n_prims x 4 quaternion array given to gf_load_primitives (16-byte aligned).
+ * tau is not differentiable where a chord appears or vanishes (grazing rays, r2 = E^2): the
+ * moving-end terms grow like 1/h there. */
+gf_status gf_trace_grad_params(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, const float *dl_dtau,
+                               float *accum, gf_stream stream);
+gf_status gf_grad_params_finish(gf_ctx *ctx, const float *accum, const float *quat, float *grad, gf_stream stream);
 
 /* Candidate sets (test path, C21): for each ray, the ORIGINAL indices of the
  * primitives accepted by the fp32 ellipsoid predicate (traversal order),

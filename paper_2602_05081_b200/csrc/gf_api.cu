@@ -399,6 +399,27 @@ gf_status gf_trace_grad_alpha(gf_ctx* c, const float* rays, int64_t n, uint64_t 
     return GF_OK;
 }
 
+gf_status gf_trace_grad_params(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, const float* dl_dtau,
+                               float* accum, gf_stream stream) {
+    TraceArgs A;
+    if (gf_status s = trace_common(c, rays, n, A, 0u)) return s;
+    if (!c->built) return fail(c, GF_E_STATE, "gf_trace_grad_params before gf_build_bvh");
+    if (n > 0 && (!dl_dtau || !accum)) return fail(c, GF_E_INVALID_ARGUMENT, "null gradient buffers");
+    A.seed = seed;
+    GF_CUDA(c, gf_launch_grad_params(A, dl_dtau, accum, (cudaStream_t)stream), "k_grad_params");
+    return GF_OK;
+}
+
+gf_status gf_grad_params_finish(gf_ctx* c, const float* accum, const float* quat, float* grad, gf_stream stream) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (!c->loaded) return fail(c, GF_E_STATE, "gf_grad_params_finish before gf_load_primitives");
+    if (c->n > 0 && (!accum || !quat || !grad)) return fail(c, GF_E_INVALID_ARGUMENT, "null gradient buffers");
+    if (((uintptr_t)quat & 15u) != 0) return fail(c, GF_E_INVALID_ARGUMENT, "quat must be 16-byte aligned");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    GF_CUDA(c, gf_launch_grad_finish(c->prims, c->n, accum, quat, grad, (cudaStream_t)stream), "k_grad_finish");
+    return GF_OK;
+}
+
 gf_status gf_trace_candidates(gf_ctx* c, const float* rays, int64_t n, uint32_t flags, int32_t* ids,
                               int32_t capacity, int32_t* count, gf_stream stream) {
     TraceArgs A;

@@ -179,6 +179,210 @@ __global__ void __launch_bounds__(128) k_grad_alpha(TraceArgs A, const float* __
     }
 }
 
+// ---------------------------------------------------------------- parameter gradient (§8(f) rank 4)
+// Complex segment moment  J0 = e^{-r2/2} (2 pi)^-1/2 int_ua^ub e^{-u^2/2} e^{i (phi0 + Om u)} du
+// (Re J0 = seg_J).  Series: 1/2 e^{-(r2+Om^2)/2} e^{i phi0} [F(ub) - F(ua)]; same midpoint and
+// Gauss-Legendre special cases as seg_J.
+__device__ inline float2 seg_J0c(const Setup& s, float ua, float ub, Work& wk) {
+    const float L = ub - ua;
+    if (L < 1e-4f) {
+        const float um = 0.5f * (ua + ub);
+        float sp, cp;
+        sincos_red(fmaf(s.Om, um, s.phi0), &sp, &cp);
+        const float e = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + um * um)) * L;
+        return make_float2(e * cp, e * sp);
+    }
+    const float wmax = 0.5f * (fmaxf(ua * ua, ub * ub) + s.Om * s.Om);
+    if (wmax > kWMaxSeries && s.Om != 0.0f) {
+        ++wk.gl;
+        const float hm = 0.5f * L, c = 0.5f * (ua + ub);
+        float ar = 0.0f, ai = 0.0f;
+        for (int k = 0; k < 12; ++k) {
+            const float x = hm * kGLx[k];
+            float s1, c1, s2, c2;
+            sincos_red(fmaf(s.Om, c + x, s.phi0), &s1, &c1);
+            sincos_red(fmaf(s.Om, c - x, s.phi0), &s2, &c2);
+            const float e1 = __expf(-0.5f * (c + x) * (c + x)), e2 = __expf(-0.5f * (c - x) * (c - x));
+            ar = fmaf(kGLw[k], e1 * c1 + e2 * c2, ar);
+            ai = fmaf(kGLw[k], e1 * s1 + e2 * s2, ai);
+        }
+        const float f = kInvSqrt2Pi * __expf(-0.5f * s.r2) * hm;
+        return make_float2(f * ar, f * ai);
+    }
+    float sp, cp;
+    sincos_red(s.phi0, &sp, &cp);
+    const float amp = 0.5f * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+    wk.erf(s.Om, 2);
+    const float2 Fb = erf_shift(ub, s.Om), Fa = erf_shift(ua, s.Om);
+    const float dr = Fb.x - Fa.x, di = Fb.y - Fa.y;
+    return make_float2(amp * fmaf(cp, dr, -sp * di), amp * fmaf(cp, di, sp * dr));
+}
+
+// Per-hit derivatives of tau_ri = c int_chord K(y(t)) dt, K(y) = (2 pi)^-1/2 e^{-|y|^2/2} cos(k.y),
+// y = W (x - mu), k = omega (1,1,1), c = alpha (2 pi)^-1 |det W|.  With the whitened
+// arc parameter u (y = cvec + u v) and the moments Jn = e^{-r2/2} (2 pi)^-1/2 int u^n e^{-u^2/2 + i phi(u)}:
+//   J1 = i Om J0 - [E],  J2 = i Om J1 - [u E] + J0   (integration by parts), E(u) the integrand;
+//   d tau/d mu    = c [ ij W^T A + sum_e K(y_e) ij/h W^T y_e ]
+//   d tau/d W     = c [ -ij (A D^T + ij B d^T) - sum_e K(y_e) ij/h y_e X_e^T ]   (|det W| part: finish)
+//   d tau/d omega = -c ij [ (1.cvec) Im J0 + (1.v) Im J1 ]
+//   A = cvec Re J0 + v Re J1 + k Im J0,  B = cvec Re(J1 - bp J0) + v Re(J2 - bp J1) + k Im(J1 - bp J0)
+// where D = o + tc d - mu, X_e = D + (u_e - bp) ij d, and e runs over chord ends on the ellipsoid
+// (u = +-h: the end moves with mu and W; a clipped end at tmin/tmax does not).
+// acc (16 floats per primitive, input order): mu[3], W[9] row-major, omega, alpha, sum l tau, -.
+template <bool STOCH>
+__global__ void __launch_bounds__(128) k_grad_params(TraceArgs A, const float* __restrict__ dl,
+                                                     float* __restrict__ acc) {
+    __shared__ WarpTrav s_t[4];
+    const int wid = threadIdx.x >> 5;
+    Work wk;
+    for (int64_t i = (int64_t)blockIdx.x * 4 + wid; i < A.n; i += (int64_t)gridDim.x * 4) {
+        const float4 r0 = __ldg((const float4*)A.rays + 2 * i);
+        const float4 r1 = __ldg((const float4*)A.rays + 2 * i + 1);
+        const float3 o = make_float3(r0.x, r0.y, r0.z), d = make_float3(r1.x, r1.y, r1.z);
+        const RayDev r = make_ray(o, d, r0.w, r1.w);
+        float w[kMaxGroups];
+        uint32_t mask;
+        if (STOCH) mask = policy_for(A.pol, A.sc, d, A.seed, (uint32_t)i, 0, 0, ST_EXT, 1, w);
+        else mask = A.pol.static_mask;
+        const float g = __ldg(dl + i);
+        if (g == 0.0f) continue;
+        warp_traverse<false>(A.nodes, A.nodes2, A.n_nodes, A.stk_limit, r, r.tmin, r.tmax, mask, s_t[wid], wk,
+                             [&](bool valid, uint32_t ref) {
+            if (!valid) return;
+            const uint32_t k = ref & kRefIdx;
+            const GPrim* pp = A.prims + k;
+            GPrim P;
+            P.a = __ldg(&pp->a);
+            if (!sphere_pretest(P.a, r, r.tmin, r.tmax)) return;
+            P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+            Setup s;
+            if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
+            const float l = STOCH ? g * w[ref >> 27] : g;
+            // world offset at the re-centring point (TwoSum as prim_setup) and whitened vectors
+            const float hx = __fsub_rn(o.x, P.a.x), hy = __fsub_rn(o.y, P.a.y), hz = __fsub_rn(o.z, P.a.z);
+            const float bx = __fsub_rn(hx, o.x), by = __fsub_rn(hy, o.y), bz = __fsub_rn(hz, o.z);
+            const float lx = __fadd_rn(__fsub_rn(o.x, __fsub_rn(hx, bx)), __fsub_rn(-P.a.x, bx));
+            const float ly = __fadd_rn(__fsub_rn(o.y, __fsub_rn(hy, by)), __fsub_rn(-P.a.y, by));
+            const float lz = __fadd_rn(__fsub_rn(o.z, __fsub_rn(hz, bz)), __fsub_rn(-P.a.z, bz));
+            const float D[3] = {__fadd_rn(__fmaf_rn(s.tc, d.x, hx), lx), __fadd_rn(__fmaf_rn(s.tc, d.y, hy), ly),
+                                __fadd_rn(__fmaf_rn(s.tc, d.z, hz), lz)};
+            const float dv[3] = {d.x, d.y, d.z};
+            const float Wm[3][3] = {{P.b.x, P.b.y, P.b.z}, {P.c.x, P.c.y, P.c.z}, {P.d.x, P.d.y, P.d.z}};
+            float pv[3], vv[3], cv[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                pv[a] = fmaf(Wm[a][0], D[0], fmaf(Wm[a][1], D[1], Wm[a][2] * D[2]));
+                vv[a] = fmaf(Wm[a][0], dv[0], fmaf(Wm[a][1], dv[1], Wm[a][2] * dv[2])) * s.ij;
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) cv[a] = fmaf(-s.bp, vv[a], pv[a]);
+            const float om = P.b.w, cst = P.d.w;
+            const float2 J0 = seg_J0c(s, s.u0, s.u1, wk);
+            float E0r, E0i, E1r, E1i;
+            {
+                float sp, cp;
+                sincos_red(fmaf(s.Om, s.u0, s.phi0), &sp, &cp);
+                const float e0 = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + s.u0 * s.u0));
+                E0r = e0 * cp; E0i = e0 * sp;
+                sincos_red(fmaf(s.Om, s.u1, s.phi0), &sp, &cp);
+                const float e1 = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + s.u1 * s.u1));
+                E1r = e1 * cp; E1i = e1 * sp;
+            }
+            const float J1r = -s.Om * J0.y - (E1r - E0r), J1i = s.Om * J0.x - (E1i - E0i);
+            const float J2r = -s.Om * J1i - (s.u1 * E1r - s.u0 * E0r) + J0.x;
+            const float Kr = J1r - s.bp * J0.x, Ki = J1i - s.bp * J0.y, Lr = J2r - s.bp * J1r;
+            float Av[3], Bv[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                Av[a] = fmaf(cv[a], J0.x, fmaf(vv[a], J1r, om * J0.y));
+                Bv[a] = fmaf(cv[a], Kr, fmaf(vv[a], Lr, om * Ki));
+            }
+            const float lc = l * cst, ij = s.ij;
+            float gmu[3], gW[3][3];
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                gmu[b] = ij * fmaf(Wm[0][b], Av[0], fmaf(Wm[1][b], Av[1], Wm[2][b] * Av[2]));
+#pragma unroll
+                for (int a = 0; a < 3; ++a) gW[a][b] = -ij * fmaf(Av[a], D[b], ij * Bv[a] * dv[b]);
+            }
+            // moving chord ends on the ellipsoid
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float ue = e ? s.u1 : s.u0;
+                if (ue != (e ? s.h : -s.h)) continue;
+                const float Ke = (e ? E1r : E0r) * ij / s.h;
+                float ye[3], Xe[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    ye[a] = fmaf(ue, vv[a], cv[a]);
+                    Xe[a] = fmaf((ue - s.bp) * ij, dv[a], D[a]);
+                }
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    gmu[b] = fmaf(Ke, fmaf(Wm[0][b], ye[0], fmaf(Wm[1][b], ye[1], Wm[2][b] * ye[2])), gmu[b]);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) gW[a][b] = fmaf(-Ke * ye[a], Xe[b], gW[a][b]);
+                }
+            }
+            const float gom = -ij * fmaf(cv[0] + cv[1] + cv[2], J0.y, (vv[0] + vv[1] + vv[2]) * J1i);
+            const float nb = sqrtf(P.b.x * P.b.x + P.b.y * P.b.y + P.b.z * P.b.z);
+            const float nc = sqrtf(P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
+            const float nd = sqrtf(P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
+            float* out = acc + (size_t)A.perm[k] * 16;
+#pragma unroll
+            for (int b = 0; b < 3; ++b) atomicAdd(out + b, lc * gmu[b]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) atomicAdd(out + 3 + 3 * a + b, lc * gW[a][b]);
+            atomicAdd(out + 12, lc * gom);
+            atomicAdd(out + 13, l * nb * nc * nd * 0.15915494309189535f * ij * J0.x);
+            atomicAdd(out + 14, lc * ij * J0.x);
+        });
+    }
+}
+
+// Chain rule to the load parameters (input order): W = S^-1 R^T (rows R_.k / s_k), |det W| = 1/(s1 s2 s3):
+//   d/ds_k = -(1/s_k) [ sum l tau + sum_b dW_kb W_kb ],  d/dR_bk = dW_kb / s_k,
+//   d/dq = (I - qh qh^T)/|q| J_R(qh)^T d/dR   (R(qh) of the unit quaternion (x, y, z, w)).
+__global__ void k_grad_finish(const GPrim* __restrict__ prims, int64_t n, const float* __restrict__ acc,
+                              const float* __restrict__ quat, float* __restrict__ grad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const GPrim P = prims[i];
+    const float* a = acc + i * 16;
+    const float Wm[3][3] = {{P.b.x, P.b.y, P.b.z}, {P.c.x, P.c.y, P.c.z}, {P.d.x, P.d.y, P.d.z}};
+    float gR[3][3], gs[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float sk = rsqrtf(Wm[k][0] * Wm[k][0] + Wm[k][1] * Wm[k][1] + Wm[k][2] * Wm[k][2]);
+        float dot = 0.0f;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            dot = fmaf(a[3 + 3 * k + b], Wm[k][b], dot);
+            gR[b][k] = a[3 + 3 * k + b] / sk;
+        }
+        gs[k] = -(a[14] + dot) / sk;
+    }
+    const float4 q = __ldg((const float4*)quat + i);
+    const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    const float x = q.x / qn, y = q.y / qn, z = q.z / qn, w = q.w / qn;
+    // d tau / d (x, y, z, w) of the unit quaternion through R (row-major entries R_rc)
+    const float gx = 2.0f * (y * (gR[0][1] + gR[1][0]) + z * (gR[0][2] + gR[2][0]) + w * (gR[2][1] - gR[1][2])) -
+                     4.0f * x * (gR[1][1] + gR[2][2]);
+    const float gy = 2.0f * (x * (gR[0][1] + gR[1][0]) + w * (gR[0][2] - gR[2][0]) + z * (gR[1][2] + gR[2][1])) -
+                     4.0f * y * (gR[0][0] + gR[2][2]);
+    const float gz = 2.0f * (w * (gR[1][0] - gR[0][1]) + x * (gR[0][2] + gR[2][0]) + y * (gR[1][2] + gR[2][1])) -
+                     4.0f * z * (gR[0][0] + gR[1][1]);
+    const float gw = 2.0f * (z * (gR[1][0] - gR[0][1]) + y * (gR[0][2] - gR[2][0]) + x * (gR[2][1] - gR[1][2]));
+    const float pr = x * gx + y * gy + z * gz + w * gw;
+    float* o = grad + i * 12;
+    o[0] = a[0]; o[1] = a[1]; o[2] = a[2];
+    o[3] = (gx - x * pr) / qn; o[4] = (gy - y * pr) / qn; o[5] = (gz - z * pr) / qn; o[6] = (gw - w * pr) / qn;
+    o[7] = gs[0]; o[8] = gs[1]; o[9] = gs[2];
+    o[10] = a[12]; o[11] = a[13];
+}
+
 template <bool BRUTE>
 __global__ void __launch_bounds__(128) k_candidates(TraceArgs A) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -242,6 +446,24 @@ cudaError_t gf_launch_grad_alpha(const TraceArgs& A, const float* dl, float* gra
     const unsigned wgrid = (unsigned)std::min<int64_t>((A.n + 3) / 4, (int64_t)sms * 16);
     if (!(A.pol.ls == 0 && A.pol.os == 0)) k_grad_alpha<true><<<wgrid, 128, 0, st>>>(A, dl, grad);
     else k_grad_alpha<false><<<wgrid, 128, 0, st>>>(A, dl, grad);
+    return cudaGetLastError();
+}
+
+cudaError_t gf_launch_grad_params(const TraceArgs& A, const float* dl, float* acc, cudaStream_t st) {
+    if (A.n == 0 || A.n_nodes == 0) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned wgrid = (unsigned)std::min<int64_t>((A.n + 3) / 4, (int64_t)sms * 16);
+    if (!(A.pol.ls == 0 && A.pol.os == 0)) k_grad_params<true><<<wgrid, 128, 0, st>>>(A, dl, acc);
+    else k_grad_params<false><<<wgrid, 128, 0, st>>>(A, dl, acc);
+    return cudaGetLastError();
+}
+
+cudaError_t gf_launch_grad_finish(const GPrim* prims, int64_t n, const float* acc, const float* quat, float* grad,
+                                  cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_grad_finish<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(prims, n, acc, quat, grad);
     return cudaGetLastError();
 }
 

@@ -98,6 +98,8 @@ def lib():
     L.gf_trace_transmittance_ex.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp, vp]
     L.gf_trace_candidates.argtypes = [vp, vp, i64, u32, vp, i32, vp, vp]
     L.gf_trace_grad_alpha.argtypes = [vp, vp, i64, u64, vp, vp, vp]
+    L.gf_trace_grad_params.argtypes = [vp, vp, i64, u64, vp, vp, vp]
+    L.gf_grad_params_finish.argtypes = [vp, vp, vp, vp, vp]
     L.gf_render_scratch_bytes.argtypes = [vp, ctypes.POINTER(RenderDesc), ctypes.POINTER(sz)]
     L.gf_render.argtypes = [vp, ctypes.POINTER(RenderDesc), vp, vp, sz, vp, vp]
     L.gf_set_profiling.argtypes = [vp, u32]
@@ -186,6 +188,7 @@ class GaborField:
                                               _ptr(self.prim_ws), pb.value, _stream()))
         self._sizes = (bb.value, sb.value)
         self.n, self.P, self.K, self.G = n, P, K, 1 + (P - 1) * K
+        self._quat = arrs["quat"]  # kept for gf_grad_params_finish (the quaternions as loaded)
         return self
 
     def build_bvh(self):
@@ -224,6 +227,22 @@ class GaborField:
         grad = out if out is not None else torch.zeros(self.n, dtype=torch.float32, device=self.device)
         self._check(self.L.gf_trace_grad_alpha(self.ctx, _ptr(rays), rays.shape[0], seed,
                                                _ptr(dl), _ptr(grad), _stream()))
+        return grad
+
+    def trace_grad_params(self, rays, dl_dtau, seed=0, accum=None, finish=True):
+        """d(sum_r dl_dtau[r] tau_r) / d(mu, q, s, omega, alpha): (n_prims, 12) fp32 in input order
+        (gf_trace_grad_params + gf_grad_params_finish).  accum (n_prims, 16) fp32 accumulates across
+        calls when given; finish=False returns it raw."""
+        torch = self.torch
+        rays = torch.as_tensor(rays).to(device=self.device, dtype=torch.float32).contiguous().view(-1, 8)
+        dl = torch.as_tensor(dl_dtau).to(device=self.device, dtype=torch.float32).contiguous()
+        acc = accum if accum is not None else torch.zeros((self.n, 16), dtype=torch.float32, device=self.device)
+        self._check(self.L.gf_trace_grad_params(self.ctx, _ptr(rays), rays.shape[0], seed, _ptr(dl), _ptr(acc),
+                                                _stream()))
+        if not finish:
+            return acc
+        grad = torch.empty((self.n, 12), dtype=torch.float32, device=self.device)
+        self._check(self.L.gf_grad_params_finish(self.ctx, _ptr(acc), _ptr(self._quat), _ptr(grad), _stream()))
         return grad
 
     def trace_candidates(self, rays, capacity=2048, brute_force=False):
