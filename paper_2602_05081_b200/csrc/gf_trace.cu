@@ -328,16 +328,13 @@ __global__ void __launch_bounds__(128) k_grad_params(TraceArgs A, const float* _
             const float nb = sqrtf(P.b.x * P.b.x + P.b.y * P.b.y + P.b.z * P.b.z);
             const float nc = sqrtf(P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
             const float nd = sqrtf(P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
-            float* out = acc + (size_t)A.perm[k] * 16;
-#pragma unroll
-            for (int b = 0; b < 3; ++b) atomicAdd(out + b, lc * gmu[b]);
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b) atomicAdd(out + 3 + 3 * a + b, lc * gW[a][b]);
-            atomicAdd(out + 12, lc * gom);
-            atomicAdd(out + 13, l * nb * nc * nd * 0.15915494309189535f * ij * J0.x);
-            atomicAdd(out + 14, lc * ij * J0.x);
+            // four 16-byte vector atomics per hit (sm_90+ float4 atomicAdd on global memory)
+            float4* out = (float4*)(acc + (size_t)A.perm[k] * 16);
+            atomicAdd(out + 0, make_float4(lc * gmu[0], lc * gmu[1], lc * gmu[2], lc * gW[0][0]));
+            atomicAdd(out + 1, make_float4(lc * gW[0][1], lc * gW[0][2], lc * gW[1][0], lc * gW[1][1]));
+            atomicAdd(out + 2, make_float4(lc * gW[1][2], lc * gW[2][0], lc * gW[2][1], lc * gW[2][2]));
+            atomicAdd(out + 3, make_float4(lc * gom, l * nb * nc * nd * 0.15915494309189535f * ij * J0.x,
+                                           lc * ij * J0.x, 0.0f));
         });
     }
 }
