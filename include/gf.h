@@ -178,7 +178,9 @@ gf_status gf_trace_grad_alpha(gf_ctx *ctx, const float *rays, int64_t n, uint64_
  * w.r.t. the primitive's mean, whitening matrix W = S^-1 R^T, omega and alpha,
  * each hit in closed form (the App. A moments J0..J2 by integration by parts, plus the terms of the
  * chord ends that move with the ellipsoid, C7) -- rays, policy and draws as
- * gf_trace_transmittance.  accum: device n_prims x 16 fp32, input order, caller-zeroed,
+ * gf_trace_transmittance.  flags: 0 (one warp per ray) or GF_TRACE_PACKETS (32 consecutive rays walk
+ * the BVH together and sum each primitive's terms across the warp before one set of atomics: faster
+ * for coherent rays, correct for any; E_INVALID_ARGUMENT for other bits).  accum: device n_prims x 16 fp32, input order, caller-zeroed,
  * accumulated across calls: [0..2] d/dmu, [3..11] d/dW (row-major), [12] d/domega, [13] d/dalpha,
  * [14] sum dl tau_ri (the |det W| part), [15] unused.
  *
@@ -188,8 +190,9 @@ gf_status gf_trace_grad_alpha(gf_ctx *ctx, const float *rays, int64_t n, uint64_
  * device n_prims x 4 quaternion array given to gf_load_primitives (16-byte aligned).
  * tau is not differentiable where a chord appears or vanishes (grazing rays, r2 = E^2): the
  * moving-end terms grow like 1/h there. */
-gf_status gf_trace_grad_params(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, const float *dl_dtau,
-                               float *accum, gf_stream stream);
+#define GF_TRACE_PACKETS 2u  /* rays come in coherent groups of 32 (e.g. 8x4 pixel blocks): packet walk */
+gf_status gf_trace_grad_params(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, uint32_t flags,
+                               const float *dl_dtau, float *accum, gf_stream stream);
 gf_status gf_grad_params_finish(gf_ctx *ctx, const float *accum, const float *quat, float *grad, gf_stream stream);
 
 /* Candidate sets (test path, C21): for each ray, the ORIGINAL indices of the

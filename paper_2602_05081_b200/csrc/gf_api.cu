@@ -399,14 +399,16 @@ gf_status gf_trace_grad_alpha(gf_ctx* c, const float* rays, int64_t n, uint64_t 
     return GF_OK;
 }
 
-gf_status gf_trace_grad_params(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, const float* dl_dtau,
-                               float* accum, gf_stream stream) {
+gf_status gf_trace_grad_params(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, uint32_t flags,
+                               const float* dl_dtau, float* accum, gf_stream stream) {
     TraceArgs A;
+    if (flags & ~GF_TRACE_PACKETS) return fail(c, GF_E_INVALID_ARGUMENT, "bad gf_trace_grad_params flags");
     if (gf_status s = trace_common(c, rays, n, A, 0u)) return s;
     if (!c->built) return fail(c, GF_E_STATE, "gf_trace_grad_params before gf_build_bvh");
     if (n > 0 && (!dl_dtau || !accum)) return fail(c, GF_E_INVALID_ARGUMENT, "null gradient buffers");
     A.seed = seed;
-    GF_CUDA(c, gf_launch_grad_params(A, dl_dtau, accum, (cudaStream_t)stream), "k_grad_params");
+    GF_CUDA(c, gf_launch_grad_params(A, dl_dtau, accum, (flags & GF_TRACE_PACKETS) != 0, (cudaStream_t)stream),
+            "k_grad_params");
     return GF_OK;
 }
 

@@ -147,7 +147,7 @@ cudaError_t gf_launch_build_frame(const void* prims, const uint8_t* group, int64
 cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
 cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
 cudaError_t gf_launch_grad_alpha(const TraceArgs& A, const float* dl, float* grad, cudaStream_t st);
-cudaError_t gf_launch_grad_params(const TraceArgs& A, const float* dl, float* acc, cudaStream_t st);
+cudaError_t gf_launch_grad_params(const TraceArgs& A, const float* dl, float* acc, bool packets, cudaStream_t st);
 cudaError_t gf_launch_grad_finish(const gfk::GPrim* prims, int64_t n, const float* acc, const float* quat, float* grad,
                                   cudaStream_t st);
 size_t gf_render_state_bytes(int64_t n_paths, int64_t n_prims, char* base, RenderDev* R, BuildScratch* light_scratch);

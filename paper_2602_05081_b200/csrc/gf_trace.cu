@@ -229,6 +229,100 @@ __device__ inline float2 seg_J0c(const Setup& s, float ua, float ub, Work& wk) {
 // where D = o + tc d - mu, X_e = D + (u_e - bp) ij d, and e runs over chord ends on the ellipsoid
 // (u = +-h: the end moves with mu and W; a clipped end at tmin/tmax does not).
 // acc (16 floats per primitive, input order): mu[3], W[9] row-major, omega, alpha, sum l tau, -.
+// The 15 partial sums of one hit (layout of acc, entries 0..14), loss weight l applied.
+__device__ __forceinline__ void hit_grad(const GPrim& P, const Setup& s, float3 o, float3 d, float l, float* G,
+                                         Work& wk) {
+    // world offset at the re-centring point (TwoSum as prim_setup) and whitened vectors
+    const float hx = __fsub_rn(o.x, P.a.x), hy = __fsub_rn(o.y, P.a.y), hz = __fsub_rn(o.z, P.a.z);
+    const float bx = __fsub_rn(hx, o.x), by = __fsub_rn(hy, o.y), bz = __fsub_rn(hz, o.z);
+    const float lx = __fadd_rn(__fsub_rn(o.x, __fsub_rn(hx, bx)), __fsub_rn(-P.a.x, bx));
+    const float ly = __fadd_rn(__fsub_rn(o.y, __fsub_rn(hy, by)), __fsub_rn(-P.a.y, by));
+    const float lz = __fadd_rn(__fsub_rn(o.z, __fsub_rn(hz, bz)), __fsub_rn(-P.a.z, bz));
+    const float D[3] = {__fadd_rn(__fmaf_rn(s.tc, d.x, hx), lx), __fadd_rn(__fmaf_rn(s.tc, d.y, hy), ly),
+                        __fadd_rn(__fmaf_rn(s.tc, d.z, hz), lz)};
+    const float dv[3] = {d.x, d.y, d.z};
+    const float Wm[3][3] = {{P.b.x, P.b.y, P.b.z}, {P.c.x, P.c.y, P.c.z}, {P.d.x, P.d.y, P.d.z}};
+    float pv[3], vv[3], cv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        pv[a] = fmaf(Wm[a][0], D[0], fmaf(Wm[a][1], D[1], Wm[a][2] * D[2]));
+        vv[a] = fmaf(Wm[a][0], dv[0], fmaf(Wm[a][1], dv[1], Wm[a][2] * dv[2])) * s.ij;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cv[a] = fmaf(-s.bp, vv[a], pv[a]);
+    const float om = P.b.w, cst = P.d.w;
+    const float2 J0 = seg_J0c(s, s.u0, s.u1, wk);
+    float E0r, E0i, E1r, E1i;
+    {
+        float sp, cp;
+        sincos_red(fmaf(s.Om, s.u0, s.phi0), &sp, &cp);
+        const float e0 = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + s.u0 * s.u0));
+        E0r = e0 * cp; E0i = e0 * sp;
+        sincos_red(fmaf(s.Om, s.u1, s.phi0), &sp, &cp);
+        const float e1 = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + s.u1 * s.u1));
+        E1r = e1 * cp; E1i = e1 * sp;
+    }
+    const float J1r = -s.Om * J0.y - (E1r - E0r), J1i = s.Om * J0.x - (E1i - E0i);
+    const float J2r = -s.Om * J1i - (s.u1 * E1r - s.u0 * E0r) + J0.x;
+    const float Kr = J1r - s.bp * J0.x, Ki = J1i - s.bp * J0.y, Lr = J2r - s.bp * J1r;
+    float Av[3], Bv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        Av[a] = fmaf(cv[a], J0.x, fmaf(vv[a], J1r, om * J0.y));
+        Bv[a] = fmaf(cv[a], Kr, fmaf(vv[a], Lr, om * Ki));
+    }
+    const float ij = s.ij;
+    float gmu[3], gW[3][3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        gmu[b] = ij * fmaf(Wm[0][b], Av[0], fmaf(Wm[1][b], Av[1], Wm[2][b] * Av[2]));
+#pragma unroll
+        for (int a = 0; a < 3; ++a) gW[a][b] = -ij * fmaf(Av[a], D[b], ij * Bv[a] * dv[b]);
+    }
+    // moving chord ends on the ellipsoid
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const float ue = e ? s.u1 : s.u0;
+        if (ue != (e ? s.h : -s.h)) continue;
+        const float Ke = (e ? E1r : E0r) * ij / s.h;
+        float ye[3], Xe[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            ye[a] = fmaf(ue, vv[a], cv[a]);
+            Xe[a] = fmaf((ue - s.bp) * ij, dv[a], D[a]);
+        }
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            gmu[b] = fmaf(Ke, fmaf(Wm[0][b], ye[0], fmaf(Wm[1][b], ye[1], Wm[2][b] * ye[2])), gmu[b]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) gW[a][b] = fmaf(-Ke * ye[a], Xe[b], gW[a][b]);
+        }
+    }
+    const float gom = -ij * fmaf(cv[0] + cv[1] + cv[2], J0.y, (vv[0] + vv[1] + vv[2]) * J1i);
+    const float nb = sqrtf(P.b.x * P.b.x + P.b.y * P.b.y + P.b.z * P.b.z);
+    const float nc = sqrtf(P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
+    const float nd = sqrtf(P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
+    const float lc = l * cst;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) G[b] = lc * gmu[b];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) G[3 + 3 * a + b] = lc * gW[a][b];
+    G[12] = lc * gom;
+    G[13] = l * nb * nc * nd * 0.15915494309189535f * ij * J0.x;
+    G[14] = lc * ij * J0.x;
+}
+
+__device__ __forceinline__ void red_grad(float* acc, const float* G) {
+    // four 16-byte vector atomics (sm_90+ float4 atomicAdd on global memory)
+    float4* out = (float4*)acc;
+    atomicAdd(out + 0, make_float4(G[0], G[1], G[2], G[3]));
+    atomicAdd(out + 1, make_float4(G[4], G[5], G[6], G[7]));
+    atomicAdd(out + 2, make_float4(G[8], G[9], G[10], G[11]));
+    atomicAdd(out + 3, make_float4(G[12], G[13], G[14], 0.0f));
+}
+
 template <bool STOCH>
 __global__ void __launch_bounds__(128) k_grad_params(TraceArgs A, const float* __restrict__ dl,
                                                      float* __restrict__ acc) {
@@ -258,84 +352,111 @@ __global__ void __launch_bounds__(128) k_grad_params(TraceArgs A, const float* _
             Setup s;
             if (!prim_setup(P, r, r.tmin, r.tmax, s)) return;
             const float l = STOCH ? g * w[ref >> 27] : g;
-            // world offset at the re-centring point (TwoSum as prim_setup) and whitened vectors
-            const float hx = __fsub_rn(o.x, P.a.x), hy = __fsub_rn(o.y, P.a.y), hz = __fsub_rn(o.z, P.a.z);
-            const float bx = __fsub_rn(hx, o.x), by = __fsub_rn(hy, o.y), bz = __fsub_rn(hz, o.z);
-            const float lx = __fadd_rn(__fsub_rn(o.x, __fsub_rn(hx, bx)), __fsub_rn(-P.a.x, bx));
-            const float ly = __fadd_rn(__fsub_rn(o.y, __fsub_rn(hy, by)), __fsub_rn(-P.a.y, by));
-            const float lz = __fadd_rn(__fsub_rn(o.z, __fsub_rn(hz, bz)), __fsub_rn(-P.a.z, bz));
-            const float D[3] = {__fadd_rn(__fmaf_rn(s.tc, d.x, hx), lx), __fadd_rn(__fmaf_rn(s.tc, d.y, hy), ly),
-                                __fadd_rn(__fmaf_rn(s.tc, d.z, hz), lz)};
-            const float dv[3] = {d.x, d.y, d.z};
-            const float Wm[3][3] = {{P.b.x, P.b.y, P.b.z}, {P.c.x, P.c.y, P.c.z}, {P.d.x, P.d.y, P.d.z}};
-            float pv[3], vv[3], cv[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                pv[a] = fmaf(Wm[a][0], D[0], fmaf(Wm[a][1], D[1], Wm[a][2] * D[2]));
-                vv[a] = fmaf(Wm[a][0], dv[0], fmaf(Wm[a][1], dv[1], Wm[a][2] * dv[2])) * s.ij;
-            }
-#pragma unroll
-            for (int a = 0; a < 3; ++a) cv[a] = fmaf(-s.bp, vv[a], pv[a]);
-            const float om = P.b.w, cst = P.d.w;
-            const float2 J0 = seg_J0c(s, s.u0, s.u1, wk);
-            float E0r, E0i, E1r, E1i;
-            {
-                float sp, cp;
-                sincos_red(fmaf(s.Om, s.u0, s.phi0), &sp, &cp);
-                const float e0 = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + s.u0 * s.u0));
-                E0r = e0 * cp; E0i = e0 * sp;
-                sincos_red(fmaf(s.Om, s.u1, s.phi0), &sp, &cp);
-                const float e1 = kInvSqrt2Pi * __expf(-0.5f * (s.r2 + s.u1 * s.u1));
-                E1r = e1 * cp; E1i = e1 * sp;
-            }
-            const float J1r = -s.Om * J0.y - (E1r - E0r), J1i = s.Om * J0.x - (E1i - E0i);
-            const float J2r = -s.Om * J1i - (s.u1 * E1r - s.u0 * E0r) + J0.x;
-            const float Kr = J1r - s.bp * J0.x, Ki = J1i - s.bp * J0.y, Lr = J2r - s.bp * J1r;
-            float Av[3], Bv[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                Av[a] = fmaf(cv[a], J0.x, fmaf(vv[a], J1r, om * J0.y));
-                Bv[a] = fmaf(cv[a], Kr, fmaf(vv[a], Lr, om * Ki));
-            }
-            const float lc = l * cst, ij = s.ij;
-            float gmu[3], gW[3][3];
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                gmu[b] = ij * fmaf(Wm[0][b], Av[0], fmaf(Wm[1][b], Av[1], Wm[2][b] * Av[2]));
-#pragma unroll
-                for (int a = 0; a < 3; ++a) gW[a][b] = -ij * fmaf(Av[a], D[b], ij * Bv[a] * dv[b]);
-            }
-            // moving chord ends on the ellipsoid
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const float ue = e ? s.u1 : s.u0;
-                if (ue != (e ? s.h : -s.h)) continue;
-                const float Ke = (e ? E1r : E0r) * ij / s.h;
-                float ye[3], Xe[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    ye[a] = fmaf(ue, vv[a], cv[a]);
-                    Xe[a] = fmaf((ue - s.bp) * ij, dv[a], D[a]);
-                }
-#pragma unroll
-                for (int b = 0; b < 3; ++b) {
-                    gmu[b] = fmaf(Ke, fmaf(Wm[0][b], ye[0], fmaf(Wm[1][b], ye[1], Wm[2][b] * ye[2])), gmu[b]);
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) gW[a][b] = fmaf(-Ke * ye[a], Xe[b], gW[a][b]);
-                }
-            }
-            const float gom = -ij * fmaf(cv[0] + cv[1] + cv[2], J0.y, (vv[0] + vv[1] + vv[2]) * J1i);
-            const float nb = sqrtf(P.b.x * P.b.x + P.b.y * P.b.y + P.b.z * P.b.z);
-            const float nc = sqrtf(P.c.x * P.c.x + P.c.y * P.c.y + P.c.z * P.c.z);
-            const float nd = sqrtf(P.d.x * P.d.x + P.d.y * P.d.y + P.d.z * P.d.z);
-            // four 16-byte vector atomics per hit (sm_90+ float4 atomicAdd on global memory)
-            float4* out = (float4*)(acc + (size_t)A.perm[k] * 16);
-            atomicAdd(out + 0, make_float4(lc * gmu[0], lc * gmu[1], lc * gmu[2], lc * gW[0][0]));
-            atomicAdd(out + 1, make_float4(lc * gW[0][1], lc * gW[0][2], lc * gW[1][0], lc * gW[1][1]));
-            atomicAdd(out + 2, make_float4(lc * gW[1][2], lc * gW[2][0], lc * gW[2][1], lc * gW[2][2]));
-            atomicAdd(out + 3, make_float4(lc * gom, l * nb * nc * nd * 0.15915494309189535f * ij * J0.x,
-                                           lc * ij * J0.x, 0.0f));
+            float G[15];
+            hit_grad(P, s, o, d, l, G, wk);
+            red_grad(acc + (size_t)A.perm[k] * 16, G);
         });
+    }
+}
+
+// Coherent rays (GF_TRACE_PACKETS: consecutive rays of a pixel block): one depth-first walk of
+// the scene BVH per 32 rays (a child pair is descended if any lane's slab test hits it), a hit
+// leaf's primitives loaded once and tested per lane; a primitive's 15 partial sums are summed over
+// the lanes (butterfly shuffles) and added with one set of vector atomics -- 32x fewer atomics on
+// the primitives every ray of a block crosses.
+constexpr int kGStk = 256;
+template <bool STOCH>
+__global__ void __launch_bounds__(128) k_grad_pkt(TraceArgs A, const float* __restrict__ dl,
+                                                  float* __restrict__ acc) {
+    __shared__ uint32_t s_stk[4][kGStk];
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* stk = s_stk[wid];
+    Work wk;
+    for (int64_t base = ((int64_t)blockIdx.x * 4 + wid) * 32; base < A.n; base += (int64_t)gridDim.x * 128) {
+        const int64_t i = base + lane;
+        const bool valid = i < A.n;
+        float4 r0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), r1 = make_float4(0.0f, 0.0f, 1.0f, 0.0f);
+        float g = 0.0f;
+        uint32_t mask = 0;
+        float w[kMaxGroups];
+        if (valid) {
+            r0 = __ldg((const float4*)A.rays + 2 * i);
+            r1 = __ldg((const float4*)A.rays + 2 * i + 1);
+            g = __ldg(dl + i);
+            const float3 dd = make_float3(r1.x, r1.y, r1.z);
+            if (STOCH) mask = policy_for(A.pol, A.sc, dd, A.seed, (uint32_t)i, 0, 0, ST_EXT, 1, w);
+            else mask = A.pol.static_mask;
+        }
+        const float3 o = make_float3(r0.x, r0.y, r0.z), d = make_float3(r1.x, r1.y, r1.z);
+        const RayDev r = make_ray(o, d, r0.w, r1.w);
+        const bool act = valid && g != 0.0f;
+        if (!__any_sync(FULL, act)) continue;
+        auto boxhit = [&](uint32_t sk, uint32_t info, float4 lo, float4 hi) {
+            return act && (node_mask(sk, info) & mask) && slab(r, lo, hi, r.tmin, r.tmax);
+        };
+        auto leaf = [&](uint32_t info, bool mine) {
+            const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, grp = info & 31u;
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const GPrim* pp = A.prims + first + k;
+                GPrim P;
+                P.a = __ldg(&pp->a);
+                const bool pass = mine && sphere_pretest(P.a, r, r.tmin, r.tmax);
+                if (!__any_sync(FULL, pass)) continue;
+                P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                Setup s;
+                float G[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) G[j] = 0.0f;
+                const bool hit = pass && prim_setup(P, r, r.tmin, r.tmax, s);
+                if (!__any_sync(FULL, hit)) continue;
+                if (hit) hit_grad(P, s, o, d, STOCH ? g * w[grp] : g, G, wk);
+                // transposing butterfly: after the halving steps (8+4+2+1 shuffles) lane L holds the
+                // partial sum of entry L>>1 over its half-warp pair; one more xor-1 completes it
+#pragma unroll
+                for (int half = 8; half >= 1; half >>= 1) {
+                    const bool up = (lane & (2 * half)) != 0;
+#pragma unroll
+                    for (int j = 0; j < half; ++j) {
+                        const float send = up ? G[j] : G[j + half];
+                        const float keep = up ? G[j + half] : G[j];
+                        G[j] = keep + __shfl_xor_sync(FULL, send, 2 * half);
+                    }
+                }
+                G[0] += __shfl_xor_sync(FULL, G[0], 1);
+                const int e = lane >> 1;
+                if (!(lane & 1) && e < 15) atomicAdd(acc + (size_t)A.perm[first + k] * 16 + e, G[0]);
+            }
+        };
+        int ns = 0;
+        {
+            const float4 lo = __ldg(&A.nodes[0].lo), hi = __ldg(&A.nodes[0].hi);
+            const uint32_t sk = __float_as_uint(lo.w), info = __float_as_uint(hi.w);
+            const bool h = boxhit(sk, info, lo, hi);
+            if (__any_sync(FULL, h)) {
+                if (sk & kLeafBit) leaf(info, h);
+                else { stk[0] = 0; ns = 1; }
+            }
+        }
+        while (ns > 0) {
+            const uint32_t i2 = stk[--ns];
+            const GNode2* q = A.nodes2 + i2;
+            const float4 lo0 = __ldg(&q->lo0), hi0 = __ldg(&q->hi0), lo1 = __ldg(&q->lo1), hi1 = __ldg(&q->hi1);
+            const uint32_t ref0 = __float_as_uint(lo0.w), inf0 = __float_as_uint(hi0.w);
+            const uint32_t ref1 = __float_as_uint(lo1.w), inf1 = __float_as_uint(hi1.w);
+            const bool h0 = boxhit(ref0, inf0, lo0, hi0), h1 = boxhit(ref1, inf1, lo1, hi1);
+            const bool a0 = __any_sync(FULL, h0), a1 = __any_sync(FULL, h1);
+            __syncwarp();
+            if (a1) {
+                if (ref1 & kLeafBit) leaf(inf1, h1);
+                else stk[ns++] = ref1;
+            }
+            if (a0) {
+                if (ref0 & kLeafBit) leaf(inf0, h0);
+                else stk[ns++] = ref0;
+            }
+            __syncwarp();
+        }
     }
 }
 
@@ -446,13 +567,20 @@ cudaError_t gf_launch_grad_alpha(const TraceArgs& A, const float* dl, float* gra
     return cudaGetLastError();
 }
 
-cudaError_t gf_launch_grad_params(const TraceArgs& A, const float* dl, float* acc, cudaStream_t st) {
+cudaError_t gf_launch_grad_params(const TraceArgs& A, const float* dl, float* acc, bool packets, cudaStream_t st) {
     if (A.n == 0 || A.n_nodes == 0) return cudaSuccess;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool stoch = !(A.pol.ls == 0 && A.pol.os == 0);
+    if (packets) {
+        const unsigned pgrid = (unsigned)std::min<int64_t>((A.n + 127) / 128, (int64_t)sms * 16);
+        if (stoch) k_grad_pkt<true><<<pgrid, 128, 0, st>>>(A, dl, acc);
+        else k_grad_pkt<false><<<pgrid, 128, 0, st>>>(A, dl, acc);
+        return cudaGetLastError();
+    }
     const unsigned wgrid = (unsigned)std::min<int64_t>((A.n + 3) / 4, (int64_t)sms * 16);
-    if (!(A.pol.ls == 0 && A.pol.os == 0)) k_grad_params<true><<<wgrid, 128, 0, st>>>(A, dl, acc);
+    if (stoch) k_grad_params<true><<<wgrid, 128, 0, st>>>(A, dl, acc);
     else k_grad_params<false><<<wgrid, 128, 0, st>>>(A, dl, acc);
     return cudaGetLastError();
 }

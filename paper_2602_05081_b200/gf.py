@@ -20,6 +20,7 @@ GF_OK = 0
 MODE_TOMOGRAPHY, MODE_SCATTER = 0, 1
 SHARD_NONE, SHARD_TILES, SHARD_SAMPLES = 0, 1, 2
 TRACE_BRUTE_FORCE = 1
+TRACE_PACKETS = 2
 
 
 class GFError(RuntimeError):
@@ -98,7 +99,7 @@ def lib():
     L.gf_trace_transmittance_ex.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp, vp]
     L.gf_trace_candidates.argtypes = [vp, vp, i64, u32, vp, i32, vp, vp]
     L.gf_trace_grad_alpha.argtypes = [vp, vp, i64, u64, vp, vp, vp]
-    L.gf_trace_grad_params.argtypes = [vp, vp, i64, u64, vp, vp, vp]
+    L.gf_trace_grad_params.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp]
     L.gf_grad_params_finish.argtypes = [vp, vp, vp, vp, vp]
     L.gf_render_scratch_bytes.argtypes = [vp, ctypes.POINTER(RenderDesc), ctypes.POINTER(sz)]
     L.gf_render.argtypes = [vp, ctypes.POINTER(RenderDesc), vp, vp, sz, vp, vp]
@@ -229,7 +230,7 @@ class GaborField:
                                                _ptr(dl), _ptr(grad), _stream()))
         return grad
 
-    def trace_grad_params(self, rays, dl_dtau, seed=0, accum=None, finish=True):
+    def trace_grad_params(self, rays, dl_dtau, seed=0, accum=None, finish=True, packets=False):
         """d(sum_r dl_dtau[r] tau_r) / d(mu, q, s, omega, alpha): (n_prims, 12) fp32 in input order
         (gf_trace_grad_params + gf_grad_params_finish).  accum (n_prims, 16) fp32 accumulates across
         calls when given; finish=False returns it raw."""
@@ -237,8 +238,8 @@ class GaborField:
         rays = torch.as_tensor(rays).to(device=self.device, dtype=torch.float32).contiguous().view(-1, 8)
         dl = torch.as_tensor(dl_dtau).to(device=self.device, dtype=torch.float32).contiguous()
         acc = accum if accum is not None else torch.zeros((self.n, 16), dtype=torch.float32, device=self.device)
-        self._check(self.L.gf_trace_grad_params(self.ctx, _ptr(rays), rays.shape[0], seed, _ptr(dl), _ptr(acc),
-                                                _stream()))
+        self._check(self.L.gf_trace_grad_params(self.ctx, _ptr(rays), rays.shape[0], seed,
+                                                TRACE_PACKETS if packets else 0, _ptr(dl), _ptr(acc), _stream()))
         if not finish:
             return acc
         grad = torch.empty((self.n, 12), dtype=torch.float32, device=self.device)

@@ -627,8 +627,9 @@ def _non_grazing_rays(S, sc, rays, band=0.01):
     return rays[keep]
 
 
+@pytest.mark.parametrize("packets", [False, True])
 @pytest.mark.parametrize("stoch", [False, True])
-def test_grad_params_parity(gfm, orc, stoch):
+def test_grad_params_parity(gfm, orc, stoch, packets):
     """Full parameter gradient: d(sum_r dl_r tau_r)/d(mu, q, s, omega, alpha) per
     primitive, closed-form moments + moving chord ends + chain rule on the GPU, against the oracle's
     Richardson central differences of the fp64 closed form.  Tolerance: 1e-3 of the sum of |per-ray
@@ -642,7 +643,7 @@ def test_grad_params_parity(gfm, orc, stoch):
     rays = _non_grazing_rays(S, sc, I.rays_through_box(6, 300))
     assert len(rays) > 60
     dl = np.random.default_rng(8).normal(size=len(rays)).astype(np.float32)
-    g = f.trace_grad_params(rays, dl, seed=5).cpu().numpy().astype(np.float64)
+    g = f.trace_grad_params(rays, dl, seed=5, packets=packets).cpu().numpy().astype(np.float64)
     if stoch:
         go = np.zeros((sc["n"], 12)); ga = np.zeros((sc["n"], 12))
         f0 = I.group_f0(sc)
