@@ -1418,8 +1418,11 @@ __global__ void __launch_bounds__(128) k_tomo_w(RenderDev R, int32_t sample) {
 // Tomography of coherent camera rays (static mask, no foveation / motion blur): the packet walk of
 // k_ff_pkt over the camera BVH for 32 consecutive pixels (one 8x4 block), each lane integrating its
 // own hits lane-locally (seg_J; all lanes test the same primitive, so the erf type is uniform).
+#ifndef GF_TOMO_MINB
+#define GF_TOMO_MINB 8  // 64 registers, 8 blocks per SM: +12-15 % over 80 registers (cfg2 / cfg5 --tomography)
+#endif
 template <bool COUNT>
-__global__ void __launch_bounds__(128) k_tomo_pkt(RenderDev R, int32_t sample) {
+__global__ void __launch_bounds__(128, GF_TOMO_MINB) k_tomo_pkt(RenderDev R, int32_t sample) {
     __shared__ uint32_t s_stk[4][kPStk];
     const unsigned FULL = 0xFFFFFFFFu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
