@@ -365,8 +365,11 @@ __global__ void __launch_bounds__(128) k_grad_params(TraceArgs A, const float* _
 // the lanes (butterfly shuffles) and added with one set of vector atomics -- 32x fewer atomics on
 // the primitives every ray of a block crosses.
 constexpr int kGStk = 256;
+#ifndef GF_GRADP_MINB
+#define GF_GRADP_MINB 5  // 96 registers (a few spills), 5 blocks per SM: -13 % vs 128 registers (tools_grad_sweep.sh)
+#endif
 template <bool STOCH>
-__global__ void __launch_bounds__(128) k_grad_pkt(TraceArgs A, const float* __restrict__ dl,
+__global__ void __launch_bounds__(128, GF_GRADP_MINB) k_grad_pkt(TraceArgs A, const float* __restrict__ dl,
                                                   float* __restrict__ acc) {
     __shared__ uint32_t s_stk[4][kGStk];
     const unsigned FULL = 0xFFFFFFFFu;
