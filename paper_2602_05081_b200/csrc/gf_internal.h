@@ -119,7 +119,6 @@ struct RenderDev {
     uint32_t* ldepth;
     // camera BVH for depth-0 rays: projective boxes, basis rows r, u, f (cb) at the eye
     int32_t camb;  // camera BVH built for this call
-    int64_t tomo_pkt_min;  // tomography chunks with at least this many paths take k_tomo_pkt
     float cb[9];
     gfk::GNode* cnodes;
     gfk::GNode2* cnodes2;
@@ -133,6 +132,8 @@ struct RenderDev {
     unsigned long long* rays;  // [2]
     float* accum;
     unsigned long long* work;  // gf_stats work counters (counting variant) or null
+    // (appended last, so the hot kernels' parameter offsets stay as measured)
+    int32_t tomo_pkt_min;  // tomography chunks with at least this many paths take k_tomo_pkt
 };
 
 cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, cudaStream_t st);
