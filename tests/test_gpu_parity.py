@@ -278,6 +278,23 @@ def test_render_tomography_cfg2_full_size_sampled(gfm, orc):
         assert np.all(d <= 1e-4 * np.maximum(1.0, np.abs(vo[:, 0]))), (i, d.max())
 
 
+def test_render_tomography_packets_two_chunks_jittered(gfm, orc):
+    """k_tomo_pkt across the 1M-path chunk boundary (2048x1024 = two chunks), jittered, 2 samples
+    (spp_begin 3): sampled pixels, both samples, against the oracle's identical Philox draws."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    desc = dict(I.render_desc_cfg2(2, 2048, 1024), mode=0, max_depth=1, jitter=1)
+    acc, rc = f.render(desc, 3, 2)
+    acc = acc.view(-1, 2).cpu().numpy().astype(np.float64)
+    assert int(rc[0]) == 2 * 2048 * 1024
+    rng = np.random.default_rng(13)
+    # pixels near the chunk boundary (path index 2^20 = tile-ordered) and random ones
+    pix = np.concatenate([rng.integers(0, 2048 * 1024, 200), np.arange(1024 * 512 - 40, 1024 * 512 + 40)]).astype(np.int32)
+    vo, _ = orc.Scene(sc).render_probes(desc, pix, 3, 2)
+    d = np.abs(acc[pix, 0] - vo.sum(axis=1))
+    assert np.all(d <= 1e-4 * np.maximum(1.0, np.abs(vo.sum(axis=1)))), d.max()
+
+
 def _probe_compare(gfm, orc, sc, desc, probes, spp, what, frac_tol=0.02, f0=None):
     f = field(gfm, sc, group_f0=f0)
     if f0 is not None:
