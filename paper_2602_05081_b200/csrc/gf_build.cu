@@ -221,6 +221,9 @@ __device__ __forceinline__ uint64_t expand3(uint32_t x) {
     return v;
 }
 
+#ifndef GF_VIEW_KEYS_2D
+#define GF_VIEW_KEYS_2D 2  // bit 0: light frame, bit 1: camera frame (camera: cfg3 +4 %, cfg2 / cfg5 within noise; light: cfg2 NEE +18 %, so off)
+#endif
 __global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, const uint32_t* cbounds, uint64_t* keys,
                        uint32_t* vals, Frame F, const float* center) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -239,7 +242,15 @@ __global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, con
         q[k] = min((uint32_t)(t * 524288.0f), 524287u);  // 19 bits
     }
     uint32_t group = groups[i];
-    keys[i] = ((uint64_t)group << 57) | (expand3(q[0]) << 2) | (expand3(q[1]) << 1) | expand3(q[2]);
+    if ((F.identity == 0 && (GF_VIEW_KEYS_2D & 1)) || (F.identity == 2 && (GF_VIEW_KEYS_2D & 2))) {
+        // view frames: 2D Morton of the two axes across the rays (19 bits each), then the axis along
+        // them (19 bits) -- the top of the tree partitions columns, the bottom orders a column
+        uint64_t m2 = 0;
+        for (int b = 18; b >= 0; --b) m2 = (m2 << 2) | (((q[0] >> b) & 1u) << 1) | ((q[1] >> b) & 1u);
+        keys[i] = ((uint64_t)group << 57) | (m2 << 19) | q[2];
+    } else {
+        keys[i] = ((uint64_t)group << 57) | (expand3(q[0]) << 2) | (expand3(q[1]) << 1) | expand3(q[2]);
+    }
     vals[i] = (uint32_t)i;
 }
 
