@@ -1,6 +1,6 @@
 """diagnostic: per-sample disagreement of the cfg2 full-frame render with the oracle (GF_LIB selects the lib)."""
 import sys, os, numpy as np
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle
 from paper_2602_05081_b200 import gf, inputs as I
 sc = I.scene_cfg2()
