@@ -234,6 +234,9 @@ __device__ __forceinline__ uint32_t bin_add(const Setup& s, float cj, float t0, 
 #ifndef GF_PRE_PF
 #define GF_PRE_PF 1  // packet resolve: load the next chunk's chord data one chunk ahead
 #endif
+#ifndef GF_MINB_PKT
+#define GF_MINB_PKT 7  // k_ff_pkt blocks per SM (72 registers)
+#endif
 #ifndef GF_PACKET
 #define GF_PACKET 1  // depth-0 (camera) free flight with packet traversal (k_ff_pkt)
 #endif
@@ -902,7 +905,7 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
 // the rays one after another with ff_resolve (chord integrals, escape test, root).
 constexpr int kPStk = 512;
 template <bool STOCH, bool COUNT, bool FOV>
-__global__ void __launch_bounds__(128, 7) k_ff_pkt(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128, GF_MINB_PKT) k_ff_pkt(RenderDev R, int32_t sample, int32_t depth) {
     __shared__ uint32_t s_stk[4][kPStk];
     __shared__ WarpEnd s_e[4];
     __shared__ float s_h[4][64];
