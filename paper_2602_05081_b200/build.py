@@ -26,17 +26,18 @@ def _deps():
     return max(os.path.getmtime(f) for f in files)
 
 
-def build(force=False, verbose=False, defines=(), lib=None):
-    """Build libgf.so; `defines` (e.g. ["GF_BATCH=16"]) + `lib` build a tuning variant elsewhere."""
+def build(force=False, verbose=False, defines=(), lib=None, flags=()):
+    """Build libgf.so; `defines` (e.g. ["GF_BATCH=16"]) / extra nvcc `flags` + `lib` build a tuning
+    variant elsewhere."""
     lib = lib or LIB
-    if not force and not defines and os.path.exists(lib) and os.path.getmtime(lib) >= _deps():
+    if not force and not defines and not flags and os.path.exists(lib) and os.path.getmtime(lib) >= _deps():
         return lib
-    obj_dir = OBJ if not defines else OBJ + "_" + os.path.basename(lib).replace(".so", "")
+    obj_dir = OBJ if not (defines or flags) else OBJ + "_" + os.path.basename(lib).replace(".so", "")
     os.makedirs(obj_dir, exist_ok=True)
 
     def comp(src):
         obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + FLAGS + list(flags) + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
