@@ -45,7 +45,7 @@ class RenderDesc(ctypes.Structure):
                 ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float), ("seed", ctypes.c_uint64),
                 ("ext", Policy), ("nee", Policy), ("group_f0", ctypes.c_void_p),
                 ("foveation", ctypes.c_int32), ("fov_gaze", ctypes.c_float * 2), ("fov_f0", ctypes.c_float),
-                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8),
+                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float),
                 ("motion_blur", ctypes.c_int32), ("mb_dir", ctypes.c_float * 3), ("mb_m", ctypes.c_float)]
 
 
@@ -57,7 +57,13 @@ def lib():
         vp, i32, i64, u32, u64, dbl = (ctypes.c_void_p, ctypes.c_int, ctypes.c_long, ctypes.c_uint32,
                                        ctypes.c_uint64, ctypes.c_double)
         L.or_scene_create.restype = vp
-        L.or_scene_create.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
+        L.or_scene_create.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, i32]
+        L.or_scene_info.argtypes = [vp, vp, vp]
+        L.or_motion_blur_mask.argtypes = [vp, vp, ctypes.c_float, ctypes.c_float, vp, vp]
+        L.or_adaptive_extent.argtypes = [i64, vp, vp, vp, ctypes.c_float, vp]
+        L.or_fov_fmax.restype = ctypes.c_float
+        L.or_fov_fmax.argtypes = [vp, u32, u32]
+        L.or_free_flight_diag.argtypes = [vp, vp, u32, vp, dbl, dbl, vp]
         L.or_scene_destroy.argtypes = [vp]
         L.or_scene_groups.argtypes = [vp, vp, vp]
         L.or_eval_kernel.restype = dbl
@@ -118,14 +124,18 @@ class Scene:
         self.P = int(scene["P"])
         self.K = int(scene["K"])
         self.G = 1 + (self.P - 1) * self.K
+        self.n_bands = int(scene.get("n_bands", 1))
+        self.G0 = self.G
+        self.G = self.G0 * self.n_bands
         self._keep = [_f32(scene["mu"]), _f32(scene["quat"]), _f32(scene["scale"]), _f32(scene["alpha"]),
                       _f32(scene["omega"]), _f32(scene.get("extent")),
                       None if scene.get("level") is None else np.ascontiguousarray(scene["level"], np.uint8),
                       None if scene.get("bin") is None else np.ascontiguousarray(scene["bin"], np.uint8),
-                      _f32(scene["bin_axes"])]
+                      _f32(scene["bin_axes"]),
+                      None if scene.get("band") is None else np.ascontiguousarray(scene["band"], np.uint8)]
         k = self._keep
         self.h = L.or_scene_create(self.n, _p(k[0]), _p(k[1]), _p(k[2]), _p(k[3]), _p(k[4]), _p(k[5]),
-                                   _p(k[6]), _p(k[7]), self.P, self.K, _p(k[8]))
+                                   _p(k[6]), _p(k[7]), self.P, self.K, _p(k[8]), _p(k[9]), self.n_bands)
         if not self.h:
             raise ValueError("oracle rejected scene")
 
@@ -139,6 +149,29 @@ class Scene:
         b = np.zeros(max(self.n, 1), np.int32)
         lib().or_scene_groups(self.h, _p(g), _p(b))
         return g[:self.n], b[:self.n]
+
+    def info(self):
+        """(level_fmax[8], group_f0[32]): the scene-derived policy parameters (readings F3, C12)."""
+        lf = np.zeros(8, np.float32)
+        f0 = np.zeros(32, np.float32)
+        lib().or_scene_info(self.h, _p(lf), _p(f0))
+        return lf, f0[:self.G]
+
+    def motion_blur_mask(self, direction, m, threshold):
+        """Accelerated motion blur (readings M1-M3): (32-bit group mask, attenuation per group)."""
+        d = _f32(direction).reshape(3)
+        mask = np.zeros(1, np.uint32)
+        att = np.zeros(32, np.float32)
+        lib().or_motion_blur_mask(self.h, _p(d), ctypes.c_float(m), ctypes.c_float(threshold), _p(mask), _p(att))
+        return int(mask[0]), att[:self.G]
+
+    def free_flight_diag(self, ray, xi, t_q, mask=0xFFFFFFFF, weights=None):
+        """(tau(t0, t_q), max cumulative tau at event points before t_q, tau*) -- C17 root checks."""
+        ray = _f32(ray).reshape(8)
+        out = np.zeros(3, np.float64)
+        w = _f32(weights)
+        lib().or_free_flight_diag(self.h, _p(ray), mask & 0xFFFFFFFF, _p(w), float(xi), float(t_q), _p(out))
+        return out
 
     def eval_kernel(self, i, x, truncated=True):
         x = np.ascontiguousarray(x, np.float64)
@@ -267,12 +300,10 @@ def make_render_desc(desc):
     d.nee = make_policy(**desc.get("nee", desc.get("ext", {})))
     fov = desc.get("foveation")
     if fov:
-        d.foveation = 1
+        d.foveation = int(fov.get("mode", 3))
         d.fov_gaze[:] = [float(x) for x in np.asarray(fov["gaze"], np.float32)]
         d.fov_f0, d.fov_slope = float(np.float32(fov["f0"])), float(np.float32(fov["slope"]))
         d.fov_jitter = float(np.float32(fov.get("jitter", 0.0)))
-        lf = [float(x) for x in np.asarray(fov["level_fmax"], np.float32)] + [0.0] * 8
-        d.fov_level_fmax[:] = lf[:8]
     mb = desc.get("motion_blur")
     if mb:
         d.motion_blur = 1
@@ -311,6 +342,21 @@ def camera_ray(desc, px, py, jx=0.5, jy=0.5):
     v = np.zeros(3, np.float32)
     lib().or_camera_ray(ctypes.byref(d), px, py, ctypes.c_float(jx), ctypes.c_float(jy), _p(o), _p(v))
     return o, v
+
+
+def adaptive_extent(scene, eps):
+    """Adaptive clamping (Eq. 15, reading C8'): per-primitive extents E for threshold eps."""
+    sc, al, om = _f32(scene["scale"]), _f32(scene["alpha"]), _f32(scene["omega"])
+    n = int(scene["n"])
+    out = np.zeros(max(n, 1), np.float32)
+    lib().or_adaptive_extent(n, _p(sc), _p(al), _p(om), ctypes.c_float(eps), _p(out))
+    return out[:n]
+
+
+def fov_fmax(desc, pix, smp):
+    """Foveation threshold of (pixel, sample) (readings F1, F2, F5)."""
+    d, keep = make_render_desc(desc)
+    return float(lib().or_fov_fmax(ctypes.byref(d), pix, smp))
 
 
 def hg_eval(g, cost):

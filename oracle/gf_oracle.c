@@ -42,7 +42,8 @@
 /* Scene                                                                      */
 /* ------------------------------------------------------------------------- */
 typedef struct {
-    int n, P, K, G;
+    int n, P, K, G;    /* G = n_bands * G0 groups in all (C24)                           */
+    int G0, n_bands;   /* groups per band 1 + (P-1) K; spatial bands (cfg5 distance bands) */
     double *mu;    /* 3n  kernel mean                                   */
     double *sinv;  /* 9n  Sigma^-1 = R S^-2 R^T (row major)             */
     double *wvec;  /* 3n  omega_vec = R S^-1 (w,w,w)^T         */
@@ -51,7 +52,11 @@ typedef struct {
     double *E2;    /* n   squared whitened extent (C7/C8; default 3^2)   */
     int *group;    /* n   group id g(l,b) (C10/C11/C24)                  */
     int *bin;      /* n   orientation bin (derived if not given)         */
+    int *level;    /* n   pyramid level                                  */
+    float *omega;  /* n   modulation scalar as given (fp32)              */
     float bin_axes[3 * 32];
+    float lfmax[8];  /* max world frequency |omega_vec| per level (F3)     */
+    float f0[32];    /* representative whitened frequency per group (C12)  */
 } or_scene;
 
 /* quaternion (x,y,z,w) -> rotation matrix R (row major), normalised in double */
@@ -108,48 +113,166 @@ static int derive_bin_f32(const float *qf, const float *sf, int K, const float *
     return best;
 }
 
+static void level_fmax_of(or_scene *s);
+static void group_f0_of(or_scene *s);
+
 /* Build the per-primitive double data.  level/bin may be NULL (bin==NULL or
- * 255 -> derived, level==NULL -> omega==0 ? 0 : 1).  Returns NULL on bad input. */
+ * 255 -> derived, level==NULL -> omega==0 ? 0 : 1); band NULL -> 0, n_bands >= 1
+ * spatial bands (group id band * G0 + g(l,b), G0 = 1 + (P-1) K, C24).  Returns NULL
+ * on bad input. */
 or_scene *or_scene_create(int n, const float *mu, const float *quat, const float *scale,
                           const float *alpha, const float *omega, const float *extent,
                           const uint8_t *level, const uint8_t *bin, int P, int K,
-                          const float *bin_axes) {
-    if (n < 0 || P < 1 || K < 1 || 1 + (P - 1) * K > OR_MAXG) return NULL;
+                          const float *bin_axes, const uint8_t *band, int n_bands) {
+    if (n_bands < 1) n_bands = 1;
+    if (n < 0 || P < 1 || K < 1 || n_bands * (1 + (P - 1) * K) > OR_MAXG) return NULL;
     or_scene *s = (or_scene *)calloc(1, sizeof(or_scene));
-    s->n = n; s->P = P; s->K = K; s->G = 1 + (P - 1) * K;
+    s->n = n; s->P = P; s->K = K; s->G0 = 1 + (P - 1) * K; s->n_bands = n_bands; s->G = n_bands * s->G0;
     if (bin_axes) memcpy(s->bin_axes, bin_axes, sizeof(float) * 3 * K);
     size_t nn = n > 0 ? (size_t)n : 1;
     s->mu = malloc(sizeof(double) * 3 * nn);   s->sinv = malloc(sizeof(double) * 9 * nn);
     s->wvec = malloc(sizeof(double) * 3 * nn); s->norm = malloc(sizeof(double) * nn);
     s->alpha = malloc(sizeof(double) * nn);    s->E2 = malloc(sizeof(double) * nn);
     s->group = malloc(sizeof(int) * nn);       s->bin = malloc(sizeof(int) * nn);
+    s->level = malloc(sizeof(int) * nn);       s->omega = malloc(sizeof(float) * nn);
     for (int i = 0; i < n; ++i) {
         const double qd[4] = {quat[4 * i], quat[4 * i + 1], quat[4 * i + 2], quat[4 * i + 3]};
         const double sx[3] = {scale[3 * i], scale[3 * i + 1], scale[3 * i + 2]};
         derive_d(qd, sx, omega[i], s->sinv + 9 * i, s->wvec + 3 * i, s->norm + i);
         for (int k = 0; k < 3; ++k) s->mu[3 * i + k] = mu[3 * i + k];
         s->alpha[i] = alpha[i];
+        s->omega[i] = omega[i];
         double E = extent ? extent[i] : 3.0;
         s->E2[i] = E * E;
         int l = level ? level[i] : (omega[i] == 0.0f ? 0 : 1);
         if (l >= P) l = P - 1;
+        s->level[i] = l;
         int b = (bin && bin[i] != 255) ? bin[i] : (l == 0 ? 0 : derive_bin_f32(quat + 4 * i, scale + 3 * i, K, s->bin_axes));
         if (b >= K) b = K - 1;
         s->bin[i] = b;
-        s->group[i] = (l == 0) ? 0 : 1 + (l - 1) * K + b;  /* C24 group id */
+        int bd = band ? band[i] : 0;
+        if (bd >= n_bands) bd = n_bands - 1;
+        s->group[i] = bd * s->G0 + ((l == 0) ? 0 : 1 + (l - 1) * K + b);  /* C24 group id */
     }
+    level_fmax_of(s);
+    group_f0_of(s);
     return s;
 }
 
 void or_scene_destroy(or_scene *s) {
     if (!s) return;
     free(s->mu); free(s->sinv); free(s->wvec); free(s->norm); free(s->alpha); free(s->E2);
-    free(s->group); free(s->bin); free(s);
+    free(s->group); free(s->bin); free(s->level); free(s->omega); free(s);
 }
 
 int or_scene_groups(const or_scene *s, int *group_out, int *bin_out) {
     for (int i = 0; i < s->n; ++i) { group_out[i] = s->group[i]; if (bin_out) bin_out[i] = s->bin[i]; }
     return s->n;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Scene-derived policy parameters                                            */
+/* ------------------------------------------------------------------------- */
+/* Maximum world frequency |omega_vec| = |R S^-1 (w,w,w)^T| of each Gabor level
+   (reading F3: "discard all levels that contain Gabor primitives with frequencies above the
+   threshold"); level 0 (Gaussians) 0.  Double, rounded to fp32 once. */
+static void level_fmax_of(or_scene *s) {
+    double mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < s->n; ++i) {
+        const double *w = s->wvec + 3 * i;
+        double f = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+        if (s->level[i] > 0 && f > mx[s->level[i]]) mx[s->level[i]] = f;
+    }
+    for (int l = 0; l < 8; ++l) s->lfmax[l] = (float)mx[l];
+}
+
+static int cmp_float(const void *a, const void *b) {
+    float x = *(const float *)a, y = *(const float *)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+/* Representative whitened frequency of each group (reading C12): the whitened
+   frequency |k_W| = sqrt(3) omega (C2) of the level's median member, median = middle element
+   of the sorted fp32 omegas (even count: the fp32 mean of the two middle ones), shared by all
+   bins (and bands) of a level; level 0: 0. */
+static void group_f0_of(or_scene *s) {
+    for (int g = 0; g < 32; ++g) s->f0[g] = 0.0f;
+    float *v = malloc(sizeof(float) * (s->n > 0 ? s->n : 1));
+    for (int l = 1; l < s->P; ++l) {
+        int m = 0;
+        for (int i = 0; i < s->n; ++i) if (s->level[i] == l) v[m++] = s->omega[i];
+        if (m == 0) continue;
+        qsort(v, m, sizeof(float), cmp_float);
+        volatile float med = (m & 1) ? v[m / 2] : (v[m / 2 - 1] + v[m / 2]) / 2.0f;
+        float f0 = (float)((double)med * sqrt(3.0));
+        for (int bd = 0; bd < s->n_bands; ++bd)
+            for (int b = 0; b < s->K; ++b) s->f0[bd * s->G0 + 1 + (l - 1) * s->K + b] = f0;
+    }
+    free(v);
+}
+
+void or_scene_info(const or_scene *s, float *lfmax8, float *f0_32) {
+    if (lfmax8) memcpy(lfmax8, s->lfmax, sizeof(float) * 8);
+    if (f0_32) memcpy(f0_32, s->f0, sizeof(float) * 32);
+}
+
+/* Accelerated motion blur (readings M1-M3): per group the mean of its members'
+   omega_vec (signs aligned with the member of largest |omega_vec|, first index on ties: +-omega_vec
+   is the same cosine), k = |mean . d| (d normalised), attenuation of the box filter of length m
+   along d on a cosine of angular frequency k = |sin(m k / 2) / (m k / 2)| (M2); group culled iff
+   attenuation < threshold.  Level-0 groups and empty groups are kept. */
+void or_motion_blur_mask(const or_scene *s, const float dir[3], float m, float threshold, uint32_t *mask_out,
+                         float *att_out) {
+    double d[3] = {dir[0], dir[1], dir[2]};
+    double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    for (int k = 0; k < 3; ++k) d[k] /= dn;
+    uint32_t mask = 0;
+    for (int g = 0; g < s->G; ++g) {
+        double att = 1.0;
+        int ref = -1;
+        double refn = -1.0;
+        for (int i = 0; i < s->n; ++i) {
+            if (s->group[i] != g) continue;
+            const double *w = s->wvec + 3 * i;
+            double f = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+            if (f > refn) { refn = f; ref = i; }
+        }
+        if (g % s->G0 != 0 && ref >= 0) {
+            const double *r = s->wvec + 3 * ref;
+            double sum[3] = {0, 0, 0};
+            long cnt = 0;
+            for (int i = 0; i < s->n; ++i) {
+                if (s->group[i] != g) continue;
+                const double *w = s->wvec + 3 * i;
+                double sg = (w[0] * r[0] + w[1] * r[1] + w[2] * r[2]) < 0.0 ? -1.0 : 1.0;
+                for (int k = 0; k < 3; ++k) sum[k] += sg * w[k];
+                ++cnt;
+            }
+            double k = fabs((sum[0] * d[0] + sum[1] * d[1] + sum[2] * d[2]) / (double)cnt);
+            double x = 0.5 * (double)m * k;
+            att = (x == 0.0) ? 1.0 : fabs(sin(x) / x);
+        }
+        if (att_out) att_out[g] = (float)att;
+        if (att >= threshold) mask |= 1u << g;
+    }
+    *mask_out = mask;
+}
+
+/* Adaptive clamping (Eq. 15; reading C8'): the whitened radius beyond which the
+   untruncated line integral of a ray is below eps in the worst case ||W v|| = 1/s_max and
+   Omega^2 = |k_W|^2 = 3 omega^2:  E = min(3, sqrt(max(0, -2 ln(eps 2 pi s1 s2 s3 / (alpha s_max))
+   - 3 omega^2))), floored at 1e-3 (the loader requires E > 0).  Double, rounded to fp32 once. */
+void or_adaptive_extent(long n, const float *scale, const float *alpha, const float *omega, float eps, float *out) {
+    for (long i = 0; i < n; ++i) {
+        double s0 = scale[3 * i], s1 = scale[3 * i + 1], s2 = scale[3 * i + 2];
+        double smax = s0 > s1 ? (s0 > s2 ? s0 : s2) : (s1 > s2 ? s1 : s2);
+        double a = alpha[i] > 1e-30f ? alpha[i] : 1e-30;
+        double w = omega[i];
+        double arg = -2.0 * log((double)eps * 2.0 * OR_PI * s0 * s1 * s2 / (a * smax)) - 3.0 * w * w;
+        double E = sqrt(arg > 0.0 ? arg : 0.0);
+        if (E > 3.0) E = 3.0;
+        if (E < 1e-3) E = 1e-3;
+        out[i] = (float)E;
+    }
 }
 
 /* ------------------------------------------------------------------------- */
@@ -550,7 +673,7 @@ typedef struct {
    weights (weights of unselected groups are 0). */
 void or_policy_eval(const or_scene *s, const or_policy *pol, const float dir[3], float ul, const float *uo,
                     const float *f0, uint32_t *mask_out, float *w_out) {
-    int P = s->P, K = s->K, G = s->G;
+    int P = s->P, K = s->K, G = s->G0;  /* draws over the G0 groups of one band */
     double lw[8];       /* per-level weight; 0 = level not selected */
     for (int l = 0; l < 8; ++l) lw[l] = 0.0;
     double om = 1.0 - pol->beta;
@@ -592,7 +715,7 @@ void or_policy_eval(const or_scene *s, const or_policy *pol, const float dir[3],
     }
     uint32_t mask = 0;
     float w[OR_MAXG];
-    for (int g = 0; g < G; ++g) w[g] = 0.0f;
+    for (int g = 0; g < OR_MAXG; ++g) w[g] = 0.0f;
     if (lw[0] != 0.0) { mask |= 1u; w[0] = (float)lw[0]; }  /* Gaussians never orientation-masked (C15) */
     for (int l = 1; l < P; ++l) {
         if (lw[l] == 0.0) continue;
@@ -653,8 +776,13 @@ void or_policy_eval(const or_scene *s, const or_policy *pol, const float dir[3],
             w[g] = (float)(lw[l] * (double)bw[b]);
         }
     }
+    /* spatial bands (C24): the same draw applies to every band's copy of the groups */
+    for (int bd = 1; bd < s->n_bands; ++bd) {
+        mask |= (mask & ((1u << G) - 1u)) << (bd * G);
+        for (int g = 0; g < G; ++g) w[bd * G + g] = w[g];
+    }
     mask &= pol->static_mask;
-    for (int g = 0; g < G; ++g) { if (!((mask >> g) & 1u)) w[g] = 0.0f; w_out[g] = w[g]; }
+    for (int g = 0; g < s->G; ++g) { if (!((mask >> g) & 1u)) w[g] = 0.0f; w_out[g] = w[g]; }
     *mask_out = mask;
 }
 
@@ -751,6 +879,52 @@ static int free_flight_f(const or_scene *s, const double o[3], const double v[3]
     return found;
 }
 
+/* tau(ta, tb) of a set of chords, each clipped to [ta, tb] (chords outside add nothing) */
+static double clipped_sum(const or_scene *s, const or_active *act, int nact, double ta, double tb) {
+    neum acc = {0, 0};
+    for (int k = 0; k < nact; ++k) {
+        const or_active *A = act + k;
+        double lo = ta > A->p.tin ? ta : A->p.tin, hi = tb < A->p.tout ? tb : A->p.tout;
+        if (!(hi > lo)) continue;
+        neum_add(&acc, A->w * s->alpha[A->idx] * seg_integral(s, A->idx, &A->p, lo, hi));
+    }
+    return neum_get(&acc);
+}
+
+/* Diagnostics of a candidate free-flight distance t_q (tests of the GPU root, C17): out[0] =
+   tau(t0, t_q) by the closed form; out[1] = the largest cumulative tau at an event point (chord
+   entry/exit) before t_q, i.e. how close an EARLIER segment end came to tau*; out[2] = tau*. */
+void or_free_flight_diag(const or_scene *s, const float *ray, uint32_t mask, const float *wts, double xi, double t_q,
+                         double *out) {
+    double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};
+    double t0 = ray[3], t1 = ray[7];
+    int cap = 64, nact = 0;
+    or_active *act = malloc(sizeof(or_active) * cap);
+    for (int i = 0; i < s->n; ++i) {
+        int g = s->group[i];
+        if (!((mask >> g) & 1u)) continue;
+        or_pair p;
+        pair_setup(s, i, o, v, t0, t1, &p);
+        if (!p.hit) continue;
+        if (nact == cap) { cap *= 2; act = realloc(act, sizeof(or_active) * cap); }
+        act[nact].idx = i; act[nact].p = p; act[nact].w = wts ? wts[g] : 1.0;
+        ++nact;
+    }
+    out[0] = clipped_sum(s, act, nact, t0, t_q);
+    double best = -INFINITY;
+    for (int k = 0; k < nact; ++k) {
+        const double te[2] = {act[k].p.tin, act[k].p.tout};
+        for (int e = 0; e < 2; ++e) {
+            if (!(te[e] < t_q)) continue;
+            double c = clipped_sum(s, act, nact, t0, te[e]);
+            if (c > best) best = c;
+        }
+    }
+    out[1] = best;
+    out[2] = -log1p(-xi);
+    free(act);
+}
+
 int or_free_flight_f(const or_scene *s, const float *ray, uint32_t mask, const float *wts, double xi, double *t_out) {
     double o[3] = {ray[0], ray[1], ray[2]}, v[3] = {ray[4], ray[5], ray[6]};
     return or_free_flight(s, o, v, ray[3], ray[7], mask, wts, xi, t_out);
@@ -766,9 +940,9 @@ typedef struct {
     float albedo, hg_g, sun_dir[3], sun_E, env_L;
     uint64_t seed;
     or_policy ext, nee;
-    const float *group_f0;  /* G floats (C12), may be NULL */
-    int32_t foveation;      /* foveated rendering */
-    float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_level_fmax[8];
+    const float *group_f0;  /* G floats (C12), NULL -> the scene's medians (group_f0_of) */
+    int32_t foveation;      /* foveated rendering: mode bits, 1 levels, 2 continuous */
+    float fov_gaze[2], fov_f0, fov_slope, fov_jitter;
     int32_t motion_blur;    /* motion-blur reference */
     float mb_dir[3], mb_m;
 } or_render_desc;
@@ -798,12 +972,15 @@ static float fov_fmax(const or_render_desc *d, uint32_t pix, uint32_t smp) {
 /* Level masking ("discard all levels that contain Gabor primitives with frequencies above
    the threshold", reading F3): level l >= 1 kept iff its maximum frequency <= f_max; level 0 kept */
 static uint32_t fov_mask(const or_scene *s, const or_render_desc *d, float fm) {
+    (void)d;
     uint32_t m = 1u;
     for (int l = 1; l < s->P; ++l)
-        if (d->fov_level_fmax[l] <= fm)
+        if (s->lfmax[l] <= fm)
             for (int b = 0; b < s->K; ++b) m |= 1u << (1 + (l - 1) * s->K + b);
+    for (int bd = 1; bd < s->n_bands; ++bd) m |= (m & ((1u << s->G0) - 1u)) << (bd * s->G0);
     return m;
 }
+float or_fov_fmax(const or_render_desc *d, uint32_t pix, uint32_t smp) { return fov_fmax(d, pix, smp); }
 
 /* camera ray in fp32 with explicit fused ops (bit-identical to the GPU) */
 static void camera_ray(const or_render_desc *d, int px, int py, float jx, float jy, float o[3], float v[3]) {
@@ -844,7 +1021,7 @@ static void eval_pol(const or_scene *s, const or_render_desc *d, const or_policy
     float ul = or_uniform(d->seed, pix, smp, dep, st, k_level);
     float uo[8];
     for (int l = 1; l < s->P; ++l) uo[l - 1] = or_uniform(d->seed, pix, smp, dep, st, k_level + l);
-    or_policy_eval(s, pol, dir, ul, uo, d->group_f0, mask, w);
+    or_policy_eval(s, pol, dir, ul, uo, d->group_f0 ? d->group_f0 : s->f0, mask, w);
 }
 
 /* one (pixel, sample) path; returns the estimate, *nrays = ray queries traced */
@@ -869,8 +1046,10 @@ double or_path(const or_scene *s, const or_render_desc *d, uint32_t pix, uint32_
     uint32_t mask;
     float w[OR_MAXG];
     /* foveation: one threshold per (pixel, sample) for every ray of the path */
-    const float fmx = d->foveation ? fov_fmax(d, pix, smp) : INFINITY;
-    const uint32_t fovm = d->foveation ? fov_mask(s, d, fmx) : 0xFFFFFFFFu;
+    /* foveation mode bit 0: level masking (F3), bit 1: the continuous per-primitive check (F4) */
+    const float fth = d->foveation ? fov_fmax(d, pix, smp) : INFINITY;
+    const float fmx = (d->foveation & 2) ? fth : INFINITY;
+    const uint32_t fovm = (d->foveation & 1) ? fov_mask(s, d, fth) : 0xFFFFFFFFu;
     if (d->mode == 0) {  /* tomography: tau-hat of the camera ray */
         eval_pol(s, d, &d->ext, vf, pix, smp, 0, ST_EXT, 1, &mask, w);
         mask &= fovm;

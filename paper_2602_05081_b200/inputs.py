@@ -10,7 +10,8 @@ Scene dict keys (SoA, fp32 unless stated):
   n, P (pyramid levels, level 0 = Gaussians), K (orientation bins per Gabor level),
   mu[n,3], quat[n,4] (x,y,z,w, unit), scale[n,3] (>0), alpha[n] (>=0), omega[n] (>=0),
   extent[n] (whitened radius E, 3 = the paper's 3 sigma bound), level u8[n],
-  bin u8[n] (255 = let each side derive it), bin_axes[K,3].
+  bin u8[n] (255 = let each side derive it), bin_axes[K,3]; optionally band u8[n] and n_bands
+  (spatial bands folded into the group id, config 5).
 """
 import math
 
@@ -237,9 +238,15 @@ def scene_cfg4(seed=SCENE_SEED + 4, counts=(12000, 48000, 192000, 748000), s_lev
                    np.concatenate(omegas), np.concatenate(levels), name="cfg4")
 
 
-def scene_cfg5(seed=SCENE_SEED + 5, copies=120, grid=(12, 10), spacing=2.2):
+CFG5_EYE = (0.0, 6.0, 22.0)
+
+
+def scene_cfg5(seed=SCENE_SEED + 5, copies=120, grid=(12, 10), spacing=2.2, n_bands=3):
     """Config 5: 'army' -- 120 yawed, scaled copies of a 33,280-primitive bunny-like asset (config-2
-    generator at 500/3,494/9,318/19,968) on a 12 x 10 ground grid: N = 3,993,600."""
+    generator at 500/3,494/9,318/19,968) on a 12 x 10 ground grid: N = 3,993,600.  Every primitive
+    carries the distance band of its copy (`fig:army_bunny` P:L606-L617): the
+    copies ranked by the distance of their grid position from the config-5 eye, split into n_bands
+    equal groups (near / mid / far), folded into the group id as band * 10 + g(l, b)."""
     base = scene_bunny(seed=seed, counts=(500, 3494, 9318, 19968), name="cfg5-asset")
     rng = np.random.default_rng(seed + 1)
     nb = base["n"]
@@ -261,6 +268,10 @@ def scene_cfg5(seed=SCENE_SEED + 5, copies=120, grid=(12, 10), spacing=2.2):
         out["scale"].append(base["scale"].astype(np.float64) * sc)
         out["alpha"].append(base["alpha"].astype(np.float64) * sc ** 2)  # keeps peak density (alpha ~ s^3 / s)
     n = nb * copies
+    pos = np.array([[(c % grid[0] - (grid[0] - 1) / 2) * spacing, 0.0, (c // grid[0] - (grid[1] - 1) / 2) * spacing]
+                    for c in range(copies)])
+    rank = np.argsort(np.argsort(np.linalg.norm(pos - np.asarray(CFG5_EYE), axis=1), kind="stable"), kind="stable")
+    copy_band = (rank * n_bands // copies).astype(np.uint8)
     q = np.concatenate(out["quat"])
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     return {"name": "cfg5", "n": n, "P": base["P"], "K": base["K"],
@@ -269,7 +280,7 @@ def scene_cfg5(seed=SCENE_SEED + 5, copies=120, grid=(12, 10), spacing=2.2):
             "alpha": np.concatenate(out["alpha"]).astype(np.float32),
             "omega": np.tile(base["omega"], copies), "extent": np.full(n, 3.0, np.float32),
             "level": np.tile(base["level"], copies), "bin": np.full(n, 255, np.uint8),
-            "bin_axes": base["bin_axes"]}
+            "bin_axes": base["bin_axes"], "band": np.repeat(copy_band, nb), "n_bands": n_bands}
 
 
 def empty_scene(P=P_DEFAULT, K=K_DEFAULT):
@@ -291,104 +302,25 @@ def scene_column(seed=SCENE_SEED + 9, n=1500, density=0.02):
     return _finish(mu, random_quats(rng, n), scale, peak, omega, level, name="column")
 
 
-def level_fmax(scene):
-    """Maximum world frequency |omega_vec| = omega |S^-1 (1,1,1)| of each pyramid level
-    (index 0: Gaussians, 0): the per-level bound the foveation policy compares with f_max."""
-    P = scene["P"]
-    s = scene["scale"].astype(np.float64)
-    f = scene["omega"].astype(np.float64) * np.linalg.norm(1.0 / s, axis=1)
-    out = np.zeros(8, np.float32)
-    for l in range(1, P):
-        sel = scene["level"] == l
-        if sel.any():
-            out[l] = np.float32(f[sel].max())
-    return out
-
-
-def foveation(scene, gaze, f0, slope, jitter=0.0):
-    """Foveated-rendering parameters (gf_render_desc foveation fields) for `scene`."""
+def foveation(gaze, f0, slope, jitter=0.0, mode=3):
+    """Foveated-rendering parameters (gf_render_desc foveation fields): gaze point in pixels, threshold
+    at the fovea, slope per unit eccentricity, jitter; mode bit 0 = level masking, bit 1 = the
+    continuous per-primitive check (3 = both, the paper's full method)."""
     return {"gaze": [float(gaze[0]), float(gaze[1])], "f0": float(f0), "slope": float(slope),
-            "jitter": float(jitter), "level_fmax": level_fmax(scene)}
-
-
-def omega_vectors(scene):
-    """World frequency vectors omega_vec = R S^-1 (omega, omega, omega), float64 [n, 3]."""
-    q = scene["quat"].astype(np.float64)
-    x, y, z, w = (q[:, k] / np.linalg.norm(q, axis=1) for k in range(4))
-    R = np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], -1),
-                  np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1),
-                  np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1)], 1)
-    return np.einsum("nij,nj->ni", R, scene["omega"].astype(np.float64)[:, None] / scene["scale"].astype(np.float64))
-
-
-def group_ids(scene):
-    """Group id per primitive (C10/C11): level 0 -> 0; Gabor level l, orientation bin b = argmax_k
-    |omega_hat . axis_k| (ties -> lower k) -> 1 + (l-1) K + b.  Host-side helper for mask policies."""
-    K = scene["K"]
-    lvl = scene["level"].astype(np.int64)
-    if np.all(scene["bin"] != 255):
-        b = scene["bin"].astype(np.int64)
-    else:
-        wv = omega_vectors(scene)
-        nrm = np.linalg.norm(wv, axis=1, keepdims=True)
-        wh = np.divide(wv, nrm, out=np.zeros_like(wv), where=nrm > 0)
-        axes = np.asarray(scene["bin_axes"], np.float64).reshape(K, 3)
-        b = np.argmax(np.abs(wh @ axes.T), axis=1)
-    return np.where(lvl == 0, 0, 1 + (lvl - 1) * K + b)
+            "jitter": float(jitter), "mode": int(mode)}
 
 
 def motion_blur(direction, m):
-    """Motion-blur reference parameters (gf_render_desc motion_blur fields)."""
+    """Motion-blur reference parameters (gf_render_desc motion_blur fields): unit direction, length."""
     d = np.asarray(direction, np.float64)
     return {"dir": (d / np.linalg.norm(d)).astype(np.float32).tolist(), "m": float(m)}
 
 
-def motion_blur_mask(scene, direction, m, threshold, groups=None):
-    """Accelerated motion blur (readings M1-M3): cull group g if the box-filter attenuation
-    |sin(m k / 2) / (m k / 2)|, k = |omega_g . d|, of the group's mean frequency vector omega_g (signs
-    aligned with the group's orientation axis before averaging) is below `threshold`.  Level 0 is never
-    culled.  Returns the static mask (32 bits) and the per-group attenuation."""
-    d = np.asarray(direction, np.float64)
-    d = d / np.linalg.norm(d)
-    if groups is None:
-        groups = group_ids(scene)
-    wv = omega_vectors(scene)
-    G = 1 + (scene["P"] - 1) * scene["K"]
-    att = np.ones(G)
-    mask = 0
-    for g in range(G):
-        sel = groups == g
-        if g == 0 or not sel.any():
-            mask |= 1 << g
-            continue
-        v = wv[sel]
-        ref = v[np.argmax(np.linalg.norm(v, axis=1))]
-        v = np.where((v @ ref)[:, None] < 0, -v, v)
-        k = abs(float(v.mean(0) @ d))
-        x = 0.5 * m * k
-        att[g] = 1.0 if x == 0 else abs(np.sin(x) / x)
-        if att[g] >= threshold:
-            mask |= 1 << g
-    return mask, att
-
-
-def adaptive_extent(scene, eps):
-    """Adaptive clamping (Eq. 15, reading C8'): per primitive
-    E = min(3, sqrt(max(0, -2 ln(eps 2 pi s1 s2 s3 / (alpha s_max)) - 3 omega^2))), the whitened
-    distance beyond which a ray's untruncated line integral (worst case ||W v|| = 1/s_max, Omega^2 =
-    k_W^2 = 3 omega^2 as in Eq. 15) is below eps.  Non-conservative for rays across the modulation
-    planes (Omega < k_W); returned as the `extent` input of both the kernels and the oracle, floored at
-    1e-3 (the loader requires E > 0; such a primitive keeps a negligible core)."""
-    s = scene["scale"].astype(np.float64)
-    a = scene["alpha"].astype(np.float64)
-    w = scene["omega"].astype(np.float64)
-    arg = -2.0 * np.log(eps * 2.0 * math.pi * s.prod(1) / (np.maximum(a, 1e-30) * s.max(1))) - 3.0 * w * w
-    return np.clip(np.sqrt(np.maximum(arg, 0.0)), 1e-3, 3.0).astype(np.float32)
-
-
-def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
+def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT, n_bands=1, bands=None):
     """32-bit group mask selecting whole pyramid levels: level 0 -> bit 0, Gabor level l ->
-    bits 1+(l-1)K .. (l)K (the group numbering g(l,b) of DESIGN.md §5; paper V_l = 2^l)."""
+    bits 1+(l-1)K .. (l)K of each spatial band (group numbering band * G0 + g(l,b) of DESIGN.md §5;
+    paper V_l = 2^l).  bands: the bands to select (default all)."""
+    G0 = 1 + (P - 1) * K
     m = 0
     for l in levels:
         if l == 0:
@@ -396,21 +328,9 @@ def level_mask(levels, P=P_DEFAULT, K=K_DEFAULT):
         else:
             for b in range(K):
                 m |= 1 << (1 + (l - 1) * K + b)
-    return m
-
-
-def group_f0(scene):
-    """Representative whitened frequency per group (reading C12): median of sqrt(3)*omega over the
-    members of the group's level (all bins of a level share it). Input parameter of the
-    Importance orientation strategy."""
-    P, K = scene["P"], scene["K"]
-    G = 1 + (P - 1) * K
-    out = np.zeros(G, np.float32)
-    for l in range(1, P):
-        sel = scene["level"] == l
-        med = float(np.median(scene["omega"][sel])) * math.sqrt(3.0) if sel.any() else 0.0
-        for b in range(K):
-            out[1 + (l - 1) * K + b] = med
+    out = 0
+    for bd in (range(n_bands) if bands is None else bands):
+        out |= m << (bd * G0)
     return out
 
 
@@ -474,10 +394,20 @@ def render_desc_cfg4(width=2048, height=2048, seed=RENDER_SEED + 4):
     return d
 
 
-def render_desc_cfg5(mask_levels=(0, 1, 2, 3), width=4096, height=4096, seed=RENDER_SEED + 5):
-    """Config 5: multiple scattering depth 8 over the army, one global static LOD mask."""
-    d = camera((0, 6, 22), (0, 0, 0), (0, 1, 0), 50.0, width, height)
-    m = level_mask(mask_levels)
+CFG5_BANDED_LEVELS = ((0, 1, 2, 3), (0, 1, 2), (0, 1))  # near / mid / far (fig:army_bunny)
+
+
+def render_desc_cfg5(mask_levels=(0, 1, 2, 3), width=4096, height=4096, seed=RENDER_SEED + 5, n_bands=3):
+    """Config 5: multiple scattering depth 8 over the army, one static LOD mask: the levels
+    `mask_levels` in every distance band, or mask_levels = "banded": levels 0..3 near, 0..2 mid,
+    0..1 far (the distance-dependent LOD of fig:army_bunny)."""
+    d = camera(CFG5_EYE, (0, 0, 0), (0, 1, 0), 50.0, width, height)
+    if isinstance(mask_levels, str) and mask_levels == "banded":
+        m = 0
+        for bd, lv in enumerate(CFG5_BANDED_LEVELS[:n_bands]):
+            m |= level_mask(lv, n_bands=n_bands, bands=[bd])
+    else:
+        m = level_mask(mask_levels, n_bands=n_bands)
     d.update(mode=1, max_depth=8, jitter=1, albedo=0.8, hg_g=0.0, sun_dir=SUN, sun_E=3.0, env_L=0.2, seed=seed,
              ext=policy(static_mask=m), nee=policy(static_mask=m))
     return d

@@ -91,3 +91,73 @@ def tau_quad(prims, o, v, t0, t1, weights=None):
         w = 1.0 if weights is None else weights[k]
         tot += w * p.alpha * p.line_integral(o, v, t0, t1)
     return tot
+
+
+# ---------------------------------------------------------------- scene-derived policy parameters
+def omega_vectors(scene):
+    """World frequency vectors omega_vec = R S^-1 (omega, omega, omega), float64 [n, 3]."""
+    return np.array([quat_R(q) @ (float(w) / np.asarray(s, np.float64))
+                     for q, s, w in zip(scene["quat"], scene["scale"], scene["omega"])]).reshape(-1, 3)
+
+
+def bins_f64(scene, margin=1e-5):
+    """Orientation bin argmax_k |d . o_k| (C11) in float64 from the quaternion, d = R S^-1 (1,1,1);
+    -1 where the two best scores are within `margin` (relative): ties decided by rounding."""
+    K = scene["K"]
+    axes = np.asarray(scene["bin_axes"], np.float64).reshape(K, 3)
+    out = []
+    for q, s in zip(scene["quat"], scene["scale"]):
+        d = quat_R(q) @ (1.0 / np.asarray(s, np.float64))
+        a = np.abs(axes @ d)
+        o = np.sort(a)[::-1]
+        out.append(-1 if K > 1 and o[0] - o[1] <= margin * o[0] else int(np.argmax(a)))
+    return np.array(out)
+
+
+def level_fmax_invariant(scene):
+    """Maximum |omega_vec| per level from the rotation-invariant form |R S^-1 (w,w,w)| = w |S^-1 (1,1,1)|
+    (R orthogonal), i.e. without forming R."""
+    s = np.asarray(scene["scale"], np.float64)
+    f = np.asarray(scene["omega"], np.float64) * np.sqrt((1.0 / s ** 2).sum(1))
+    out = np.zeros(8)
+    for l in range(1, scene["P"]):
+        sel = np.asarray(scene["level"]) == l
+        if sel.any():
+            out[l] = f[sel].max()
+    return out
+
+
+def group_f0_median(scene):
+    """Reading C12: sqrt(3) x the median omega of each Gabor level (numpy's median), for every bin and
+    band of the level."""
+    P, K, nb = scene["P"], scene["K"], int(scene.get("n_bands", 1))
+    G0 = 1 + (P - 1) * K
+    out = np.zeros(G0 * nb)
+    for l in range(1, P):
+        sel = np.asarray(scene["level"]) == l
+        if not sel.any():
+            continue
+        med = float(np.median(np.asarray(scene["omega"], np.float32)[sel])) * math.sqrt(3.0)
+        for bd in range(nb):
+            for b in range(K):
+                out[bd * G0 + 1 + (l - 1) * K + b] = med
+    return out
+
+
+def motion_blur_group_k(scene, groups, direction):
+    """Reading M3: per group |mean omega_vec . d| with each member's sign aligned to the group's member
+    of largest |omega_vec| (first index on ties); nan for empty groups."""
+    d = np.asarray(direction, np.float64)
+    d = d / np.linalg.norm(d)
+    wv = omega_vectors(scene)
+    G = int(groups.max()) + 1 if len(groups) else 0
+    out = np.full(G, np.nan)
+    for g in range(G):
+        sel = np.flatnonzero(groups == g)
+        if not len(sel):
+            continue
+        v = wv[sel]
+        ref = v[np.argmax(np.linalg.norm(v, axis=1))]
+        v = np.where((v @ ref)[:, None] < 0, -v, v)
+        out[g] = abs(float(v.mean(0) @ d))
+    return out

@@ -518,7 +518,7 @@ def test_tomography_estimator_unbiased(orc):
     sc = _tiny_scene()
     S = orc.Scene(sc)
     det = S.render_probes(_tiny_desc(0), [27, 36], 0, 1)[0][:, 0]
-    d = _tiny_desc(0, ext=I.policy(level_strategy=5, beta=0.2, orient_strategy=2), group_f0=I.group_f0(sc))
+    d = _tiny_desc(0, ext=I.policy(level_strategy=5, beta=0.2, orient_strategy=3))  # scene-default f0 (C12)
     vals, nr = S.render_probes(d, [27, 36], 0, 4000)
     mean, se = vals.mean(1), vals.std(1) / math.sqrt(vals.shape[1])
     assert np.all(np.abs(mean - det) <= 4 * se + 1e-12), (mean, det, se)
@@ -585,8 +585,8 @@ def test_foveation_limits_reduce_to_plain_renders(orc):
         base = _tiny_desc(mode, jitter=1)
         plain = S.render_probes(base, pix, 0, 6)[0]
         lvl0 = S.render_probes(dict(base, ext=I.policy(static_mask=1), nee=I.policy(static_mask=1)), pix, 0, 6)[0]
-        hi = S.render_probes(dict(base, foveation=I.foveation(sc, (4, 4), 1e30, 0.0, 0.3)), pix, 0, 6)[0]
-        zero = S.render_probes(dict(base, foveation=I.foveation(sc, (4, 4), 0.0, 0.0, 0.3)), pix, 0, 6)[0]
+        hi = S.render_probes(dict(base, foveation=I.foveation((4, 4), 1e30, 0.0, 0.3)), pix, 0, 6)[0]
+        zero = S.render_probes(dict(base, foveation=I.foveation((4, 4), 0.0, 0.0, 0.3)), pix, 0, 6)[0]
         assert np.array_equal(hi, plain)
         assert np.array_equal(zero, lvl0)
         assert not np.array_equal(plain, lvl0)
@@ -617,9 +617,9 @@ def test_foveation_primitive_check_follows_definition(orc):
     assert np.all(np.abs(full) > 1e-6)
     for k, p in enumerate(pix):
         f = abs(float(dirs[k] @ wvec))
-        lf = I.level_fmax(sc) * 0  # level masking off: every level bound 0 <= f_max
-        above = dict(d, foveation={"gaze": [0, 0], "f0": f * 1.01, "slope": 0.0, "level_fmax": lf})
-        below = dict(d, foveation={"gaze": [0, 0], "f0": f * 0.99, "slope": 0.0, "level_fmax": lf})
+        # continuous mode only (foveation mode 2: the per-primitive check without level masking)
+        above = dict(d, foveation=I.foveation((0, 0), f * 1.01, 0.0, 0.0, mode=2))
+        below = dict(d, foveation=I.foveation((0, 0), f * 0.99, 0.0, 0.0, mode=2))
         assert S.render_probes(above, [p], 0, 1)[0][0, 0] == full[k]
         assert S.render_probes(below, [p], 0, 1)[0][0, 0] == 0.0
 
@@ -664,15 +664,152 @@ def test_motion_blur_is_the_box_filtered_field(orc):
 
 def test_motion_blur_mask_attenuation(orc):
     """M3: a group is culled iff |sin(m k/2)/(m k/2)| of its mean frequency along d is
-    below the threshold; level 0 is never culled; m = 0 culls nothing."""
+    below the threshold, k from the sign-aligned group means computed here independently in numpy
+    (tests/refmath.py); level 0 is never culled; m = 0 culls nothing."""
     sc = I.scene_cfg1()
-    mask0, att0 = I.motion_blur_mask(sc, (1, 0, 0), 0.0, 0.99)
+    S = orc.Scene(sc)
+    mask0, att0 = S.motion_blur_mask((1, 0, 0), 0.0, 0.99)
     assert mask0 == (1 << 10) - 1 and np.all(att0 == 1.0)
-    mask, att = I.motion_blur_mask(sc, (1, 0, 0), 0.2, 0.6)
-    assert mask & 1
+    groups, _ = S.groups()
+    k = RM.motion_blur_group_k(sc, groups, (1, 0, 0))
+    mask, att = S.motion_blur_mask((1, 0, 0), 0.2, 0.6)
+    assert mask & 1 and att[0] == 1.0
     for g in range(1, 10):
+        x = 0.5 * 0.2 * k[g]
+        assert att[g] == pytest.approx(abs(math.sin(x) / x), rel=1e-6)
         assert bool(mask >> g & 1) == (att[g] >= 0.6)
     assert 0 < bin(mask).count("1") < 10
+
+
+@pytest.mark.parametrize("mk", [1.0, 2.5, 5.0])
+def test_motion_blur_attenuation_is_the_box_filter_response(orc, mk):
+    """M2 pinned to the physics it stands for: for a Gabor whose envelope is wide against
+    the blur length (s = 40, m = 0.08), the box-filtered optical depth (shift average of the closed
+    form over s = m (u - 1/2) d, 64-node Gauss-Legendre) divided by the unblurred one equals the signed
+    sinc(m k / 2), k = omega_vec . d -- for a ray through the centre across d, so the envelope barely
+    moves.  The oracle's attenuation for that one-member group must be its magnitude."""
+    s_ = 40.0
+    m = 0.08
+    k = mk / m  # omega_vec . d with omega_vec along d = x: |omega_vec| = omega sqrt(3) / s for R = I?
+    # omega_vec = R S^-1 (w, w, w): with R = I and isotropic s it is (w/s)(1,1,1); choose d along it
+    w = k * s_ / math.sqrt(3.0)
+    sc = make_scene([((0, 0, 0), ID, (s_, s_, s_), w, 1.0, 3.0)])
+    S = orc.Scene(sc)
+    d = np.ones(3) / math.sqrt(3.0)
+    v = np.array([1.0, -1.0, 0.0]) / math.sqrt(2.0)  # ray across the motion direction, through the centre
+    o = -300.0 * v
+    xs, ws = np.polynomial.legendre.leggauss(64)
+    blur = 0.0
+    for x, wgt in zip(xs, ws):
+        ray = I.pack_rays((o - m * 0.5 * x * d)[None], v[None])[0]
+        blur += 0.5 * wgt * S.prim_integral(0, ray[:3], ray[4:7], 0.0, np.inf)
+    plain = S.prim_integral(0, o, v, 0.0, np.inf)
+    ratio = blur / plain
+    sinc = math.sin(0.5 * m * k) / (0.5 * m * k)
+    assert ratio == pytest.approx(sinc, abs=2e-4), (ratio, sinc)
+    _, att = S.motion_blur_mask(d, m, 0.0)
+    assert att[1] == pytest.approx(abs(ratio), abs=2e-4)
+
+
+# ---------------------------------------------------------------- scene-derived parameters (C11, C12, F3, C8')
+def test_orientation_bins_match_independent_argmax(orc):
+    """C11: bin = argmax_k |d . o_k|, d = R S^-1 (1,1,1), ties -> lower k.  The oracle's fp32 decision
+    equals a float64 numpy argmax (tests/refmath.py) wherever the best two scores differ by more than
+    1e-5 relative, for K = 3 and K = 6; constructed exact ties go to the lower bin."""
+    rng = np.random.default_rng(21)
+    for K in (3, 6):
+        n = 800
+        sc = I._finish(rng.uniform(-1, 1, (n, 3)), I.random_quats(rng, n), np.exp(rng.normal(-3, 0.6, (n, 3))),
+                       np.ones(n), np.full(n, 1.0), np.ones(n, np.uint8), K=K, name="bins")
+        _, b = orc.Scene(sc).groups()
+        ref = RM.bins_f64(sc)
+        ok = ref >= 0
+        assert ok.mean() > 0.98
+        assert np.array_equal(b[ok], ref[ok])
+        assert len(set(b.tolist())) == K
+    ties = [((1, 1, 1), 0), ((2, 1, 1), 1), ((1, 2, 2), 0), ((3, 3, 1), 2), ((1, 2, 1), 0)]
+    sc = make_scene([((0, 0, 0), ID, s, 1.0, 1.0, 3.0) for s, _ in ties])
+    _, b = orc.Scene(sc).groups()
+    assert list(b) == [t for _, t in ties]
+
+
+def test_level_fmax_is_the_level_maximum(orc):
+    """F3: the per-level bound the foveation level mask compares with is the maximum of
+    |omega_vec| over the level; pinned by the rotation-invariant form w |S^-1 (1,1,1)| (no R)."""
+    for sc in (I.scene_cfg1(), I.scene_bunny(counts=(50, 300, 600, 900))):
+        lf, _ = orc.Scene(sc).info()
+        ref = RM.level_fmax_invariant(sc)
+        assert lf[0] == 0.0
+        np.testing.assert_allclose(lf, ref, rtol=1e-6)
+        assert np.all(lf[1:4] > 0)
+
+
+def test_group_f0_is_the_level_median(orc):
+    """C12: the representative whitened frequency of a group is sqrt(3) x the median omega of its level
+    (numpy's median), shared by every bin (and band) of the level; level 0 gets 0."""
+    for sc in (I.scene_cfg1(), I.scene_bunny(counts=(50, 301, 600, 900))):
+        _, f0 = orc.Scene(sc).info()
+        np.testing.assert_allclose(f0, RM.group_f0_median(sc), rtol=1e-6)
+    sc = I.scene_cfg5()
+    sub = {k: (v[::97] if isinstance(v, np.ndarray) and v.ndim and len(v) == sc["n"] else v) for k, v in sc.items()}
+    sub["n"] = len(sub["mu"])
+    _, f0 = orc.Scene(sub).info()
+    assert len(f0) == 30
+    np.testing.assert_allclose(f0, RM.group_f0_median(sub), rtol=1e-6)
+
+
+def test_adaptive_extent_level_set(orc):
+    """C8' (Eq. 15): E is the whitened distance at which the worst-case untruncated line
+    integral alpha s_max /(2 pi s1 s2 s3) e^{-(E^2 + 3 w^2)/2} equals eps.  Pinned by the oracle's own
+    closed-form integral (itself pinned to quadrature above) on rays that realise the worst case:
+    a Gaussian (w = 0) crossed along its major axis, and an isotropic Gabor crossed along k_W at
+    a closest point with zero phase (Omega^2 = 3 w^2, cos = 1)."""
+    eps = 1e-3
+    # anisotropic Gaussian, major axis x
+    s = (0.3, 0.1, 0.15)
+    sc = make_scene([((0, 0, 0), ID, s, 0.0, 0.005, 3.0)])
+    E = float(orc.adaptive_extent(sc, eps)[0])
+    assert 1e-3 < E < 3.0
+    # whitened perpendicular distance E along y: world offset E * s_y
+    o = np.array([-5.0, E * 0.1, 0.0])
+    val = float(sc["alpha"][0]) * orc.Scene(dict(sc, extent=np.array([50.0], np.float32))).prim_integral_infinite(
+        0, o, np.array([1.0, 0.0, 0.0]))
+    assert val == pytest.approx(eps, rel=1e-5)
+    # isotropic Gabor, ray along (1,1,1)/sqrt3 (k_W direction), offset along (1,-1,0)/sqrt2 (phase 0)
+    s0, w = 0.2, 0.9
+    sc = make_scene([((0, 0, 0), ID, (s0, s0, s0), w, 0.05, 3.0)])
+    E = float(orc.adaptive_extent(sc, eps)[0])
+    assert 1e-3 < E < 3.0
+    v = np.ones(3) / math.sqrt(3.0)
+    off = np.array([1.0, -1.0, 0.0]) / math.sqrt(2.0) * E * s0
+    o = off - 4.0 * v
+    val = float(sc["alpha"][0]) * orc.Scene(dict(sc, extent=np.array([50.0], np.float32))).prim_integral_infinite(
+        0, o, v)
+    assert val == pytest.approx(eps, rel=1e-5)
+    # clamps: huge alpha -> 3, tiny alpha -> the 1e-3 floor
+    big = make_scene([((0, 0, 0), ID, s, 0.0, 1e9, 3.0), ((0, 0, 0), ID, s, 0.0, 1e-12, 3.0)])
+    assert list(orc.adaptive_extent(big, eps)) == [3.0, np.float32(1e-3)]
+
+
+def test_foveation_threshold_closed_forms(orc):
+    """F1/F2/F5 at points where the threshold has a closed form: at the gaze pixel centre
+    e = 0 so f_max = f0 (1 + sigma (2u - 1)) with u the stream-6 uniform; along a row the threshold
+    falls linearly, f0 - slope |dx| / max(W, H); beyond e = f0 / slope it is 0."""
+    d = _tiny_desc(0)
+    W = d["width"]
+    f0, slope, sig = 2.0, 3.0, 0.25
+    gaze = (3.5, 2.5)  # the centre of pixel (3, 2)
+    fov = I.foveation(gaze, f0, slope, sig)
+    dd = dict(d, foveation=fov)
+    for smp in range(4):
+        u = orc.uniform(d["seed"], 2 * W + 3, smp, 0, 6, 0)
+        assert orc.fov_fmax(dd, 2 * W + 3, smp) == pytest.approx(f0 * (1 + sig * (2 * u - 1)), rel=1e-6)
+    dn = dict(d, foveation=I.foveation(gaze, f0, slope, 0.0))
+    for px in range(W):
+        e = abs(px + 0.5 - gaze[0]) / W
+        assert orc.fov_fmax(dn, 2 * W + px, 0) == pytest.approx(max(0.0, f0 - slope * e), rel=1e-6, abs=1e-7)
+    far = dict(d, foveation=I.foveation((0.0, 0.0), 0.5, 10.0, 0.3))
+    assert orc.fov_fmax(far, 7 * W + 7, 1) == 0.0
 
 
 # ---------------------------------------------------------------- backward (SURVEY §8(f) rank 4, alpha part)
@@ -793,3 +930,30 @@ def test_grad_params_truncated_leibniz(orc):
         assert np.all(np.abs(g[0, 0:3] - dmu) <= 1e-6 * scale), (trial, g[0, 0:3], dmu)
         assert abs(g[0, 10] - dom) <= 1e-6 * max(abs(dom), scale), (trial, g[0, 10], dom)
         assert abs(g[0, 0:3] @ v) <= 1e-6 * scale
+
+
+def test_distance_bands_fold_into_groups(orc):
+    """Config 5's distance bands (C24, fig:army_bunny P:L606-L617): group = band * 10 + g(l, b); a mask
+    selecting one band's groups gives exactly the optical depth of that band's primitives (per-group
+    sums), and a stochastic policy draws once and applies the same weights to every band's copy."""
+    sc = I.scene_cfg5()
+    keep = np.flatnonzero(np.isin(np.arange(sc["n"]) // 33280, [0, 60, 119]))[::40]
+    sub = {k: (v[keep] if isinstance(v, np.ndarray) and v.ndim and len(v) == sc["n"] else v) for k, v in sc.items()}
+    sub["n"] = len(keep)
+    assert set(np.unique(sub["band"]).tolist()) == {0, 1, 2}
+    S = orc.Scene(sub)
+    g, _ = S.groups()
+    np.testing.assert_array_equal(g // 10, sub["band"])
+    rng = np.random.default_rng(5)
+    tgt = sub["mu"][rng.integers(0, sub["n"], 24)]
+    rays = I.pack_rays(tgt - 30 * np.array([0.1, 0.3, 0.95]), np.tile([0.1, 0.3, 0.95], (24, 1)))
+    full = S.trace(rays, want_groups=True)
+    for bd in range(3):
+        m = I.level_mask((0, 1, 2, 3), n_bands=3, bands=[bd])
+        r = S.trace(rays, mask=m)
+        np.testing.assert_allclose(r["tau"], full["groups"][:, 10 * bd:10 * bd + 10].sum(1), rtol=1e-12, atol=1e-15)
+    pol = I.policy(level_strategy=5, beta=0.2, orient_strategy=3)
+    m, w = S.policy_eval(pol, np.array([0.0, 0.6, 0.8]), 0.7, [0.3, 0.5, 0.9], group_f0=S.info()[1])
+    assert m == (m & 0x3FF) * (1 | 1 << 10 | 1 << 20)
+    np.testing.assert_array_equal(w[:10], w[10:20])
+    np.testing.assert_array_equal(w[:10], w[20:30])
