@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 6
+#define GF_ABI_VERSION 7
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -79,32 +79,40 @@ gf_status gf_query_workspace(int64_t n_prims, size_t *prim_bytes, size_t *bvh_by
  *   omega_vec = R S^-1 (omega,omega,omega)^T, >= 0; 0 = Gaussian);
  *   extent[n] whitened truncation radius E (C7/C8), NULL -> 3 (the 3 sigma bound);
  *   level[n] pyramid level (0 = Gaussians), NULL -> derived from level_cutoffs (C10);
- *   bin[n] orientation bin, NULL or 255 -> derived: argmax_k |omega_vec . o_k| in fp32 (C11). */
+ *   bin[n] orientation bin, NULL or 255 -> derived: argmax_k |omega_vec . o_k| in fp32 (C11);
+ *   band[n] spatial band (e.g. the distance band of an instance, config 5, fig:army_bunny
+ *     P:L606-L617), < gf_pyramid.n_bands, NULL -> 0.  Group id = band * G0 + g(level, bin). */
 typedef struct {
     const float *mu, *quat, *scale, *alpha, *omega, *extent;
-    const uint8_t *level, *bin;
+    const uint8_t *level, *bin, *band;
 } gf_prims;
 
 /* Pyramid description, HOST pointers:
- *   n_levels P (1..8), n_bins K (>= 1), G = 1 + (P-1) K <= 32 groups;
- *   group id g(0,*) = 0, g(l,b) = 1 + (l-1) K + b  (C24);
+ *   n_levels P (1..8), n_bins K (>= 1), G0 = 1 + (P-1) K groups per band,
+ *   n_bands B (0 or 1: no bands), G = B G0 <= 32 groups;
+ *   group id g(0,*) = 0, g(l,b) = 1 + (l-1) K + b, plus band * G0  (C24);
  *   bin_axes[3K] unit axes o_k (C11);
  *   level_cutoffs[P-2] ascending world peak frequencies f0 = |omega_vec| separating
  *     Gabor levels 1..P-1 (used only when prims.level == NULL; may be NULL otherwise);
  *   group_f0[G] representative whitened frequency per group for the Importance
- *     orientation strategy (C12); NULL -> 0 (uniform importance). */
+ *     orientation strategy (C12); NULL -> computed by gf_build_bvh on the device:
+ *     sqrt(3) x the median omega of the group's level (even count: fp32 mean of the
+ *     two middle values), the same for every bin and band of the level. */
 typedef struct {
     int32_t n_levels;
     int32_t n_bins;
     const float *bin_axes;
     const float *level_cutoffs;
     const float *group_f0;
+    int32_t n_bands;
 } gf_pyramid;
 
 /* Convert n primitives into the 64-byte device records (W = S^-1 R^T whitening,
- * c = alpha/(2 pi s1 s2 s3), E^2, group) stored in prim_ws (device, >= prim_bytes).
- * Validates on the device and synchronises `stream`; returns the first error
- * class found (GF_E_SINGULAR_COVARIANCE, GF_E_INVALID_BOUNDS, GF_E_ASSIGNMENT).
+ * c = alpha/(2 pi s1 s2 s3), E^2, group) stored in prim_ws (device, >= prim_bytes),
+ * and derive the per-level maximum world frequency max |omega_vec| (reading F3, used by
+ * foveated rendering; gf_scene_info).  Validates on the device and synchronises
+ * `stream`; returns the first error class found (GF_E_SINGULAR_COVARIANCE,
+ * GF_E_INVALID_BOUNDS, GF_E_ASSIGNMENT: level/bin/band out of range or |q| != 1).
  * n == 0 is valid (empty scene: every ray has tau = 0). Invalidates the BVH. */
 gf_status gf_load_primitives(gf_ctx *ctx, const gf_prims *prims, int64_t n, const gf_pyramid *pyr,
                              void *prim_ws, size_t prim_ws_bytes, gf_stream stream);
@@ -120,6 +128,38 @@ gf_status gf_load_primitives(gf_ctx *ctx, const gf_prims *prims, int64_t n, cons
  * reused after the call.  Synchronises `stream`. */
 gf_status gf_build_bvh(gf_ctx *ctx, void *bvh_ws, size_t bvh_ws_bytes, void *scratch, size_t scratch_bytes,
                        gf_stream stream);
+
+/* Scene-derived quantities (synchronous; after gf_load_primitives, the BVH fields after
+ * gf_build_bvh).  bvh_hash: a 64-bit hash of the whole BVH workspace (nodes, child pairs,
+ * reordered primitives, permutation), equal on every rank that built the same scene -- the
+ * multi-GPU replica check; 0 before gf_build_bvh. */
+typedef struct {
+    int64_t n_prims;
+    int32_t n_levels, n_bins, n_bands, n_groups;
+    float level_fmax[8];    /* max |omega_vec| per level (F3); [0] = 0 (Gaussians)          */
+    float group_f0[32];     /* the Importance strategy's f0 per group (C12), as used        */
+    float root_lo[3], root_hi[3];
+    uint32_t n_nodes, max_depth;
+    uint64_t bvh_hash;
+} gf_scene_info;
+gf_status gf_scene_info_get(gf_ctx *ctx, gf_scene_info *out);
+
+/* Accelerated motion blur (readings M1-M3): for a blur of
+ * length m along dir (host float[3], normalised here), per group the mean of its members'
+ * omega_vec (signs aligned with the member of largest |omega_vec|) -> k = |mean . dir| -> box-filter
+ * attenuation |sin(m k/2) / (m k/2)|; *mask_out (host) = the groups with attenuation >= threshold
+ * (level-0 and empty groups always kept), att_out (host, n_groups floats, nullable) the
+ * attenuations.  Device reductions over the loaded primitives; synchronous. */
+gf_status gf_motion_blur_mask(gf_ctx *ctx, const float *dir, float m, float threshold, uint32_t *mask_out,
+                              float *att_out);
+
+/* Adaptive clamping (Eq. 15; reading C8'): per primitive the whitened extent
+ *   E = min(3, sqrt(max(0, -2 ln(eps 2 pi s1 s2 s3 / (alpha s_max)) - 3 omega^2))), floored at 1e-3,
+ * beyond which the worst-case untruncated line integral is below eps.  scale[3n], alpha[n],
+ * omega[n]: device inputs as for gf_load_primitives; extent_out: device n floats (the `extent`
+ * input of a later gf_load_primitives).  Asynchronous on `stream`. */
+gf_status gf_adaptive_extent(gf_ctx *ctx, const float *scale, const float *alpha, const float *omega, int64_t n,
+                             float eps, float *extent_out, gf_stream stream);
 
 /* ---- a3: LOD policy (Tables B1/B2) ------------- */
 typedef enum {
@@ -148,7 +188,7 @@ typedef struct {
 gf_status gf_set_lod_mask(gf_ctx *ctx, const gf_lod_policy *ext, const gf_lod_policy *nee);
 
 /* ---- a4-a7: masked traversal + fused line integral + transmittance -------- */
-/* rays: device, n x 8 fp32 (ox,oy,oz,tmin, dx,dy,dz,tmax), |d| = 1, tmin < tmax,
+/* rays: device, 16-byte aligned, n x 8 fp32 (ox,oy,oz,tmin, dx,dy,dz,tmax), |d| = 1, tmin < tmax,
  * tmax may be +inf.  tau_out: device n fp32 optical depth tau = sum_i w_g alpha_i
  * int_tmin^tmax K_i (Eq. 2, App. A closed form, C3-C5), accumulated in fp64.
  * T_out: device n fp32 exp(-tau) (Eq. 3) or NULL.  The `ext` policy applies;
@@ -180,7 +220,7 @@ gf_status gf_trace_grad_alpha(gf_ctx *ctx, const float *rays, int64_t n, uint64_
  * chord ends that move with the ellipsoid, C7) -- rays, policy and draws as
  * gf_trace_transmittance.  flags: 0 (one warp per ray) or GF_TRACE_PACKETS (32 consecutive rays walk
  * the BVH together and sum each primitive's terms across the warp before one set of atomics: faster
- * for coherent rays, correct for any; E_INVALID_ARGUMENT for other bits).  accum: device n_prims x 16 fp32, input order, caller-zeroed,
+ * for coherent rays, correct for any; E_INVALID_ARGUMENT for other bits).  accum: device n_prims x 16 fp32 (16-byte aligned), input order, caller-zeroed,
  * accumulated across calls: [0..2] d/dmu, [3..11] d/dW (row-major), [12] d/domega, [13] d/dalpha,
  * [14] sum dl tau_ri (the |det W| part), [15] unused.
  *
@@ -194,6 +234,22 @@ gf_status gf_trace_grad_alpha(gf_ctx *ctx, const float *rays, int64_t n, uint64_
 gf_status gf_trace_grad_params(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, uint32_t flags,
                                const float *dl_dtau, float *accum, gf_stream stream);
 gf_status gf_grad_params_finish(gf_ctx *ctx, const float *accum, const float *quat, float *grad, gf_stream stream);
+
+/* Free-flight distance sampling of single rays (a8, Eq. 5; test / measurement path of
+ * the kernels gf_render uses): for ray i, xi = uniform (seed, pixel = i, sample 0, depth 0, stream 0,
+ * k = 0), tau* = -ln(1 - xi), and t_out[i] = the first t in [tmin, tmax] at which the
+ * optical depth of the `ext`-masked field reaches tau* (C17: the first of the gf_free_flight_bins()
+ * equal t-bins of the ray's scene interval -- the root box within [tmin, tmax] -- whose right edge
+ * reaches tau*, then the root inside it), +inf if no bin edge reaches tau* (escape).  rays as gf_trace_transmittance (tmax = +inf allowed); t_out: device n floats.
+ * flags: 0, or GF_TRACE_PACKETS (32 consecutive rays walk the BVH together, as gf_render's camera
+ * rays do).  scratch: device, >= gf_free_flight_scratch_bytes(n). */
+gf_status gf_trace_free_flight(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, uint32_t flags,
+                               float *t_out, void *scratch, size_t scratch_bytes, gf_stream stream);
+/* Number of t-bins of the free-flight pass A (reading C17: t* is the root inside the first of these
+ * equal bins of the ray's scene interval whose right edge reaches tau*). */
+int gf_free_flight_bins(void);
+/* Device scratch gf_trace_free_flight needs for n rays (per-path state of <= 2^20 rays at a time). */
+gf_status gf_free_flight_scratch_bytes(gf_ctx *ctx, int64_t n, size_t *bytes);
 
 /* Candidate sets (test path, C21): for each ray, the ORIGINAL indices of the
  * primitives accepted by the fp32 ellipsoid predicate (traversal order),
@@ -223,6 +279,8 @@ typedef enum { GF_SHARD_NONE = 0, GF_SHARD_TILES = 1, GF_SHARD_SAMPLES = 2 } gf_
  *   step j of a segment uses Philox block k = 4j of stream 4 (free flight: u0 distance, u1
  *   acceptance) or stream 5 (NEE: u0 distance). */
 typedef enum { GF_EST_ANALYTIC = 0, GF_EST_TRACKING = 1 } gf_estimator;
+#define GF_FOV_LEVELS 1u
+#define GF_FOV_CONTINUOUS 2u
 typedef struct {
     int32_t mode;               /* gf_render_mode */
     int32_t width, height;
@@ -239,16 +297,16 @@ typedef struct {
     int32_t estimator;          /* gf_estimator (SCATTER) */
     int32_t reuse_accel;        /* 1: reuse the light / camera BVHs left in scratch by the previous
                                    call (see gf_render); 0: rebuild them */
-    /* Foveated rendering (readings F1-F5): foveation = 1
+    /* Foveated rendering (readings F1-F5): foveation != 0
      * gives every path of pixel (px, py) the frequency threshold
      *   f_max = max(0, fov_f0 - fov_slope e) (1 + fov_jitter (2u - 1)),
      *   e = |(px + 0.5, py + 0.5) - fov_gaze| / max(W, H),  u = uniform of stream 6, k = 0, depth 0;
-     * Gabor levels l with fov_level_fmax[l] > f_max are masked (level 0 never), and a primitive
-     * whose frequency along the ray |omega_vec . d| exceeds f_max is not integrated. */
+     * mode bit 0 (GF_FOV_LEVELS): Gabor levels whose maximum frequency (gf_scene_info.level_fmax)
+     * exceeds f_max are masked (level 0 never); bit 1 (GF_FOV_CONTINUOUS): a primitive whose
+     * frequency along the ray |omega_vec . d| exceeds f_max is not integrated.  3 = both. */
     int32_t foveation;
     float fov_gaze[2];          /* gaze point in pixels */
     float fov_f0, fov_slope, fov_jitter;
-    float fov_level_fmax[8];    /* maximum world frequency |omega_vec| of each level (index 0 unused) */
     /* Motion-blur reference (readings M1-M3):
      * motion_blur = 1 renders the field moving along mb_dir by mb_m during the exposure, a box
      * filter of length mb_m: each (pixel, sample) draws u (stream 7, k = 0, depth 0) and the field
@@ -268,32 +326,33 @@ gf_status gf_render_scratch_bytes(gf_ctx *ctx, const gf_render_desc *desc, size_
  *     (only the shard's pixels/samples are touched; caller zeroes it);
  *   probes: n_probe * spp_count, accum[i*spp_count + k] = estimate of sample
  *     spp_begin + k at probe i (overwritten).
- * ray_counts: device uint64[2] or NULL, += (camera+extension rays, NEE rays).
+ * ray_counts: device uint64[3] or NULL, += (camera rays, extension rays, NEE rays).
  * scratch also holds two acceleration structures gf_render builds on the stream: the light BVH
  *   (boxes in the light's frame, for NEE) and, for static camera masks, the camera BVH
  *   (projective boxes at the eye, for the camera rays).  With desc->reuse_accel = 1 they are
  *   reused when this call has the same scratch pointer, scene (no gf_load_primitives /
  *   gf_build_bvh in between), light and camera as the one that built them: the caller
- *   guarantees that scratch was not written in between. */
+ *   guarantees that scratch was not written in between by anything but gf_render calls of this
+ *   context (a gf_render call with a different chunk layout of the same scratch invalidates them). */
 gf_status gf_render(gf_ctx *ctx, const gf_render_desc *desc, float *accum, void *scratch, size_t scratch_bytes,
                     uint64_t *ray_counts, gf_stream stream);
 
 /* ---- measurement (bench.py roofline / launch counts) ---------------------- */
 #define GF_PROFILE_TIMING 1u  /* record CUDA events around every kernel launch (on its stream)   */
 #define GF_PROFILE_WORK 2u    /* use the counting kernel variants (work[] below; slower)          */
-/* Stages: 0 gen (camera rays), 1 ff (free flight, k_ff: traversal -> hit records -> tau_total ->
- * root of tau(t) = tau*), 2 ff_fallback (single-pass free flight for paths with more hit records
- * than the record buffer), 3 nee (shadow rays + phase sampling), 4 finish (queue rotation +
- * accumulation), 5 tomo, 6 trace (gf_trace_transmittance), 7 unused.  work[s][0] counts node box
- * tests (the warp traversal tests both children of a popped node). */
+/* Stages: 0 gen (camera rays), 1 ffA (free flight pass A: tau of the whole ray into 32 exact t-bins,
+ * escape test, the bin of the first crossing), 2 ffB (pass B: that bin's chords -> root of tau(t) = tau*),
+ * 3 nee (shadow rays + phase sampling), 4 finish (queue rotation + accumulation), 5 tomo,
+ * 6 trace (gf_trace_transmittance), 7 unused.  work[s][0] counts node box tests (the warp traversal
+ * tests both children of a popped node). */
 typedef struct {
     uint64_t launches;           /* kernels launched by the library since the last reset        */
     uint64_t stage_launches[8];
     double stage_ms[8];          /* summed event time per stage (GF_PROFILE_TIMING)             */
     uint64_t work[8][12];        /* GF_PROFILE_WORK, per stage: nodes visited, primitives tested,
                                     hits, complex-erf endpoint evaluations (Eq. 13 series), real
-                                    erf evaluations (Omega = 0), Gauss-Legendre fallbacks, ffB
-                                    overflow brackets, root-finder evaluations, paths/rays, 3 spare */
+                                    erf evaluations (Omega = 0), Gauss-Legendre fallbacks, pass-B
+                                    window halvings, root-finder evaluations, paths/rays, 3 spare */
 } gf_stats;
 gf_status gf_set_profiling(gf_ctx *ctx, uint32_t flags);
 /* Synchronises the context's device, fills *out, optionally resets the counters. */

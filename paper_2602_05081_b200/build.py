@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libgf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["gf_api.cu", "gf_build.cu", "gf_trace.cu", "gf_render.cu"]
+SOURCES = ["gf_api.cu", "gf_build.cu", "gf_trace.cu", "gf_render.cu", "gf_ffa_pkt.cu", "gf_ffa_w.cu", "gf_ffb.cu", "gf_ff.cu", "gf_nee.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
@@ -53,6 +53,11 @@ def build(force=False, verbose=False, defines=(), lib=None, flags=()):
         for s in SOURCES:
             print(open(os.path.join(obj_dir, s + ".ptxas.txt")).read())
     return lib
+
+
+def build_checked():
+    """Debug variant with the device bounds checks (GF_DEBUG_CHECKS): variants/libgf_checked.so."""
+    return build(defines=["GF_DEBUG_CHECKS"], lib=os.path.join(HERE, "variants", "libgf_checked.so"))
 
 
 if __name__ == "__main__":

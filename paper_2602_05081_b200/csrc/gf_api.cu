@@ -17,7 +17,13 @@ struct gf_ctx {
     int device = 0;
     std::string err;
     uint32_t* d_err = nullptr;            // [4] load error bits, first bad index
-    unsigned long long* d_rays = nullptr;  // [2] dummy ray counters
+    unsigned long long* d_rays = nullptr;  // [3] dummy ray counters
+    uint32_t* d_lfmax = nullptr;           // [8] per-level max |omega_vec| (float bits, F3)
+    float* d_f0 = nullptr;                 // [8] per-level representative whitened frequency (C12)
+    void* d_mb = nullptr;                  // motion-blur reduction scratch
+    unsigned long long* d_hash = nullptr;  // BVH hash
+    float lfmax[8] = {};
+    bool f0_given = false;
     // scene
     bool loaded = false, built = false;
     int64_t n = 0;
@@ -43,30 +49,43 @@ struct gf_ctx {
     // scene generation (bumped by load/build) and the frame BVHs gf_render left in a scratch buffer
     uint64_t gen = 0;
     struct FrameCache {
-        const void* where = nullptr;  // node array inside the scratch
+        const char* base = nullptr;   // scratch buffer the BVH was built in
+        size_t layout = 0;            // its chunk layout (bytes of the render state)
         uint64_t gen = ~0ull;
         float key[12] = {};
     } light_cache[4], cam_cache[4];  // per scratch buffer (up to 4 in flight, e.g. one per stream)
 };
 
-// true if the frame BVH (node array at `where`, scene generation, key floats) is already there;
+// A gf_render call writes [base, base + layout) of its scratch: drop every cached frame BVH that
+// another layout placed inside that range (its nodes are overwritten by this call's per-path state).
+static void frame_invalidate(gf_ctx::FrameCache* fcs, const char* base, size_t layout) {
+    for (int i = 0; i < 4; ++i) {
+        gf_ctx::FrameCache& f = fcs[i];
+        if (!f.base || (f.base == base && f.layout == layout)) continue;
+        if (f.base < base + layout && base < f.base + f.layout) f = gf_ctx::FrameCache{};
+    }
+}
+// true if the frame BVH of (scratch base, layout, scene generation, key floats) is already there;
 // otherwise records it as built now
-static bool frame_cached(gf_ctx::FrameCache* fcs, const void* where, uint64_t gen, const float* key, int nkey) {
+static bool frame_cached(gf_ctx::FrameCache* fcs, const char* base, size_t layout, uint64_t gen, const float* key,
+                         int nkey) {
+    frame_invalidate(fcs, base, layout);
     gf_ctx::FrameCache* fc = nullptr;
     for (int i = 0; i < 4 && !fc; ++i)
-        if (fcs[i].where == where) fc = fcs + i;
+        if (fcs[i].base == base && fcs[i].layout == layout) fc = fcs + i;
     if (!fc) {  // new scratch buffer: take a free slot, else the first (round robin)
         for (int i = 0; i < 4 && !fc; ++i)
-            if (!fcs[i].where) fc = fcs + i;
+            if (!fcs[i].base) fc = fcs + i;
         if (!fc) {
             for (int i = 0; i < 3; ++i) fcs[i] = fcs[i + 1];
             fc = fcs + 3;
         }
         fc->gen = ~0ull;
     }
-    bool same = fc->where == where && fc->gen == gen;
+    bool same = fc->base == base && fc->layout == layout && fc->gen == gen;
     for (int k = 0; k < nkey && same; ++k) same = fc->key[k] == key[k];
-    fc->where = where;
+    fc->base = base;
+    fc->layout = layout;
     fc->gen = gen;
     for (int k = 0; k < nkey; ++k) fc->key[k] = key[k];
     return same;
@@ -199,7 +218,11 @@ gf_status gf_create(int cuda_device, gf_ctx** out) {
     gf_ctx* c = new gf_ctx();
     c->device = cuda_device;
     if (cudaMalloc(&c->d_err, 4 * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&c->d_rays, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->d_rays, 3 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->d_lfmax, 8 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&c->d_f0, 8 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&c->d_mb, gf_mb_scratch_bytes()) != cudaSuccess ||
+        cudaMalloc(&c->d_hash, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&c->d_work, 8 * kWorkSlots * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(c->d_work, 0, 8 * kWorkSlots * sizeof(unsigned long long)) != cudaSuccess) {
         delete c;
@@ -218,6 +241,10 @@ void gf_destroy(gf_ctx* c) {
     for (cudaEvent_t e : c->timer.pool) cudaEventDestroy(e);
     cudaFree(c->d_err);
     cudaFree(c->d_rays);
+    cudaFree(c->d_lfmax);
+    cudaFree(c->d_f0);
+    cudaFree(c->d_mb);
+    cudaFree(c->d_hash);
     cudaFree(c->d_work);
     delete c;
 }
@@ -248,9 +275,10 @@ gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_p
     if (n >= (1 << 24)) return fail(c, GF_E_INVALID_ARGUMENT, "n must be < 2^24");
     if (n > 0 && (!p->mu || !p->quat || !p->scale || !p->alpha || !p->omega || !prim_ws))
         return fail(c, GF_E_INVALID_ARGUMENT, "null primitive array");
-    const int P = pyr->n_levels, K = pyr->n_bins;
-    if (P < 1 || P > kMaxLevels || K < 1 || K > 16) return fail(c, GF_E_INVALID_ARGUMENT, "bad n_levels / n_bins");
-    if (1 + (P - 1) * K > GF_MAX_GROUPS) return fail(c, GF_E_MASK_OVERFLOW, "1 + (P-1) K > 32 groups");
+    const int P = pyr->n_levels, K = pyr->n_bins, B = std::max(1, (int)pyr->n_bands);
+    if (P < 1 || P > kMaxLevels || K < 1 || K > 16 || pyr->n_bands < 0)
+        return fail(c, GF_E_INVALID_ARGUMENT, "bad n_levels / n_bins / n_bands");
+    if (B * (1 + (P - 1) * K) > GF_MAX_GROUPS) return fail(c, GF_E_MASK_OVERFLOW, "n_bands (1 + (P-1) K) > 32 groups");
     if (!pyr->bin_axes) return fail(c, GF_E_INVALID_ARGUMENT, "bin_axes required");
     if (n > 0 && !p->level && P > 2 && !pyr->level_cutoffs)
         return fail(c, GF_E_INVALID_ARGUMENT, "level_cutoffs required when level == NULL");
@@ -263,15 +291,17 @@ gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_p
     c->loaded = c->built = false;
     LoadArgs A{};
     A.n = n; A.mu = p->mu; A.quat = p->quat; A.scale = p->scale; A.alpha = p->alpha; A.omega = p->omega;
-    A.extent = p->extent; A.level = p->level; A.bin = p->bin; A.P = P; A.K = K;
+    A.extent = p->extent; A.level = p->level; A.bin = p->bin; A.band = p->band; A.P = P; A.K = K; A.n_bands = B;
     for (int i = 0; i < P - 2 && pyr->level_cutoffs; ++i) A.cutoffs[i] = pyr->level_cutoffs[i];
     for (int i = 0; i < 3 * K; ++i) A.axes[i] = pyr->bin_axes[i];
     uint32_t init[4] = {0u, 0xFFFFFFFFu, 0u, 0u};
     GF_CUDA(c, cudaMemcpyAsync(c->d_err, init, sizeof(init), cudaMemcpyHostToDevice, st), "memcpy");
     uint8_t* gptr = (uint8_t*)prim_ws + align256(sizeof(GPrim) * (size_t)std::max<int64_t>(n, 1));
-    GF_CUDA(c, gf_launch_load(A, prim_ws, gptr, c->d_err, st), "k_load_prims");
-    uint32_t herr[4];
+    GF_CUDA(c, cudaMemsetAsync(c->d_lfmax, 0, 8 * sizeof(uint32_t), st), "memset");
+    GF_CUDA(c, gf_launch_load(A, prim_ws, gptr, c->d_err, c->d_lfmax, st), "k_load_prims");
+    uint32_t herr[4], hlf[8];
     GF_CUDA(c, cudaMemcpyAsync(herr, c->d_err, sizeof(herr), cudaMemcpyDeviceToHost, st), "memcpy");
+    GF_CUDA(c, cudaMemcpyAsync(hlf, c->d_lfmax, sizeof(hlf), cudaMemcpyDeviceToHost, st), "memcpy");
     GF_CUDA(c, cudaStreamSynchronize(st), "load sync");
     if (herr[0]) {
         char msg[160];
@@ -282,9 +312,11 @@ gf_status gf_load_primitives(gf_ctx* c, const gf_prims* p, int64_t n, const gf_p
         return fail(c, GF_E_INVALID_ARGUMENT, msg);
     }
     c->n = n;
-    c->sc.P = P; c->sc.K = K; c->sc.G = 1 + (P - 1) * K;
+    c->sc.P = P; c->sc.K = K; c->sc.G0 = 1 + (P - 1) * K; c->sc.n_bands = B; c->sc.G = B * c->sc.G0;
     for (int i = 0; i < 3 * K; ++i) c->sc.axes[i] = pyr->bin_axes[i];
+    c->f0_given = pyr->group_f0 != nullptr;  // else medians computed by gf_build_bvh (C12)
     for (int g = 0; g < kMaxGroups; ++g) c->sc.f0[g] = (pyr->group_f0 && g < c->sc.G) ? pyr->group_f0[g] : 0.0f;
+    for (int l = 0; l < 8; ++l) { float f; std::memcpy(&f, hlf + l, 4); c->lfmax[l] = f; }
     c->prims = (GPrim*)prim_ws;
     c->group = gptr;
     c->dext = make_policy_dev(c->ext, P);
@@ -313,6 +345,16 @@ gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch,
     c->nodes2 = (GNode2*)(base + align256(sizeof(GPrim) * n1) + align256(sizeof(GNode) * 2 * n1) +
                           align256(sizeof(int32_t) * n1));
     BuildScratch S = gf_scratch_layout(c->n, (char*)scratch);
+    if (!c->f0_given) {  // C12: sqrt(3) x the median omega of each level, on the device (radix sort)
+        float f0l[8];
+        GF_CUDA(c, gf_launch_group_f0(c->prims, c->group, c->n, c->sc.P, c->sc.K, c->sc.G0, S, c->d_f0, st), "group f0");
+        GF_CUDA(c, cudaMemcpyAsync(f0l, c->d_f0, sizeof(f0l), cudaMemcpyDeviceToHost, st), "memcpy");
+        GF_CUDA(c, cudaStreamSynchronize(st), "group f0 sync");
+        for (int g = 0; g < kMaxGroups; ++g) {
+            const int gl = g % c->sc.G0;
+            c->sc.f0[g] = (g < c->sc.G && gl > 0) ? f0l[1 + (gl - 1) / c->sc.K] : 0.0f;
+        }
+    }
     uint32_t nn = 0, md = 0;
     GF_CUDA(c, gf_launch_build(c->prims, c->group, c->n, S, c->nodes, c->nodes2, c->sorted, c->perm, &nn, &md, c->root,
                                st),
@@ -324,6 +366,70 @@ gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch,
     c->stk_limit = kWStk - 34 - (int)md;
     c->built = true;
     ++c->gen;
+    return GF_OK;
+}
+
+gf_status gf_scene_info_get(gf_ctx* c, gf_scene_info* out) {
+    if (!c || !out) return GF_E_INVALID_ARGUMENT;
+    if (!c->loaded) return fail(c, GF_E_STATE, "gf_scene_info_get before gf_load_primitives");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    std::memset(out, 0, sizeof(*out));
+    out->n_prims = c->n;
+    out->n_levels = c->sc.P;
+    out->n_bins = c->sc.K;
+    out->n_bands = c->sc.n_bands;
+    out->n_groups = c->sc.G;
+    for (int l = 0; l < 8; ++l) out->level_fmax[l] = c->lfmax[l];
+    for (int g = 0; g < kMaxGroups; ++g) out->group_f0[g] = c->built || c->f0_given ? c->sc.f0[g] : 0.0f;
+    if (c->built) {
+        for (int k = 0; k < 3; ++k) { out->root_lo[k] = c->root[k]; out->root_hi[k] = c->root[3 + k]; }
+        out->n_nodes = c->n_nodes;
+        out->max_depth = c->max_depth;
+        // hash of the tree as built: reordered primitives, nodes, permutation (the child pairs are
+        // derived from the nodes; unused tails of the workspace are not hashed)
+        cudaStream_t st = nullptr;
+        GF_CUDA(c, cudaMemsetAsync(c->d_hash, 0, sizeof(unsigned long long), st), "memset");
+        unsigned long long h = 0, part = 0;
+        const struct { const void* p; size_t b; } parts[3] = {
+            {c->sorted, sizeof(GPrim) * (size_t)c->n}, {c->nodes, sizeof(GNode) * (size_t)c->n_nodes},
+            {c->perm, sizeof(int32_t) * (size_t)c->n}};
+        for (const auto& pt : parts) {
+            GF_CUDA(c, gf_launch_hash(pt.p, pt.b, c->d_hash, st), "hash");
+            GF_CUDA(c, cudaMemcpy(&part, c->d_hash, sizeof(part), cudaMemcpyDeviceToHost), "memcpy");
+            h = h * 0x100000001B3ull + part;
+        }
+        out->bvh_hash = h;
+    }
+    return GF_OK;
+}
+
+gf_status gf_motion_blur_mask(gf_ctx* c, const float* dir, float m, float threshold, uint32_t* mask_out,
+                              float* att_out) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (!dir || !mask_out) return fail(c, GF_E_INVALID_ARGUMENT, "null dir / mask_out");
+    if (!c->loaded) return fail(c, GF_E_STATE, "gf_motion_blur_mask before gf_load_primitives");
+    if (!(m >= 0.0f) || !std::isfinite(m) || !std::isfinite(threshold) ||
+        !(std::fabs(dir[0]) + std::fabs(dir[1]) + std::fabs(dir[2]) > 0.0f))
+        return fail(c, GF_E_INVALID_ARGUMENT, "motion blur: m >= 0 finite, dir != 0");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    GF_CUDA(c, gf_launch_mb_mask(c->prims, c->group, c->n, c->sc.G, c->sc.G0, dir, m, threshold, c->d_mb, mask_out,
+                                 att_out, nullptr),
+            "motion-blur mask");
+    return GF_OK;
+}
+
+gf_status gf_adaptive_extent(gf_ctx* c, const float* scale, const float* alpha, const float* omega, int64_t n, float eps,
+                             float* extent_out, gf_stream stream) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (n < 0 || (n > 0 && (!scale || !alpha || !omega || !extent_out)))
+        return fail(c, GF_E_INVALID_ARGUMENT, "bad adaptive-extent arrays");
+    if (!(eps > 0.0f) || !std::isfinite(eps)) return fail(c, GF_E_INVALID_ARGUMENT, "eps must be > 0");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    GF_CUDA(c, gf_launch_adaptive_extent(scale, alpha, omega, n, eps, extent_out, (cudaStream_t)stream),
+            "k_adaptive_extent");
     return GF_OK;
 }
 
@@ -346,6 +452,7 @@ static gf_status trace_common(gf_ctx* c, const float* rays, int64_t n, TraceArgs
     if (!c->loaded || (!c->built && !(flags & GF_TRACE_BRUTE_FORCE)))
         return fail(c, GF_E_STATE, "trace before gf_load_primitives / gf_build_bvh");
     if (n < 0 || (n > 0 && !rays)) return fail(c, GF_E_INVALID_ARGUMENT, "bad rays");
+    if (((uintptr_t)rays & 15u) != 0) return fail(c, GF_E_INVALID_ARGUMENT, "rays must be 16-byte aligned");
     GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
     if (gf_status s = check_sticky(c)) return s;
     A = TraceArgs{};
@@ -406,6 +513,7 @@ gf_status gf_trace_grad_params(gf_ctx* c, const float* rays, int64_t n, uint64_t
     if (gf_status s = trace_common(c, rays, n, A, 0u)) return s;
     if (!c->built) return fail(c, GF_E_STATE, "gf_trace_grad_params before gf_build_bvh");
     if (n > 0 && (!dl_dtau || !accum)) return fail(c, GF_E_INVALID_ARGUMENT, "null gradient buffers");
+    if (((uintptr_t)accum & 15u) != 0) return fail(c, GF_E_INVALID_ARGUMENT, "accum must be 16-byte aligned");
     A.seed = seed;
     GF_CUDA(c, gf_launch_grad_params(A, dl_dtau, accum, (flags & GF_TRACE_PACKETS) != 0, (cudaStream_t)stream),
             "k_grad_params");
@@ -438,7 +546,7 @@ gf_status gf_trace_candidates(gf_ctx* c, const float* rays, int64_t n, uint32_t 
 #ifndef GF_CHUNK_LOG2
 #define GF_CHUNK_LOG2 20
 #endif
-static constexpr int64_t kRenderChunk = 1ll << GF_CHUNK_LOG2;  // paths per wavefront chunk (scratch ~34 GB at 2^20)
+static constexpr int64_t kRenderChunk = 1ll << GF_CHUNK_LOG2;  // paths per wavefront chunk (per-path state ~50 MB at 2^20)
 
 static int64_t render_paths(const gf_render_desc* d) {
     if (d->probe_pixels) return d->n_probe;
@@ -468,6 +576,7 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
         return fail(c, GF_E_INVALID_ARGUMENT, "bad estimator");
     if (d->motion_blur && !(d->mb_m >= 0.0f && std::isfinite(d->mb_m)))
         return fail(c, GF_E_INVALID_ARGUMENT, "motion blur: mb_m must be finite and >= 0");
+    if (d->foveation < 0 || d->foveation > 3) return fail(c, GF_E_INVALID_ARGUMENT, "foveation: mode bits 0..3");
     if (d->foveation && !(d->fov_f0 >= 0.0f && d->fov_slope >= 0.0f && d->fov_jitter >= 0.0f && d->fov_jitter < 1.0f))
         return fail(c, GF_E_INVALID_ARGUMENT, "foveation: f0, slope >= 0 and jitter in [0,1)");
     return GF_OK;
@@ -496,6 +605,9 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     RenderDev R{};
     BuildScratch LS;
     gf_render_state_bytes(chunk, c->n, (char*)scratch, &R, &LS);
+    // this call writes [scratch, scratch + need): frame BVHs another layout left there are gone
+    frame_invalidate(c->light_cache, (const char*)scratch, need);
+    frame_invalidate(c->cam_cache, (const char*)scratch, need);
     R.rec_cap = std::max(0, std::min(R.rec_cap, env_int("GF_DEBUG_REC_CAP", R.rec_cap)));
     R.nodes = c->nodes;
     R.nodes2 = c->nodes2;
@@ -517,10 +629,10 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.max_depth = d->mode == GF_MODE_SCATTER ? d->max_depth : 1;
     R.jitter = d->jitter;
     R.estimator = d->estimator;
-    R.fov = d->foveation != 0;
+    R.fov = d->foveation;
     R.fov_gaze[0] = d->fov_gaze[0]; R.fov_gaze[1] = d->fov_gaze[1];
     R.fov_f0 = d->fov_f0; R.fov_slope = d->fov_slope; R.fov_jitter = d->fov_jitter;
-    for (int k = 0; k < 8; ++k) R.fov_lfmax[k] = d->fov_level_fmax[k];
+    for (int k = 0; k < 8; ++k) R.fov_lfmax[k] = c->lfmax[k];  // F3: the library's per-level maxima
     R.mb = d->motion_blur != 0;
     for (int k = 0; k < 3; ++k) R.mb_dir[k] = d->mb_dir[k];
     R.mb_m = d->mb_m;
@@ -555,7 +667,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         for (int k = 0; k < 3; ++k) {
             R.lf[k] = (float)x[k]; R.lf[3 + k] = (float)y[k]; R.lf[6 + k] = (float)z[k];
         }
-        if (!frame_cached(c->light_cache, R.lnodes, c->gen, R.lf, 9) || !d->reuse_accel) {
+        if (!frame_cached(c->light_cache, (const char*)scratch, need, c->gen, R.lf, 9) || !d->reuse_accel) {
             GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.lf, nullptr, R.lnodes, R.lnodes2,
                                              R.lprims, R.lperm, R.ldepth, st),
                     "light BVH build");
@@ -567,6 +679,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
              env_int("GF_DEBUG_NO_CAMERA_BVH", 0) == 0;  // (motion blur moves the eye per sample)
     // packets pay off once the chunk fills the GPU (small images: one warp per pixel, k_tomo_w)
     R.tomo_pkt_min = env_int("GF_DEBUG_TOMO_PKT_MIN", 1 << 16);
+    R.ffb_cam = env_int("GF_FFB_CAM", 1);
     if (R.camb) {
         const float* axes[3] = {d->cam_right, d->cam_up, d->cam_fwd};
         for (int a = 0; a < 3; ++a) {
@@ -577,7 +690,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         float key[12];
         for (int k = 0; k < 9; ++k) key[k] = R.cb[k];
         for (int k = 0; k < 3; ++k) key[9 + k] = d->cam_pos[k];
-        if (!frame_cached(c->cam_cache, R.cnodes, c->gen, key, 12) || !d->reuse_accel) {
+        if (!frame_cached(c->cam_cache, (const char*)scratch, need, c->gen, key, 12) || !d->reuse_accel) {
             GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.cb, d->cam_pos, R.cnodes, R.cnodes2,
                                              R.cprims, R.cperm, R.cdepth, st),
                     "camera BVH build");
@@ -594,6 +707,58 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         }
     }
     if (c->timer.recs.size() > 4096) harvest(c);  // bound the event pool
+    return GF_OK;
+}
+
+gf_status gf_free_flight_scratch_bytes(gf_ctx* c, int64_t n, size_t* bytes) {
+    if (!c || !bytes || n < 0) return GF_E_INVALID_ARGUMENT;
+    *bytes = gf_render_state_bytes(std::min<int64_t>(std::max<int64_t>(n, 1), kRenderChunk), 0, nullptr, nullptr, nullptr);
+    return GF_OK;
+}
+
+gf_status gf_trace_free_flight(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, uint32_t flags, float* t_out,
+                               void* scratch, size_t scratch_bytes, gf_stream stream) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (flags & ~GF_TRACE_PACKETS) return fail(c, GF_E_INVALID_ARGUMENT, "bad gf_trace_free_flight flags");
+    if (!c->loaded || !c->built) return fail(c, GF_E_STATE, "free flight before gf_load_primitives / gf_build_bvh");
+    if (n < 0 || (n > 0 && (!rays || !t_out || !scratch))) return fail(c, GF_E_INVALID_ARGUMENT, "bad buffers");
+    if (((uintptr_t)rays & 15u) != 0) return fail(c, GF_E_INVALID_ARGUMENT, "rays must be 16-byte aligned");
+    const int64_t chunk = std::min<int64_t>(std::max<int64_t>(n, 1), kRenderChunk);
+    const size_t need = gf_render_state_bytes(chunk, 0, nullptr, nullptr, nullptr);
+    if (scratch_bytes < need) return fail(c, GF_E_OUT_OF_MEMORY, "free-flight scratch too small");
+    GF_CUDA(c, cudaSetDevice(c->device), "cudaSetDevice");
+    if (gf_status s = check_sticky(c)) return s;
+    RenderDev R{};
+    gf_render_state_bytes(chunk, 0, (char*)scratch, &R, nullptr);
+    frame_invalidate(c->light_cache, (const char*)scratch, need);
+    frame_invalidate(c->cam_cache, (const char*)scratch, need);
+    R.rec_cap = std::max(0, std::min(R.rec_cap, env_int("GF_DEBUG_REC_CAP", R.rec_cap)));
+    R.nodes = c->nodes;
+    R.nodes2 = c->nodes2;
+    R.stk_limit = stk_limit_of(c);
+    R.n_nodes = c->n_nodes;
+    R.prims = c->sorted;
+    R.ext = c->dext;
+    R.nee = c->dnee;
+    R.sc = c->sc;
+    R.root_lo = make_float4(c->root[0], c->root[1], c->root[2], 0.0f);
+    R.root_hi = make_float4(c->root[3], c->root[4], c->root[5], 0.0f);
+    R.mode = 2;
+    R.max_depth = 1;
+    R.seed = seed;
+    R.n_total = n;
+    R.rays = c->d_rays;
+    R.work = (c->prof & GF_PROFILE_WORK) ? c->d_work : nullptr;
+    R.trays = rays;
+    R.tout = t_out;
+    R.packets = (flags & GF_TRACE_PACKETS) ? 1 : 2;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int64_t base = 0; base < n; base += chunk) {
+        R.path_base = base;
+        R.n_paths = std::min<int64_t>(chunk, n - base);
+        GF_CUDA(c, gf_launch_render_pass(R, 0, 0, st, c->timer), "free flight");
+    }
+    if (c->timer.recs.size() > 4096) harvest(c);
     return GF_OK;
 }
 

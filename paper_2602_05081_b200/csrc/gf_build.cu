@@ -38,7 +38,7 @@ __device__ int derive_bin(const float* q, const float* sc, int K, const float* a
     return best;
 }
 
-__global__ void k_load_prims(LoadArgs A, GPrim* out, uint8_t* gout, uint32_t* err) {
+__global__ void k_load_prims(LoadArgs A, GPrim* out, uint8_t* gout, uint32_t* err, uint32_t* lfmax_bits) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.n) return;
     const float* q = A.quat + 4 * i;
@@ -74,6 +74,8 @@ __global__ void k_load_prims(LoadArgs A, GPrim* out, uint8_t* gout, uint32_t* er
     } else {
         bin = (lev == 0) ? 0 : derive_bin(q, sc, A.K, A.axes);
     }
+    const int band = A.band ? A.band[i] : 0;
+    if (band >= A.n_bands) e |= ERR_ASSIGN;
     if (e) {
         atomicOr(err, e);
         atomicMin(err + 1, (uint32_t)i);
@@ -81,7 +83,11 @@ __global__ void k_load_prims(LoadArgs A, GPrim* out, uint8_t* gout, uint32_t* er
     }
     lev = min(lev, A.P - 1);
     bin = min(bin, A.K - 1);
-    int group = lev == 0 ? 0 : 1 + (lev - 1) * A.K + bin;
+    int group = band * (1 + (A.P - 1) * A.K) + (lev == 0 ? 0 : 1 + (lev - 1) * A.K + bin);  // C24
+    if (lev > 0) {  // reading F3: the level's maximum world frequency |omega_vec| = omega |S^-1 (1,1,1)|
+        const float f = om * sqrtf(1.0f / (sc[0] * sc[0]) + 1.0f / (sc[1] * sc[1]) + 1.0f / (sc[2] * sc[2]));
+        atomicMax(lfmax_bits + lev, __float_as_uint(f));  // f >= 0: the bits order like the values
+    }
     // R from the normalised quaternion, W = S^-1 R^T: row k of W = (column k of R) / s_k
     float x = q[0] / qn, y = q[1] / qn, z = q[2] / qn, w = q[3] / qn;
     float R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
@@ -438,9 +444,166 @@ using namespace gfk;
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, cudaStream_t st) {
+cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, uint32_t* lfmax_bits,
+                           cudaStream_t st) {
     if (A.n == 0) return cudaSuccess;
-    k_load_prims<<<nblk(A.n, 256), 256, 0, st>>>(A, (GPrim*)out, group, err);
+    k_load_prims<<<nblk(A.n, 256), 256, 0, st>>>(A, (GPrim*)out, group, err, lfmax_bits);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- C12: group f0 = sqrt(3) median omega
+// keys (level << 32 | bits(omega)) of the Gabor members (omega >= 0: the bits order like the values),
+// radix-sorted; per level its member count, then the median from the sorted run of the level.
+__global__ void k_f0_keys(const GPrim* prims, const uint8_t* group, int64_t n, int G0, int K, uint64_t* keys,
+                          uint32_t* vals, uint32_t* counts) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int gl = group[i] % G0, lev = gl == 0 ? 0 : 1 + (gl - 1) / K;
+    keys[i] = ((uint64_t)(uint32_t)lev << 32) | __float_as_uint(prims[i].b.w);  // b.w = omega as loaded
+    vals[i] = 0u;
+    if (lev > 0) atomicAdd(counts + lev, 1u);
+}
+__global__ void k_f0_count0(uint32_t* counts, int64_t n) {
+    uint32_t rest = 0;
+    for (int l = 1; l < kMaxLevels; ++l) rest += counts[l];
+    counts[0] = (uint32_t)n - rest;
+}
+__global__ void k_f0_median(const uint64_t* sorted, const uint32_t* counts, int64_t n, int P, float* f0) {
+    const int l = threadIdx.x;
+    if (l >= kMaxLevels) return;
+    f0[l] = 0.0f;
+    if (l == 0 || l >= P) return;
+    uint32_t off = 0;
+    for (int k = 0; k < l; ++k) off += counts[k];
+    const uint32_t c = counts[l];
+    if (c == 0) return;
+    const float a = __uint_as_float((uint32_t)sorted[off + (c - 1) / 2]), b = __uint_as_float((uint32_t)sorted[off + c / 2]);
+    const float med = (c & 1u) ? b : __fdiv_rn(__fadd_rn(a, b), 2.0f);  // numpy's median (fp32 mean of the middle two)
+    f0[l] = (float)((double)med * 1.7320508075688772);  // whitened |k_W| = sqrt(3) omega (C2)
+}
+cudaError_t gf_launch_group_f0(const GPrim* prims, const uint8_t* group, int64_t n, int P, int K, int G0,
+                               const BuildScratch& S, float* f0_dev, cudaStream_t st) {
+    cudaError_t e;
+    uint32_t* counts = S.flags;  // kMaxLevels counters (flags are rewritten by the BVH build afterwards)
+    if ((e = cudaMemsetAsync(counts, 0, sizeof(uint32_t) * kMaxLevels, st))) return e;
+    if (n > 0) {
+        k_f0_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, G0, K, S.keys_in, S.vals_in, counts);
+        size_t tb = S.sort_temp_bytes;
+        if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
+                                                 0, 64, st)))
+            return e;
+    }
+    k_f0_count0<<<1, 1, 0, st>>>(counts, n);  // level 0 precedes level 1 in the sorted order
+    k_f0_median<<<1, 32, 0, st>>>(S.keys_out, counts, n, P, f0_dev);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- motion-blur group mask (M1-M3)
+// omega_vec = R S^-1 (w,w,w)^T = W^T (w,w,w)^T: w times the sum of the rows of W
+__device__ __forceinline__ float3 omega_vec(const GPrim& P) {
+    return make_float3(P.b.w * (P.b.x + P.c.x + P.d.x), P.b.w * (P.b.y + P.c.y + P.d.y),
+                       P.b.w * (P.b.z + P.c.z + P.d.z));
+}
+struct MbScratch {
+    unsigned long long ref[kMaxGroups];  // (bits(|omega_vec|) << 32) | ~index: max -> largest, first on ties
+    double sum[kMaxGroups][3];
+    unsigned long long cnt[kMaxGroups];
+    float att[kMaxGroups];
+    uint32_t mask;
+};
+__global__ void k_mb_ref(const GPrim* prims, const uint8_t* group, int64_t n, MbScratch* M) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float3 w = omega_vec(prims[i]);
+    const float f = sqrtf(w.x * w.x + w.y * w.y + w.z * w.z);
+    atomicMax(&M->ref[group[i]], ((unsigned long long)__float_as_uint(f) << 32) | (0xFFFFFFFFu - (uint32_t)i));
+}
+__global__ void k_mb_sum(const GPrim* prims, const uint8_t* group, int64_t n, MbScratch* M) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int g = group[i];
+    const uint32_t ri = 0xFFFFFFFFu - (uint32_t)(M->ref[g] & 0xFFFFFFFFull);
+    const float3 w = omega_vec(prims[i]), r = omega_vec(prims[ri]);
+    const double sg = (w.x * r.x + w.y * r.y + w.z * r.z) < 0.0f ? -1.0 : 1.0;  // +-omega_vec: the same cosine
+    atomicAdd(&M->sum[g][0], sg * w.x);
+    atomicAdd(&M->sum[g][1], sg * w.y);
+    atomicAdd(&M->sum[g][2], sg * w.z);
+    atomicAdd(&M->cnt[g], 1ull);
+}
+__global__ void k_mb_fin(MbScratch* M, int G, int G0, float dx, float dy, float dz, float m, float thr) {
+    __shared__ uint32_t mask;
+    if (threadIdx.x == 0) mask = 0;
+    __syncthreads();
+    const int g = threadIdx.x;
+    if (g < G) {
+        double att = 1.0;
+        if (g % G0 != 0 && M->cnt[g] > 0) {
+            const double dn = sqrt((double)dx * dx + (double)dy * dy + (double)dz * dz);
+            const double k = fabs((M->sum[g][0] * dx + M->sum[g][1] * dy + M->sum[g][2] * dz) / dn) / (double)M->cnt[g];
+            const double x = 0.5 * (double)m * k;
+            att = x == 0.0 ? 1.0 : fabs(sin(x) / x);  // box filter on a cosine of frequency k (M2)
+        }
+        M->att[g] = (float)att;
+        if (att >= (double)thr) atomicOr(&mask, 1u << g);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) M->mask = mask;
+}
+size_t gf_mb_scratch_bytes() { return sizeof(MbScratch); }
+cudaError_t gf_launch_mb_mask(const GPrim* prims, const uint8_t* group, int64_t n, int32_t G, int32_t G0, const float* dir,
+                              float m, float threshold, void* dev_scratch, uint32_t* mask_host, float* att_host,
+                              cudaStream_t st) {
+    cudaError_t e;
+    MbScratch* M = (MbScratch*)dev_scratch;
+    if ((e = cudaMemsetAsync(M, 0, sizeof(MbScratch), st))) return e;
+    if (n > 0) {
+        k_mb_ref<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, M);
+        k_mb_sum<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, M);
+    }
+    k_mb_fin<<<1, 32, 0, st>>>(M, G, G0, dir[0], dir[1], dir[2], m, threshold);
+    if ((e = cudaMemcpyAsync(mask_host, &M->mask, sizeof(uint32_t), cudaMemcpyDeviceToHost, st))) return e;
+    if (att_host && (e = cudaMemcpyAsync(att_host, M->att, sizeof(float) * G, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaStreamSynchronize(st))) return e;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- C8': adaptive extents (Eq. 15)
+__global__ void k_adaptive_extent(const float* scale, const float* alpha, const float* omega, int64_t n, float eps,
+                                  float* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double s0 = scale[3 * i], s1 = scale[3 * i + 1], s2 = scale[3 * i + 2];
+    const double smax = fmax(s0, fmax(s1, s2));
+    const double a = fmax((double)alpha[i], 1e-30), w = omega[i];
+    const double arg = -2.0 * log((double)eps * 2.0 * 3.14159265358979323846 * s0 * s1 * s2 / (a * smax)) - 3.0 * w * w;
+    out[i] = (float)fmin(3.0, fmax(1e-3, sqrt(fmax(arg, 0.0))));
+}
+cudaError_t gf_launch_adaptive_extent(const float* scale, const float* alpha, const float* omega, int64_t n, float eps,
+                                      float* out, cudaStream_t st) {
+    if (n > 0) k_adaptive_extent<<<nblk(n, 256), 256, 0, st>>>(scale, alpha, omega, n, eps, out);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- 64-bit hash of a workspace (replica check)
+// H = sum_i mix(word_i ^ (i * golden)) mod 2^64 (splitmix64 finaliser): order-independent reduction,
+// position-sensitive words; equal builds give equal hashes.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__global__ void k_hash(const unsigned long long* w, size_t nw, unsigned long long* out) {
+    unsigned long long h = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (size_t)gridDim.x * blockDim.x)
+        h += mix64(w[i] ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(i + 1)));
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xFFFFFFFFu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+cudaError_t gf_launch_hash(const void* data, size_t bytes, unsigned long long* out_dev, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(out_dev, 0, sizeof(unsigned long long), st))) return e;
+    const size_t nw = bytes / 8;
+    if (nw > 0) k_hash<<<1184, 256, 0, st>>>((const unsigned long long*)data, nw, out_dev);
     return cudaGetLastError();
 }
 

@@ -15,6 +15,23 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Bounds checks of the shared-memory frontiers and queues (debug builds, -DGF_DEBUG_CHECKS: the
+// stand-in for compute-sanitizer, which this pool does not run): a failed check prints and traps.
+#ifdef GF_DEBUG_CHECKS
+#include <cstdio>
+#define GF_CHECK(c)                                                                         \
+    do {                                                                                    \
+        if (!(c)) {                                                                         \
+            printf("GF_CHECK failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);               \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define GF_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
+
 namespace gfk {
 
 constexpr int kMaxGroups = 32;
@@ -48,7 +65,8 @@ struct PolicyDev {
 };
 
 struct SceneDev {
-    int32_t P, K, G;
+    int32_t P, K, G;     // G = n_bands * G0 groups in all (C24)
+    int32_t G0, n_bands; // groups per spatial band (1 + (P-1) K), bands (config-5 distance bands)
     float axes[3 * 16];
     float f0[kMaxGroups];
 };
@@ -180,6 +198,11 @@ __device__ inline uint32_t policy_eval(const PolicyDev& pol, const SceneDev& sc,
             mask |= 1u << g;
             w[g] = lw[l] * bw[b];
         }
+    }
+    // spatial bands: one draw, the same groups and weights in every band (C24)
+    for (int bd = 1; bd < sc.n_bands; ++bd) {
+        mask |= (mask & ((1u << sc.G0) - 1u)) << (bd * sc.G0);
+        for (int g = 0; g < sc.G0; ++g) w[bd * sc.G0 + g] = w[g];
     }
     return mask & pol.static_mask;
 }
@@ -755,6 +778,7 @@ __device__ __forceinline__ void warp_traverse_b(const GNode* __restrict__ nodes,
             if (i0) sm.stk[ns + __popc(b0 & lt)] = ref0;
             if (i1) sm.stk[ns + __popc(b0) + __popc(b1 & lt)] = ref1;
             ns += __popc(b0) + __popc(b1);
+            GF_CHECK(ns <= kWStk);
             const uint32_t c0 = (h0 && (ref0 & kLeafBit)) ? ((inf0 >> 5) & 7u) : 0u;
             const uint32_t c1 = (h1 && (ref1 & kLeafBit)) ? ((inf1 >> 5) & 7u) : 0u;
             if (__any_sync(FULL, c0 + c1 > 0)) {
@@ -773,6 +797,7 @@ __device__ __forceinline__ void warp_traverse_b(const GNode* __restrict__ nodes,
                 for (uint32_t k = 0; k < (uint32_t)kLeafMax; ++k)
                     if (k < c1) sm.prm[pos + c0 + k] = v1 + k;
                 np += (int)__shfl_sync(FULL, incl, 31);
+                GF_CHECK(np <= kWPrm);
             }
             __syncwarp();
         } else {
@@ -880,6 +905,7 @@ __device__ __forceinline__ double warp_tau_b(const GNode* __restrict__ nodes, co
                     if (ne == 2) q.e[t][nq + __popc(m1) + __popc(m2 & lt)] = e1;
                 }
                 nq += __popc(m1) + __popc(m2);
+                GF_CHECK(nq <= kWEnd);
                 __syncwarp();
                 while (nq >= 32) run(t, 32);
             }

@@ -10,8 +10,8 @@
 struct LoadArgs {
     int64_t n;
     const float *mu, *quat, *scale, *alpha, *omega, *extent;
-    const uint8_t *level, *bin;
-    int32_t P, K;
+    const uint8_t *level, *bin, *band;
+    int32_t P, K, n_bands;
     float cutoffs[8];
     float axes[48];
 };
@@ -81,8 +81,8 @@ struct RenderDev {
     gfk::CamDev cam;
     float4 root_lo, root_hi;
     int32_t mode, max_depth, jitter, estimator;
-    int32_t fov;  // foveated rendering (gf_render_desc.foveation)
-    float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_lfmax[8];
+    int32_t fov;  // foveated rendering mode bits (gf_render_desc.foveation: 1 levels, 2 continuous)
+    float fov_gaze[2], fov_f0, fov_slope, fov_jitter, fov_lfmax[8];  // fov_lfmax: gf_scene_info.level_fmax
     int32_t mb;  // motion-blur reference (gf_render_desc.motion_blur)
     float mb_dir[3], mb_m;
     float albedo, hg_g, sun_E, env_L;
@@ -98,17 +98,19 @@ struct RenderDev {
     int32_t spp_count;
     // per-path state (SoA, n_paths each)
     float *ox, *oy, *oz, *dx, *dy, *dz, *beta, *L;
-    double* cum;  // 3 n: tau before the bracketing bin, tau*, tau in the bin
-    int32_t* bin;
     uint32_t* pix;
-    uint32_t* nhit;  // hits recorded by ffA
-    uint2* hits;     // [n_paths][hit_cap]: sorted prim index | group << 24, bin span ka | kb << 8
-    int32_t hit_cap;
-    float4* wrec;    // [k_ff warp][rec_cap] x 2 float4 hit records (per warp, reused across paths)
-    float4* waux;    // [k_ff warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
+    int32_t* ffk;    // free flight: the bin of the first crossing (pass A -> pass B)
+    double* ffc;     // free flight: tau before that bin
+    float4* wrec;    // [warp][rec_cap] x 2 float4 hit records (pass-B windows, tracking; reused per path)
+    float4* waux;    // [warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;
-    uint32_t* qO;    // record-overflow paths (k_ff redo after k_ff_pkt, else single-pass k_ffA)
-    uint32_t* qO2;   // record-overflow paths of the k_ff redo (single-pass k_ffA)
+    uint32_t* qW;    // paths that collide: pass B queue
+    uint32_t* qO;    // paths with more chords than the record buffer (one-pass / tracking -> passes A + B)
+    uint32_t* qV;    // pass-B windows with more chords than the record buffer (k_ffb_over)
+    // gf_trace_free_flight (mode 2): the caller's rays (n x 8) and output distances, else null
+    const float* trays;
+    float* tout;
+    int32_t packets;  // 0: packets for depth-0 camera rays; 1: always (static masks); 2: never
     // light BVH for NEE (built per gf_render call in the frame lf: rows x', y', z' = light direction)
     int32_t light;
     float lf[9];
@@ -125,18 +127,28 @@ struct RenderDev {
     gfk::GPrim* cprims;
     int32_t* cperm;
     uint32_t* cdepth;
-    uint32_t* qB2;   // record-overflow paths after single-pass ffA (per-thread ffB)
     // queues
     uint32_t *qA, *qB, *qNext;
-    uint32_t* qcount;  // [4]: A, B, next, overflow
-    unsigned long long* rays;  // [2]
+    uint32_t* qcount;  // [16]: queue counts and work cursors (gf_render.cu QC_* / CUR_*)
+    unsigned long long* rays;  // [3]: camera, extension, NEE rays
     float* accum;
     unsigned long long* work;  // gf_stats work counters (counting variant) or null
     // (appended last, so the hot kernels' parameter offsets stay as measured)
     int32_t tomo_pkt_min;  // tomography chunks with at least this many paths take k_tomo_pkt
+    int32_t ffb_cam;       // pass B of depth-0 rays walks the camera BVH (1) or the world BVH (0)
 };
 
-cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, cudaStream_t st);
+cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, uint32_t* lfmax_bits,
+                           cudaStream_t st);
+cudaError_t gf_launch_group_f0(const gfk::GPrim* prims, const uint8_t* group, int64_t n, int P, int K, int G0,
+                               const BuildScratch& S, float* f0_dev, cudaStream_t st);
+cudaError_t gf_launch_mb_mask(const gfk::GPrim* prims, const uint8_t* group, int64_t n, int32_t G, int32_t G0,
+                              const float* dir, float m, float threshold, void* dev_scratch, uint32_t* mask_host,
+                              float* att_host, cudaStream_t st);
+size_t gf_mb_scratch_bytes();
+cudaError_t gf_launch_adaptive_extent(const float* scale, const float* alpha, const float* omega, int64_t n, float eps,
+                                      float* out, cudaStream_t st);
+cudaError_t gf_launch_hash(const void* data, size_t bytes, unsigned long long* out_dev, cudaStream_t st);
 size_t gf_sort_temp_bytes(int64_t n);
 BuildScratch gf_scratch_layout(int64_t n, char* base);
 cudaError_t gf_launch_build(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes,

@@ -452,11 +452,11 @@ __global__ void __launch_bounds__(128, GF_GRADP_MINB) k_grad_pkt(TraceArgs A, co
             __syncwarp();
             if (a1) {
                 if (ref1 & kLeafBit) leaf(inf1, h1);
-                else stk[ns++] = ref1;
+                else { GF_CHECK(ns < kGStk); stk[ns++] = ref1; }
             }
             if (a0) {
                 if (ref0 & kLeafBit) leaf(inf0, h0);
-                else stk[ns++] = ref0;
+                else { GF_CHECK(ns < kGStk); stk[ns++] = ref0; }
             }
             __syncwarp();
         }

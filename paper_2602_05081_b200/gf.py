@@ -30,12 +30,20 @@ class GFError(RuntimeError):
 
 
 class Prims(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_void_p) for n in ("mu", "quat", "scale", "alpha", "omega", "extent", "level", "bin")]
+    _fields_ = [(n, ctypes.c_void_p) for n in ("mu", "quat", "scale", "alpha", "omega", "extent", "level", "bin",
+                                               "band")]
 
 
 class Pyramid(ctypes.Structure):
     _fields_ = [("n_levels", ctypes.c_int32), ("n_bins", ctypes.c_int32), ("bin_axes", ctypes.c_void_p),
-                ("level_cutoffs", ctypes.c_void_p), ("group_f0", ctypes.c_void_p)]
+                ("level_cutoffs", ctypes.c_void_p), ("group_f0", ctypes.c_void_p), ("n_bands", ctypes.c_int32)]
+
+
+class SceneInfo(ctypes.Structure):
+    _fields_ = [("n_prims", ctypes.c_int64), ("n_levels", ctypes.c_int32), ("n_bins", ctypes.c_int32),
+                ("n_bands", ctypes.c_int32), ("n_groups", ctypes.c_int32), ("level_fmax", ctypes.c_float * 8),
+                ("group_f0", ctypes.c_float * 32), ("root_lo", ctypes.c_float * 3), ("root_hi", ctypes.c_float * 3),
+                ("n_nodes", ctypes.c_uint32), ("max_depth", ctypes.c_uint32), ("bvh_hash", ctypes.c_uint64)]
 
 
 class LodPolicy(ctypes.Structure):
@@ -48,8 +56,8 @@ class Stats(ctypes.Structure):
                 ("stage_ms", ctypes.c_double * 8), ("work", (ctypes.c_uint64 * 12) * 8)]
 
 
-STAGES = ("gen", "ff", "ff_fallback", "nee", "finish", "tomo", "trace", "unused")
-WORK = ("nodes", "tests", "hits", "erf_complex", "erf_real", "gl_fallbacks", "ffb_overflow", "root_evals", "paths")
+STAGES = ("gen", "ffA", "ffB", "nee", "finish", "tomo", "trace", "unused")
+WORK = ("nodes", "tests", "hits", "erf_complex", "erf_real", "gl_fallbacks", "window_splits", "root_evals", "paths")
 PROFILE_TIMING, PROFILE_WORK = 1, 2
 
 
@@ -63,7 +71,7 @@ class RenderDesc(ctypes.Structure):
                 ("sun_dir", ctypes.c_float * 3), ("sun_E", ctypes.c_float), ("env_L", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("estimator", ctypes.c_int32), ("reuse_accel", ctypes.c_int32),
                 ("foveation", ctypes.c_int32), ("fov_gaze", ctypes.c_float * 2), ("fov_f0", ctypes.c_float),
-                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float), ("fov_level_fmax", ctypes.c_float * 8),
+                ("fov_slope", ctypes.c_float), ("fov_jitter", ctypes.c_float),
                 ("motion_blur", ctypes.c_int32), ("mb_dir", ctypes.c_float * 3), ("mb_m", ctypes.c_float)]
 
 
@@ -98,6 +106,12 @@ def lib():
     L.gf_trace_transmittance.argtypes = [vp, vp, i64, u64, vp, vp, vp, vp]
     L.gf_trace_transmittance_ex.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp, vp]
     L.gf_trace_candidates.argtypes = [vp, vp, i64, u32, vp, i32, vp, vp]
+    L.gf_trace_free_flight.argtypes = [vp, vp, i64, u64, u32, vp, vp, sz, vp]
+    L.gf_free_flight_scratch_bytes.argtypes = [vp, i64, ctypes.POINTER(sz)]
+    L.gf_free_flight_bins.restype = ctypes.c_int
+    L.gf_scene_info_get.argtypes = [vp, ctypes.POINTER(SceneInfo)]
+    L.gf_motion_blur_mask.argtypes = [vp, vp, ctypes.c_float, ctypes.c_float, vp, vp]
+    L.gf_adaptive_extent.argtypes = [vp, vp, vp, vp, i64, ctypes.c_float, vp, vp]
     L.gf_trace_grad_alpha.argtypes = [vp, vp, i64, u64, vp, vp, vp]
     L.gf_trace_grad_params.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp]
     L.gf_grad_params_finish.argtypes = [vp, vp, vp, vp, vp]
@@ -176,19 +190,22 @@ class GaborField:
         arrs = {k: dev(k, torch.float32) for k in ("mu", "quat", "scale", "alpha", "omega", "extent")}
         arrs["level"] = dev("level", torch.uint8)
         arrs["bin"] = dev("bin", torch.uint8)
-        prims = Prims(*[_ptr(arrs[k]) for k in ("mu", "quat", "scale", "alpha", "omega", "extent", "level", "bin")])
+        arrs["band"] = dev("band", torch.uint8)
+        prims = Prims(*[_ptr(arrs[k]) for k in ("mu", "quat", "scale", "alpha", "omega", "extent", "level", "bin",
+                                                 "band")])
         axes = np.ascontiguousarray(scene["bin_axes"], np.float32)
         cut = None if level_cutoffs is None else np.ascontiguousarray(level_cutoffs, np.float32)
         f0 = None if group_f0 is None else np.ascontiguousarray(group_f0, np.float32)
+        nb = int(scene.get("n_bands", 1))
         pyr = Pyramid(P, K, axes.ctypes.data, None if cut is None else cut.ctypes.data,
-                      None if f0 is None else f0.ctypes.data)
+                      None if f0 is None else f0.ctypes.data, nb)
         pb, bb, sb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
         self._check(self.L.gf_query_workspace(n, ctypes.byref(pb), ctypes.byref(bb), ctypes.byref(sb)))
         self.prim_ws = self._buf(pb.value)
         self._check(self.L.gf_load_primitives(self.ctx, ctypes.byref(prims), n, ctypes.byref(pyr),
                                               _ptr(self.prim_ws), pb.value, _stream()))
         self._sizes = (bb.value, sb.value)
-        self.n, self.P, self.K, self.G = n, P, K, 1 + (P - 1) * K
+        self.n, self.P, self.K, self.G = n, P, K, nb * (1 + (P - 1) * K)
         self._quat = arrs["quat"]  # kept for gf_grad_params_finish (the quaternions as loaded)
         return self
 
@@ -199,6 +216,36 @@ class GaborField:
         self._check(self.L.gf_build_bvh(self.ctx, _ptr(self.bvh_ws), bb, _ptr(scratch), sb, _stream()))
         del scratch
         return self
+
+    def scene_info(self):
+        """gf_scene_info_get: level_fmax (F3), group_f0 (C12), root box, node count, BVH hash."""
+        si = SceneInfo()
+        self._check(self.L.gf_scene_info_get(self.ctx, ctypes.byref(si)))
+        return {"n_prims": si.n_prims, "n_levels": si.n_levels, "n_bins": si.n_bins, "n_bands": si.n_bands,
+                "n_groups": si.n_groups, "level_fmax": np.array(si.level_fmax[:], np.float32),
+                "group_f0": np.array(si.group_f0[:si.n_groups], np.float32),
+                "root_lo": list(si.root_lo), "root_hi": list(si.root_hi), "n_nodes": si.n_nodes,
+                "max_depth": si.max_depth, "bvh_hash": int(si.bvh_hash)}
+
+    def motion_blur_mask(self, direction, m, threshold):
+        """gf_motion_blur_mask (readings M1-M3): (32-bit group mask, attenuation per group)."""
+        d = np.ascontiguousarray(direction, np.float32).reshape(3)
+        mask = ctypes.c_uint32()
+        att = np.zeros(32, np.float32)
+        self._check(self.L.gf_motion_blur_mask(self.ctx, d.ctypes.data, ctypes.c_float(m), ctypes.c_float(threshold),
+                                               ctypes.byref(mask), att.ctypes.data))
+        return int(mask.value), att[:self.G]
+
+    def adaptive_extent(self, scene, eps):
+        """gf_adaptive_extent (Eq. 15, C8'): per-primitive extents for threshold eps (device tensor)."""
+        torch = self.torch
+        t = {k: torch.as_tensor(np.ascontiguousarray(scene[k], np.float32)).to(self.device).contiguous()
+             for k in ("scale", "alpha", "omega")}
+        n = int(scene["n"])
+        out = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
+        self._check(self.L.gf_adaptive_extent(self.ctx, _ptr(t["scale"]), _ptr(t["alpha"]), _ptr(t["omega"]), n,
+                                              ctypes.c_float(eps), _ptr(out), _stream()))
+        return out[:n]
 
     # -------------------------------------------------------------- a3
     def set_lod_mask(self, ext=None, nee=None):
@@ -219,6 +266,20 @@ class GaborField:
         self._check(self.L.gf_trace_transmittance_ex(self.ctx, _ptr(rays), n, seed & 0xFFFFFFFFFFFFFFFF, flags,
                                                      _ptr(tau), _ptr(T), _ptr(cnt), _stream()))
         return tau, T, cnt
+
+    def trace_free_flight(self, rays, seed=0, packets=False):
+        """gf_trace_free_flight: first t with tau(tmin, t) = tau* per ray (+inf: escape)."""
+        torch = self.torch
+        rays = torch.as_tensor(rays).to(device=self.device, dtype=torch.float32).contiguous().view(-1, 8)
+        n = rays.shape[0]
+        t = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
+        nb = ctypes.c_size_t()
+        self._check(self.L.gf_free_flight_scratch_bytes(self.ctx, n, ctypes.byref(nb)))
+        scratch = self._buf(nb.value)
+        self._check(self.L.gf_trace_free_flight(self.ctx, _ptr(rays), n, seed & 0xFFFFFFFFFFFFFFFF,
+                                                TRACE_PACKETS if packets else 0, _ptr(t), _ptr(scratch), nb.value,
+                                                _stream()))
+        return t[:n]
 
     def trace_grad_alpha(self, rays, dl_dtau, seed=0, out=None):
         """d(sum_r dl_dtau[r] tau_r) / d alpha (input order, fp32)."""
@@ -276,11 +337,9 @@ class GaborField:
         d.reuse_accel = int(desc.get("reuse_accel", 0))
         fov = desc.get("foveation")
         if fov:
-            d.foveation = 1
+            d.foveation = int(fov.get("mode", 3))
             d.fov_gaze[:] = [float(x) for x in fov["gaze"]]
             d.fov_f0, d.fov_slope, d.fov_jitter = float(fov["f0"]), float(fov["slope"]), float(fov.get("jitter", 0.0))
-            lf = list(np.asarray(fov["level_fmax"], np.float32)) + [0.0] * 8
-            d.fov_level_fmax[:] = [float(x) for x in lf[:8]]
         mb = desc.get("motion_blur")
         if mb:
             d.motion_blur = 1
@@ -306,7 +365,7 @@ class GaborField:
             size = probes.numel() * spp_count if probes is not None else desc["width"] * desc["height"] * 2
             accum = torch.zeros(size, dtype=torch.float32, device=self.device)
         if ray_counts is None:
-            ray_counts = torch.zeros(2, dtype=torch.int64, device=self.device)
+            ray_counts = torch.zeros(3, dtype=torch.int64, device=self.device)  # camera, extension, NEE
         self._check(self.L.gf_render(self.ctx, ctypes.byref(d), _ptr(accum), _ptr(scratch), scratch.numel(),
                                      _ptr(ray_counts), _stream()))
         self._last_scratch = scratch

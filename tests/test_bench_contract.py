@@ -41,7 +41,7 @@ def test_gpu_arm_json_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     r = d["roofline"]
-    assert r["bound"] in ("alu", "hbm", "tensor") and r["peak"] > 0 and 0 < r["frac"] < 1
+    assert r["bound"] in ("alu", "hbm", "tensor") and r["peak"] > 0 and 0 < r["frac"] < 1 and d["roofline_alu"]["frac"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     e = d["e2e"]

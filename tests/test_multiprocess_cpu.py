@@ -47,7 +47,18 @@ def _worker(rank, world, port, W, H, spp, out):
             acc[2 * pix] += v
             acc[2 * pix + 1] += v * v
     dist.all_reduce(cover)
+    tiles = acc.clone()
+    dist.reduce(tiles, dst=0)  # bench.py gathers the disjoint tiles on rank 0
     dist.all_reduce(acc)
+    if rank == 0:
+        assert torch.equal(tiles, acc)
+    # replica check of the BVH hash (bench.replica_check): equal hashes pass, one differing rank fails
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    h = 0xFEDCBA9876543210
+    assert bench.replica_check(h, dist, "cpu")
+    assert not bench.replica_check(h ^ (rank << 40), dist, "cpu")
     # sample sharding: all pixels, samples s with s mod world == rank (kind 2)
     acc2 = torch.zeros(W * H * 2, dtype=torch.float64)
     n2 = gf.shard_paths(W, H, 2, rank, world)

@@ -13,7 +13,7 @@ from paper_2602_05081_b200 import gf, inputs as I  # noqa: E402
 
 sc = I.scene_cfg2()
 f = gf.GaborField(0)
-f.load_primitives(sc, group_f0=I.group_f0(sc))
+f.load_primitives(sc)
 f.build_bvh()
 d = I.render_desc_cfg2(3)
 idx = np.arange(d["width"] * d["height"])

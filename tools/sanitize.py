@@ -42,7 +42,7 @@ def main():
     # scattering with stochastic masks (warp free flight), tracking estimator
     sc2 = I.scene_bunny(counts=(150, 1050, 2800, 6000) if small else (600, 4200, 11200, 24000))
     g = gf.GaborField(0)
-    g.load_primitives(sc2, group_f0=I.group_f0(sc2))
+    g.load_primitives(sc2)
     g.build_bvh()
     w = 32 if small else 64
     g.render(I.render_desc_cfg2(3, w, w))

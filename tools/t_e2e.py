@@ -4,11 +4,11 @@ sys.path.insert(0, '.')
 from paper_2602_05081_b200 import gf, inputs as I
 sc = I.scene_cfg2()
 f = gf.GaborField(0)
-f.load_primitives(sc, group_f0=I.group_f0(sc)); f.build_bvh()
+f.load_primitives(sc); f.build_bvh()
 descs = [dict(I.render_desc_cfg2(i), reuse_accel=1) for i in range(4)]
 scratch = f.render_scratch(descs[0], 1)
 accum = torch.zeros((4, 1024 * 1024 * 2), device='cuda')
-rays = torch.zeros(2, dtype=torch.int64, device='cuda')
+rays = torch.zeros(3, dtype=torch.int64, device='cuda')
 keys = ("mu", "quat", "scale", "alpha", "omega", "extent", "level", "bin")
 host = {k: torch.from_numpy(np.ascontiguousarray(sc[k])).pin_memory() for k in keys}
 out_host = torch.empty_like(accum, device="cpu").pin_memory()
@@ -19,8 +19,7 @@ def tm(label, fn):
 for step in range(3):
     print("step", step)
     dev = tm("h2d", lambda: {kk: v.to('cuda', non_blocking=True) for kk, v in host.items()})
-    f0 = tm("group_f0 (host)", lambda: I.group_f0(sc))
-    tm("load", lambda: g2.load_primitives(dict(sc, **dev), group_f0=f0))
+    tm("load", lambda: g2.load_primitives(dict(sc, **dev)))
     tm("build", lambda: g2.build_bvh())
     for i, d in enumerate(descs):
         tm(f"render {i}", lambda: g2.render(d, 0, 1, accum=accum[i], ray_counts=rays, scratch=scratch))
