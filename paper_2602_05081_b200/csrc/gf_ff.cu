@@ -17,7 +17,7 @@
 namespace gfk {
 
 #ifndef GF_FF_ONEPASS
-#define GF_FF_ONEPASS 1  // extension rays: one-pass kernel (0: the two-pass kernels for every ray)
+#define GF_FF_ONEPASS 0  // 1: extension rays take the one-pass kernel (measured slower: instruction-cache bound)
 #endif
 
 template <bool STOCH, bool COUNT, bool FOV, bool CAM>
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(128) k_ff(RenderDev R, int32_t sample, int32_t
         bin_records<COUNT>(rec, aux, cap, ng, nb, coarse_bins(f), cols, cols + kNC * 32,
                            kNF > 1 ? cols + 2 * kNC * 32 : nullptr, q, wk);
         double cstart;
-        const int ks = coarse_decide_warp(cols, f.tstar, &cstart);
+        const int ks = kNF == 1 ? coarse_first_warp(cols, f.tstar, &cstart) : coarse_decide_warp(cols, f.tstar, &cstart);
         const int k1 = ks & 0xFF, s0 = ks >> 8;
         bool col = false;
         float t = 0.0f;

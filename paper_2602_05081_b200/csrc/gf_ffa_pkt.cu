@@ -18,6 +18,12 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
                                                               int cur_slot) {
     __shared__ uint32_t s_stk[4][kPStk];
     __shared__ float s_h[kNRows][kNC * 128];  // Gaussian pieces, Gabor pieces (, Gabor masses)
+#if GF_REFS
+    __shared__ WarpEnd s_e[4];  // pass B of the colliding lanes from their hit lists
+#else
+    WarpEnd* s_e = nullptr;  // (no in-kernel pass B)
+#endif
+    __shared__ uint32_t s_gm[kNC * 128];  // per lane and coarse bin: the groups with chords in the bin
     const unsigned FULL = 0xFFFFFFFFu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t count = R.qcount[cnt_slot];
@@ -25,9 +31,15 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
     float* hg = s_h[0] + threadIdx.x;  // coarse bin m of this lane's ray at [m * 128] (conflict-free columns)
     float* hb = s_h[1] + threadIdx.x;
     float* hm = s_h[kNRows - 1] + threadIdx.x;  // (only written when kNF > 1)
+    uint32_t* gm = s_gm + threadIdx.x;
     const GNode* __restrict__ nodes = CAM ? R.cnodes : R.nodes;
     const GNode2* __restrict__ nodes2 = CAM ? R.cnodes2 : R.nodes2;
     const GPrim* __restrict__ prims = CAM ? R.cprims : R.prims;
+    const size_t gw = (size_t)blockIdx.x * 4 + wid;
+    uint32_t* __restrict__ wrefs = R.wref + gw * kRefWarp;  // lane l's hit list at [l * kRefCapL]
+    uint32_t* __restrict__ myrefs = wrefs + lane * kRefCapL;
+    float4* __restrict__ rec = R.wrec + gw * (size_t)R.rec_cap * 2;
+    float4* __restrict__ aux = R.waux + gw * (size_t)R.rec_cap;
     Work wk;
     uint32_t nray = 0;
     while (true) {
@@ -54,7 +66,11 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
         const float t0 = act ? f.tlo : 0.0f, t1 = act ? f.thi : 0.0f;
         const uint32_t mask = act ? f.mask : 0u;
 #pragma unroll
-        for (int m = 0; m < kNC; ++m) hg[m * 128] = hb[m * 128] = hm[m * 128] = 0.0f;  // (hm may alias hb: zero)
+        for (int m = 0; m < kNC; ++m) {
+            hg[m * 128] = hb[m * 128] = hm[m * 128] = 0.0f;  // (hm may alias hb: zero)
+            gm[m * 128] = 0u;
+        }
+        uint32_t nref = 0;
         auto leaf = [&](uint32_t info, bool mine) {
             const uint32_t first = info >> 8, cnt = (info >> 5) & 7u, g = info & 31u;
             for (uint32_t k = 0; k < cnt; ++k) {
@@ -71,9 +87,15 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
                 Setup s;
                 if (pass && prim_setup(P, r, t0, t1, s)) {
                     if (COUNT) ++wk.hits;
+                    if (GF_REFS) {  // this lane's hit list for pass B
+                        if (nref < (uint32_t)kRefCapL) myrefs[nref] = (first + k) | (g << 27);
+                        ++nref;
+                    }
                     float cj = P.d.w * s.ij;
                     if (STOCH) cj *= f.w[g];
                     coarse_chord<COUNT>(s, cj, f, hg, hb, hm, 128, wk);  // all lanes: the same primitive type
+                    const int ka = ff_bin(f, fmaf(s.u0 - s.bp, s.ij, s.tc)), kb = ff_bin(f, fmaf(s.u1 - s.bp, s.ij, s.tc));
+                    for (int m = ka; m <= kb; ++m) gm[m * 128] |= 1u << g;
                 }
             }
         };
@@ -108,20 +130,65 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
                 __syncwarp();
             }
         }
+        int ks = 0;
+        double cstart = 0.0;
         if (act) {
-            double g[kNC], b[kNC], mm[kNC], cstart;
+            if (kNF == 1) {  // uniform bins: the first edge reaching tau*, lane-local over this lane's columns
+                double c = 0.0;
+                int k1 = kNC;
+                for (int m = 0; m < kNC; ++m) {
+                    const double c2 = c + (double)hg[m * 128] + (double)hb[m * 128];
+                    if (c2 >= f.tstar) { k1 = m; break; }
+                    c = c2;
+                }
+                ks = k1 | (k1 << 8);
+                cstart = c;
+            } else {
+                double g[kNC], b[kNC], mm[kNC];
 #pragma unroll
-            for (int m = 0; m < kNC; ++m) { g[m] = hg[m * 128]; b[m] = hb[m * 128]; mm[m] = kNF > 1 ? hm[m * 128] : 0.0; }
-            const int ks = coarse_decide(g, b, mm, f.tstar, &cstart);
+                for (int m = 0; m < kNC; ++m) { g[m] = hg[m * 128]; b[m] = hb[m * 128]; mm[m] = hm[m * 128]; }
+                ks = coarse_decide(g, b, mm, f.tstar, &cstart);
+            }
             if ((ks >> 8) == kNC) {  // no coarse bin can reach tau*: escape
                 ff_escape(R, p);
                 act = false;
             } else {
                 R.ffk[p] = ks;
                 R.ffc[p] = cstart;
+                uint32_t g = 0;
+                for (int m = ks >> 8; m <= min(ks & 0xFF, kNC - 1); ++m) g |= gm[m * 128];
+                R.ffg[p] = g;
             }
         }
-        push(R.qW, R.qcount + QC_W, act, p);
+        // pass B here for the colliding lanes whose hit list fits, one lane after another with the whole
+        // warp (uniform bins); the others re-traverse their crossing bin in k_ffb_w
+        const bool here = GF_REFS && kNF == 1 && act && nref <= (uint32_t)kRefCapL;
+        unsigned todo = __ballot_sync(FULL, here);
+        bool done = false;
+        while (todo) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const float3 ol = make_float3(__shfl_sync(FULL, r.o.x, l), __shfl_sync(FULL, r.o.y, l), __shfl_sync(FULL, r.o.z, l));
+            const float3 dl = make_float3(__shfl_sync(FULL, r.d.x, l), __shfl_sync(FULL, r.d.y, l), __shfl_sync(FULL, r.d.z, l));
+            const RayDev rl = make_ray(ol, dl, 0.0f, INFINITY, __shfl_sync(FULL, r.fmax, l));
+            const int kl = __shfl_sync(FULL, ks, l) & 0xFF;
+            const float lo_l = __shfl_sync(FULL, t0, l), hi_l = __shfl_sync(FULL, t1, l), bw_l = __shfl_sync(FULL, f.bw, l);
+            const float wa = kl == 0 ? lo_l : fmaf((float)kl, bw_l, lo_l);  // ff_edge of the lane's bins
+            const float wb = kl >= kNC - 1 ? hi_l : fmaf((float)(kl + 1), bw_l, lo_l);
+            float tl = 0.0f;
+            const bool ok = window_from_refs<false, COUNT>(wrefs + l * kRefCapL, __shfl_sync(FULL, nref, l), prims, rl, nullptr,
+                                                           wa, wb, __shfl_sync(FULL, cstart, l),
+                                                           __shfl_sync(FULL, f.tstar, l), rec, aux, (uint32_t)R.rec_cap,
+                                                           s_e[wid], wk, tl);
+            const float tl_l = __shfl_sync(FULL, tl, 0);
+            if (lane == l && ok) {
+                ff_collide(R, p, f, tl_l);
+                done = true;
+            }
+            __syncwarp();
+        }
+        push(R.qB, R.qcount + QC_B, done, p);
+        push(R.qW, R.qcount + QC_W, act && !done, p);
         __syncwarp();
     }
 #pragma unroll

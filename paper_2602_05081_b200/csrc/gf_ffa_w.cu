@@ -23,6 +23,12 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
     __shared__ WarpTrav s_t[4];
     __shared__ WarpBinQ s_q[4];
     __shared__ float s_h[4][kNRows * kNC * 32];  // per warp: G, Gabor (, mass) rows; bin m of lane l at [m * 32 + l]
+#if GF_REFS
+    __shared__ WarpEnd s_e[4];  // pass B from the hit list (window_from_refs)
+#else
+    WarpEnd* s_e = nullptr;  // (no in-kernel pass B)
+#endif
+    __shared__ uint32_t s_gm[4][kNC];  // per coarse bin: the groups with chords in it
     const unsigned FULL = 0xFFFFFFFFu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -32,6 +38,10 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
     float* cb = cols + kNC * 32 + lane;
     float* cm = cols + (kNRows - 1) * kNC * 32 + lane;  // (only written when kNF > 1)
     WarpBinQ& q = s_q[wid];
+    const size_t gw = (size_t)blockIdx.x * 4 + wid;
+    uint32_t* __restrict__ refs = R.wref + gw * kRefWarp;  // this ray's hit list
+    float4* __restrict__ rec = R.wrec + gw * (size_t)R.rec_cap * 2;
+    float4* __restrict__ aux = R.waux + gw * (size_t)R.rec_cap;
     const GNode* __restrict__ nodes = CAM ? R.cnodes : R.nodes;
     const GNode2* __restrict__ nodes2 = CAM ? R.cnodes2 : R.nodes2;
     const GPrim* __restrict__ prims = CAM ? R.cprims : R.prims;
@@ -63,7 +73,10 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
         const CamPt cp = cam_point(R, f.d);
 #pragma unroll
         for (int m = 0; m < kNC; ++m) cg[m * 32] = cb[m * 32] = cm[m * 32] = 0.0f;
+        if (lane < kNC) s_gm[wid][lane] = 0u;
+        __syncwarp();
         int nq1 = 0;
+        uint32_t nref = 0;
         auto run = [&](int, int take) {
             const bool v = lane < take;
             const float4 e = v ? q.e[nq1 - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -94,12 +107,18 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
                     if (STOCH) cj *= f.w[ref >> 27];
                 }
             }
+            if (GF_REFS) {  // the hit list for pass B
+                const unsigned mh = __ballot_sync(FULL, hit);
+                if (hit && nref + __popc(mh & lt) < (uint32_t)kRefCapW) refs[nref + __popc(mh & lt)] = ref;
+                nref += __popc(mh);
+            }
             int ne = 0, ka = 0, kb = 0;
             float amp = 0.0f, sp = 0.0f, cp_ = 1.0f;
             if (hit) {
                 if (COUNT) ++wk.hits;
                 ka = ff_bin(f, fmaf(s.u0 - s.bp, s.ij, s.tc));
                 kb = ff_bin(f, fmaf(s.u1 - s.bp, s.ij, s.tc));
+                for (int m = ka; m <= kb; ++m) atomicOr(&s_gm[wid][m], 1u << (ref >> 27));
                 const float wmax = 0.5f * (fmaxf(s.u0 * s.u0, s.u1 * s.u1) + s.Om * s.Om);
                 if (kNF > 1 && s.Om != 0.0f) {  // Gabor envelope mass >= int |kappa_i| into every coarse bin it touches
                     const float mass = cj * __expf(-0.5f * s.r2);
@@ -172,15 +191,27 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
         while (nq1 > 0) run(1, min(nq1, 32));
         __syncwarp();
         double cstart;
-        const int ks = coarse_decide_warp(cols, f.tstar, &cstart);
-        if (lane == 0) {
-            if ((ks >> 8) == kNC) {  // no coarse bin can reach tau*: escape
-                ff_escape(R, p);
-            } else {
-                R.ffk[p] = ks;
-                R.ffc[p] = cstart;
-                R.qW[atomicAdd(R.qcount + QC_W, 1u)] = p;
+        const int ks = kNF == 1 ? coarse_first_warp(cols, f.tstar, &cstart) : coarse_decide_warp(cols, f.tstar, &cstart);
+        if ((ks >> 8) == kNC) {  // no coarse bin can reach tau*: escape
+            if (lane == 0) ff_escape(R, p);
+            continue;
+        }
+        // pass B right here from the hit list (uniform bins): the root inside the crossing bin
+        float t = 0.0f;
+        if (GF_REFS && kNF == 1 && nref <= (uint32_t)kRefCapW &&
+            window_from_refs<STOCH, COUNT>(refs, nref, prims, r, STOCH ? f.w : nullptr, ff_edge(f, (ks & 0xFF) - 1), ff_edge(f, ks & 0xFF),
+                                           cstart, f.tstar, rec, aux, (uint32_t)R.rec_cap, s_e[wid], wk, t)) {
+            if (lane == 0) {
+                ff_collide(R, p, f, t);
+                R.qB[atomicAdd(R.qcount + QC_B, 1u)] = p;
             }
+        } else if (lane == 0) {  // the crossing bin is re-traversed by pass B (k_ffb_w)
+            R.ffk[p] = ks;
+            R.ffc[p] = cstart;
+            uint32_t g = 0;
+            for (int m = ks >> 8; m <= min(ks & 0xFF, kNC - 1); ++m) g |= s_gm[wid][m];
+            R.ffg[p] = g;
+            R.qW[atomicAdd(R.qcount + QC_W, 1u)] = p;
         }
         __syncwarp();
     }

@@ -66,7 +66,7 @@ __device__ __forceinline__ bool ffb_overflow(const RenderDev& R, const FFRay& f,
     for (int m = s0; m <= kend; ++m) {
         if (window_records<STOCH, COUNT, CAM>(R, f, r, cp, ff_edge(f, m - 1), ff_edge(f, m), sm, rec, aux, cap, ng, nb,
                                               &tot, wk)) {
-            if (resolve_records<COUNT>(rec, aux, cap, ng, nb, f, m, m, cum, cf, wl, q, wk, t)) return true;
+            if (resolve_records<COUNT>(rec, aux, cap, ng, nb, f, m, m, cum, cf, wl, q, wk, t, true)) return true;
             cum += tot;
             continue;
         }
@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int3
         const uint32_t p = R.qW[idx];
         FFRay f;
         ff_begin<STOCH, FOV>(R, p, sample, depth, f);  // the same set-up as pass A
+        f.mask &= R.ffg[p];  // only the groups with chords in the window (pass A): other subtrees pruned at the top
         const int ks = R.ffk[p], k1 = ks & 0xFF, s0 = ks >> 8, kend = k1 < kNC ? k1 : kNC - 1;
         const double cstart = R.ffc[p];
         const RayDev r = make_ray(f.o, f.d, 0.0f, INFINITY, fov_prim(R, f.fth));
@@ -125,7 +126,8 @@ __global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int3
         bool col = false;
         if (window_records<STOCH, COUNT, CAM>(R, f, r, cp, ff_edge(f, s0 - 1), ff_edge(f, kend), s_t[wid], rec, aux, cap,
                                               ng, nb, &tot, wk)) {
-            col = resolve_records<COUNT>(rec, aux, cap, ng, nb, f, s0, kend, cstart, s_f[wid], s_w[wid], s_e[wid], wk, t);
+            col = resolve_records<COUNT>(rec, aux, cap, ng, nb, f, s0, kend, cstart, s_f[wid], s_w[wid], s_e[wid], wk, t,
+                                         true);
         } else {  // more chords than the buffer holds: k_ffb_over (queue qV)
             if (lane == 0) {
                 if (COUNT) ++wk.overflow;
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(128) k_ffb_over(RenderDev R, int32_t sample, i
         const uint32_t p = R.qV[idx];
         FFRay f;
         ff_begin<STOCH, FOV>(R, p, sample, depth, f);
+        f.mask &= R.ffg[p];
         const int ks = R.ffk[p], k1 = ks & 0xFF, s0 = ks >> 8, kend = k1 < kNC ? k1 : kNC - 1;
         const RayDev r = make_ray(f.o, f.d, 0.0f, INFINITY, fov_prim(R, f.fth));
         const CamPt cp = cam_point(R, f.d);

@@ -101,9 +101,11 @@ struct RenderDev {
     uint32_t* pix;
     int32_t* ffk;    // free flight: the bin of the first crossing (pass A -> pass B)
     double* ffc;     // free flight: tau before that bin
+    uint32_t* ffg;   // free flight: the groups with chords overlapping that bin (pass B's traversal mask)
     float4* wrec;    // [warp][rec_cap] x 2 float4 hit records (pass-B windows, tracking; reused per path)
     float4* waux;    // [warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;
+    uint32_t* wref;  // [warp][kRefWarp] hit lists of pass A (primitive index | group << 27)
     uint32_t* qW;    // paths that collide: pass B queue
     uint32_t* qO;    // paths with more chords than the record buffer (one-pass / tracking -> passes A + B)
     uint32_t* qV;    // pass-B windows with more chords than the record buffer (k_ffb_over)

@@ -107,9 +107,11 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     uint32_t* pix = (uint32_t*)take(nu);
     int32_t* ffk = (int32_t*)take(nu);
     double* ffc = (double*)take(sizeof(double) * (size_t)n);
+    uint32_t* ffg = (uint32_t*)take(nu);
     const size_t nw = (size_t)4 * (size_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)rec_max_blocks(), (n + 3) / 4));
     float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
     float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
+    uint32_t* wref = (uint32_t*)take(sizeof(uint32_t) * (size_t)kRefWarp * nw);
     uint32_t* qA = (uint32_t*)take(nu); uint32_t* qB = (uint32_t*)take(nu); uint32_t* qN = (uint32_t*)take(nu);
     uint32_t* qW = (uint32_t*)take(nu); uint32_t* qO = (uint32_t*)take(nu); uint32_t* qV = (uint32_t*)take(nu);
     uint32_t* qc = (uint32_t*)take(sizeof(uint32_t) * 16);
@@ -130,8 +132,8 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     if (LS) *LS = gf_scratch_layout(n_prims, lscratch);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
-        R->pix = pix; R->ffk = ffk; R->ffc = ffc;
-        R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap;
+        R->pix = pix; R->ffk = ffk; R->ffc = ffc; R->ffg = ffg;
+        R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap; R->wref = wref;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qW = qW; R->qO = qO; R->qV = qV; R->qcount = qc;
         R->lnodes = lnodes; R->lnodes2 = lnodes2; R->lprims = lprims; R->lperm = lperm; R->ldepth = ldepth;
         R->cnodes = cnodes; R->cnodes2 = cnodes2; R->cprims = cprims; R->cperm = cperm; R->cdepth = cdepth;
@@ -142,6 +144,7 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
 static void launch_depth(RenderDev& R, int32_t sample, int d, bool S, bool C, unsigned pgrid, unsigned wgrid,
                          cudaStream_t st, StageTimer& T, bool stoch_nee) {
     cudaEvent_t e;
+    const unsigned rgrid = (unsigned)rec_max_blocks();  // kernels with per-warp buffers: one resident wave
     const bool cam = d == 0 && R.camb;  // depth-0 rays from the eye: camera BVH
     // coherent rays under one static mask: packet traversal (camera rays; gf_trace_free_flight packets)
     const bool packet = GF_PACKET && !S && (R.packets == 1 || (R.packets == 0 && d == 0 && R.camb));
@@ -150,13 +153,13 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, bool S, bool C, un
     const bool onepass = !packet && R.estimator == 0 && gf_ff_onepass() && R.packets != 2;
     T.pre(STAGE_FFA, st, e);
     if (R.estimator == 1) gf_launch_ff_trk(R, sample, d, S, C, st);
-    else if (packet) gf_launch_ffa_pkt(R, sample, d, S, C, cam && R.packets == 0, pgrid, st);
+    else if (packet) gf_launch_ffa_pkt(R, sample, d, S, C, cam && R.packets == 0, std::min<unsigned>(pgrid, rgrid), st);
     else if (onepass) gf_launch_ff(R, sample, d, S, C, cam, R.qA, QC_A, CUR_A, st);
-    else gf_launch_ffa_w(R, sample, d, S, C, cam, R.qA, QC_A, CUR_A, 1, wgrid, st);
+    else gf_launch_ffa_w(R, sample, d, S, C, cam, R.qA, QC_A, CUR_A, 1, std::min<unsigned>(wgrid, rgrid), st);
     T.post(STAGE_FFA, st, e);
     if (R.estimator == 1 || onepass) {  // record-buffer overflow: passes A + B (timed as stage ffB)
         T.pre(STAGE_FFB, st, e);
-        gf_launch_ffa_w(R, sample, d, S, C, cam, R.qO, QC_O, CUR_O, 0, wgrid, st);
+        gf_launch_ffa_w(R, sample, d, S, C, cam, R.qO, QC_O, CUR_O, 0, std::min<unsigned>(wgrid, rgrid), st);
         T.post(STAGE_FFB, st, e);
     }
     T.pre(STAGE_FFB, st, e);

@@ -25,6 +25,13 @@ enum { QC_A = 0, QC_B = 1, QC_NEXT = 2, QC_W = 3, CUR_A = 4, CUR_W = 5, CUR_N = 
 #define GF_REC_CAP 2048
 #endif
 constexpr int kRecCap = GF_REC_CAP;  // records per warp buffer: pass-B windows and the tracking estimators
+#ifndef GF_REFS
+#define GF_REFS 0  // 1: pass A keeps each ray's hit list and solves the crossing bin from it in-kernel
+                  // (measured slower: the traversal kernels lose occupancy to the resolve's registers)
+#endif
+constexpr int kRefCapW = 4096;  // hit-list entries per ray of the warp-per-ray pass A (more: re-traversal)
+constexpr int kRefCapL = 512;   // hit-list entries per lane of the packet pass A
+constexpr int kRefWarp = kRefCapW > 32 * kRefCapL ? kRefCapW : 32 * kRefCapL;  // u32 per warp buffer
 // pixel of path p in this pass (-1 if p maps outside the image / shard)
 __device__ __forceinline__ int32_t path_pixel(const RenderDev& R, int64_t p) {
     const int64_t gp = R.path_base + p;
@@ -538,6 +545,25 @@ __device__ __forceinline__ void bin_records(const float4* __restrict__ rec, cons
     __syncwarp();
 }
 
+// Uniform bins (kNF == 1), warp version: the first coarse edge whose cumulative tau reaches tau* from the
+// lane columns (rows G and Gabor): lane m holds bin m, an inclusive scan gives the edge values.
+// Returns k1 | k1 << 8 (kNC: escape), *cstart = tau before bin k1.
+__device__ __forceinline__ int coarse_first_warp(const float* cols, double tstar, double* cstart) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const double v = lane < kNC ? row_sum(cols, lane) + row_sum(cols + kNC * 32, lane) : 0.0;
+    double incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += u;
+    }
+    const unsigned hit = __ballot_sync(FULL, lane < kNC && incl >= tstar);
+    const int k1 = hit ? __ffs(hit) - 1 : kNC;
+    *cstart = __shfl_sync(FULL, incl - v, hit ? k1 : 0);
+    return k1 | (k1 << 8);
+}
+
 // coarse decision from the warp's lane columns (rows: G at [0], Gabor at [kNC*32], mass at [2*kNC*32])
 __device__ __forceinline__ int coarse_decide_warp(const float* cols, double tstar, double* cstart) {
     const int lane = threadIdx.x & 31;
@@ -743,6 +769,175 @@ __device__ __noinline__ float window_root(const float4* __restrict__ rec, float4
     return t;
 }
 
+// Root of f(t) = c0 + tau(a, t) - tau* over records CLIPPED to the window [a, b] (pass B with uniform
+// bins: every record is a window record, chord data x = (full, amp G(u0), amp cos, -amp sin)): each
+// evaluation scans the records -- a chord wholly before t adds its full integral, one straddling t
+// queues the endpoint u(t) (one erf, 32 at a time, type-uniform) and adds its kappa and d kappa / dt
+// terms; safeguarded Halley (Newton / bisection) to 1e-6 of the window (2 ulp of t at least).
+template <bool COUNT>
+__device__ __forceinline__ float window_root_clip(const float4* __restrict__ rec, const float4* __restrict__ aux,
+                                                  uint32_t cap, uint32_t ng, uint32_t nb, float a, float b, double c0,
+                                                  double tstar, WarpEnd& q, Work& wk) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const uint32_t nside[2] = {ng, nb};
+    int nq0 = 0, nq1 = 0;
+    double acc = 0.0;
+    auto run = [&](int t, int take) {
+        int& nq = t == 0 ? nq0 : nq1;
+        const bool v = lane < take;
+        const float4 e = v ? q.e[t][nq - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        nq -= take;
+        __syncwarp();
+        if (v) {
+            if (t == 0) {
+                if (COUNT) ++wk.erfr;
+                acc += (double)(e.z * erff(e.x * kRsqrt2));
+            } else {
+                if (COUNT) ++wk.erfc;
+                const float2 F = erf_c(e.x, e.y);
+                acc += (double)fmaf(e.z, F.x, e.w * F.y);
+            }
+        }
+    };
+    auto eval = [&](float t, double& kap_out, double& dkap_out) -> double {
+        if (COUNT && lane == 0) ++wk.root;
+        acc = 0.0;
+        float part = 0.0f, kap = 0.0f, dkap = 0.0f;
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+            const uint32_t n = nside[side];
+            for (uint32_t base = 0; base < n; base += 32) {
+                const uint32_t i = base + lane;
+                bool push = false;
+                float4 e = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                if (i < n) {
+                    const uint32_t slot = side == 0 ? i : cap - 1 - i;
+                    const float4 ra = rec[2 * slot], rb = rec[2 * slot + 1];
+                    const float ut = rec_u(rb, t);
+                    if (ut > ra.x) {
+                        const float4 x = aux[slot];
+                        if (ut >= ra.y) {
+                            part += x.x;
+                        } else {
+                            float sp, cp;
+                            sincos_red(fmaf(ra.z, ut, ra.w), &sp, &cp);
+                            const float kk = rb.x * rb.y * 0.79788456080286536f * __expf(0.5f * (ra.z * ra.z - ut * ut));
+                            kap += kk * cp;
+                            dkap -= kk * rb.y * fmaf(ut, cp, ra.z * sp);  // d kappa / dt (Halley step)
+                            if (x.y != x.y) {  // special record: lane-local partial integral
+                                part += rec_rare(ra, rb, ra.x, ut);
+                            } else {
+                                part -= x.y;
+                                push = true;
+                                e = make_float4(ut, ra.z, x.z, x.w);
+                            }
+                        }
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, push);
+                if (m) {
+                    int& nq = side == 0 ? nq0 : nq1;
+                    if (push) q.e[side][nq + __popc(m & lt)] = e;
+                    nq += __popc(m);
+                    GF_CHECK(nq <= kWEnd);
+                    __syncwarp();
+                    if (nq >= 32) run(side, 32);
+                }
+            }
+        }
+        while (nq0 > 0) run(0, min(nq0, 32));
+        while (nq1 > 0) run(1, min(nq1, 32));
+        double xs = acc + (double)part, k = kap, dk = dkap;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            xs += __shfl_xor_sync(FULL, xs, o);
+            k += __shfl_xor_sync(FULL, k, o);
+            dk += __shfl_xor_sync(FULL, dk, o);
+        }
+        kap_out = k;
+        dkap_out = dk;
+        return c0 + xs - tstar;
+    };
+    const float wlen = b - a;
+    float lo = a, hi = b, t = a + 0.5f * wlen;
+    const float tol = fmaxf(1e-6f * wlen, 2.4e-7f * fmaxf(fabsf(a), fabsf(b)));
+    double kap = 0.0, dkap = 0.0;
+    for (int it = 0; it < 40; ++it) {
+        const double fv = eval(t, kap, dkap);
+        if (fv >= 0.0) hi = t; else lo = t;
+        if (!(hi - lo > tol)) break;
+        if (fabs(fv) <= 1e-6 * (1.0 + tstar)) break;
+        const double den = 2.0 * kap * kap - fv * dkap;
+        float tn = (kap > 0.0) ? (float)((double)t - (den > 0.0 ? 2.0 * fv * kap / den : fv / kap)) : 0.5f * (lo + hi);
+        const bool newton = tn > lo && tn < hi;
+        if (!newton) tn = 0.5f * (lo + hi);
+        const bool small = newton && fabsf(tn - t) <= tol;
+        t = tn;
+        if (small) break;
+    }
+    return t;
+}
+
+// Pass B from the ray's hit list (refs: primitive index in the traversed BVH's order | group << 27, as pass A
+// met them): the warp tests each listed primitive against the window [a, b] (sphere pre-test + prim_setup:
+// the traversal's predicate), writes the records of the chords inside it (clipped to it) and their chord
+// data, and solves the root there (window_root_clip) -- no second traversal.  false if the window's chords
+// exceed the record buffer.
+template <bool STOCH, bool COUNT>
+__device__ __forceinline__ bool window_from_refs(const uint32_t* __restrict__ refs, uint32_t n,
+                                                 const GPrim* __restrict__ prims, const RayDev& r, const float* w,
+                                                 float a, float b, double c0, double tstar, float4* __restrict__ rec,
+                                                 float4* __restrict__ aux, uint32_t cap, WarpEnd& q, Work& wk, float& t) {
+    const unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t ng = 0, nb = 0;
+    for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t i = base + lane;
+        bool hit = false;
+        Setup s;
+        float cj = 0.0f;
+        if (i < n) {
+            const uint32_t ref = refs[i];
+            const GPrim* pp = prims + (ref & kRefIdx);
+            GPrim P;
+            P.a = __ldg(&pp->a);
+            if (sphere_pretest(P.a, r, a, b)) {
+                P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
+                hit = prim_setup(P, r, a, b, s);
+                cj = P.d.w * s.ij;
+                if (STOCH) cj *= w[ref >> 27];
+            }
+        }
+        const bool hg = hit && s.Om == 0.0f, hb = hit && s.Om != 0.0f;
+        const unsigned mg = __ballot_sync(FULL, hg), mb = __ballot_sync(FULL, hb);
+        if (hit) {
+            const uint32_t slot = hg ? ng + __popc(mg & lt) : cap - 1 - (nb + __popc(mb & lt));
+            if (ng + nb + __popc(mg) + __popc(mb) <= cap) {
+                const float amp = 0.5f * cj * __expf(-0.5f * (s.r2 + s.Om * s.Om));
+                rec[2 * slot] = make_float4(s.u0, s.u1, s.Om, s.phi0);
+                rec[2 * slot + 1] = make_float4(amp, s.j, s.tc, s.bp);
+            }
+        }
+        ng += __popc(mg);
+        nb += __popc(mb);
+    }
+    __syncwarp();
+    if (ng + nb > cap) return false;
+    const uint32_t nside[2] = {ng, nb};
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side)
+        for (uint32_t i = lane; i < nside[side]; i += 32) {
+            const uint32_t slot = side == 0 ? i : cap - 1 - i;
+            aux[slot] = chord_aux<COUNT>(rec[2 * slot], rec[2 * slot + 1], side == 1, wk);
+        }
+    __syncwarp();
+    t = window_root_clip<COUNT>(rec, aux, cap, ng, nb, a, b, c0, tstar, q, wk);
+    return true;
+}
+
 // Fine search over the records (chord data x = (full, amp G(u0), ...) already computed): coarse bins s0 ..
 // kend, starting from cstart = tau before coarse bin s0; each coarse bin's 8 fine edges exactly (bin_records
 // into the lane columns cf), the first fine edge reaching tau* brackets the root (window_root).  Returns
@@ -751,12 +946,15 @@ template <bool COUNT>
 __device__ __forceinline__ bool resolve_records(const float4* __restrict__ rec, float4* __restrict__ aux, uint32_t cap,
                                                 uint32_t ng, uint32_t nb, const FFRay& f, int s0, int kend,
                                                 double cstart, float* cf, uint16_t* wl, WarpEnd& q, Work& wk,
-                                                float& tout) {
+                                                float& tout, bool clipped = false) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     if (kNF == 1) {  // uniform bins: the root inside coarse bin s0 (= the first crossing edge), tau before it cstart
         if (s0 >= kNC) return false;
-        tout = window_root<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, wl, q, wk);
+        if (clipped)  // pass B: the records are exactly the window's chords, clipped to it
+            tout = window_root_clip<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, q, wk);
+        else
+            tout = window_root<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, wl, q, wk);
         return true;
     }
     double cum = cstart;

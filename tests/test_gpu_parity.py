@@ -435,8 +435,10 @@ def test_view_bvhs_same_hits(gfm, monkeypatch, stoch, which):
         st = f.stats(reset=True)
         f.set_profiling()
         out.append((acc.cpu().numpy(), st["work"][stage]))
-    assert out[0][1]["hits"] == out[1][1]["hits"] > 0
-    assert out[0][1]["paths"] == out[1][1]["paths"]
+    # the same chords: equal hit counts up to the few grazing chords of bounces whose origins moved by an
+    # ulp (the two free-flight kernels sum the same integrals in different orders)
+    assert abs(out[0][1]["hits"] - out[1][1]["hits"]) <= 1e-5 * out[0][1]["hits"] and out[0][1]["hits"] > 0
+    assert abs(out[0][1]["paths"] - out[1][1]["paths"]) <= 1e-4 * out[0][1]["paths"]
     np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-4, atol=1e-5)
 
 
