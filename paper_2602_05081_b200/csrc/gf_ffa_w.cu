@@ -77,6 +77,22 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
         __syncwarp();
         int nq1 = 0;
         uint32_t nref = 0;
+        // Windows of bins [wa, wb], front to back: each window's chords, clipped to it, go into its bins and
+        // the exact prefix at its edges decides -- a ray whose first crossing lies in an early window never
+        // visits the rest of the scene (the edge values are the same sums as in one sweep: C17 unchanged).
+        // R.ff_win 1: one split, after the bin where tau*/kappa (kappa at the path's last collision, scaled
+        // by win_scale) predicts the crossing; 2: windows of 1, 2, 4, .. bins; 0: one sweep.
+        int split = kNC;  // first bin of the second window (kNC: one window)
+        if (kNF == 1 && R.ff_win == 1 && depth > 0) {
+            const float k0 = R.fkap[p];
+            if (k0 > 0.0f)
+                split = (int)fmin((double)kNC, fmax(1.0, R.win_scale * (f.tstar / k0 - (double)f.tlo) * f.ibw + 1.0));
+        }
+        int ks = kNC;
+        double cstart = 0.0;
+        for (int wa = 0; wa < kNC;) {
+        const int wb = kNF > 1 ? kNC - 1 : R.ff_win == 2 ? min(kNC - 1, 2 * wa) : (wa < split ? split - 1 : kNC - 1);
+        const float wlo = ff_edge(f, wa - 1), whi = ff_edge(f, wb);
         auto run = [&](int, int take) {
             const bool v = lane < take;
             const float4 e = v ? q.e[nq1 - take + lane] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -100,9 +116,9 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
                 GPrim P;
                 P.a = __ldg(&pp->a);
                 if (COUNT) ++wk.tests;
-                if (sphere_pretest(P.a, r, f.tlo, f.thi)) {
+                if (sphere_pretest(P.a, r, wlo, whi)) {
                     P.b = __ldg(&pp->b); P.c = __ldg(&pp->c); P.d = __ldg(&pp->d);
-                    hit = prim_setup(P, r, f.tlo, f.thi, s);
+                    hit = prim_setup(P, r, wlo, whi, s);
                     cj = P.d.w * s.ij;
                     if (STOCH) cj *= f.w[ref >> 27];
                 }
@@ -116,8 +132,8 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
             float amp = 0.0f, sp = 0.0f, cp_ = 1.0f;
             if (hit) {
                 if (COUNT) ++wk.hits;
-                ka = ff_bin(f, fmaf(s.u0 - s.bp, s.ij, s.tc));
-                kb = ff_bin(f, fmaf(s.u1 - s.bp, s.ij, s.tc));
+                ka = min(wb, max(wa, ff_bin(f, fmaf(s.u0 - s.bp, s.ij, s.tc))));  // (the chord is clipped to
+                kb = min(wb, max(wa, ff_bin(f, fmaf(s.u1 - s.bp, s.ij, s.tc))));  //  the window)
                 for (int m = ka; m <= kb; ++m) atomicOr(&s_gm[wid][m], 1u << (ref >> 27));
                 const float wmax = 0.5f * (fmaxf(s.u0 * s.u0, s.u1 * s.u1) + s.Om * s.Om);
                 if (kNF > 1 && s.Om != 0.0f) {  // Gabor envelope mass >= int |kappa_i| into every coarse bin it touches
@@ -187,11 +203,13 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
                 __syncwarp();
                 if (nq1 >= 32) run(1, 32);
             }
-        }, [&](float4 lo, float4 hi) { return ff_box<CAM>(r, cp, lo, hi, f.tlo, f.thi); });
+        }, [&](float4 lo, float4 hi) { return ff_box<CAM>(r, cp, lo, hi, wlo, whi); });
         while (nq1 > 0) run(1, min(nq1, 32));
         __syncwarp();
-        double cstart;
-        const int ks = kNF == 1 ? coarse_first_warp(cols, f.tstar, &cstart) : coarse_decide_warp(cols, f.tstar, &cstart);
+        ks = kNF == 1 ? coarse_first_warp(cols, f.tstar, &cstart, wb) : coarse_decide_warp(cols, f.tstar, &cstart);
+        if ((ks >> 8) < kNC) break;
+        wa = wb + 1;
+        }
         if ((ks >> 8) == kNC) {  // no coarse bin can reach tau*: escape
             if (lane == 0) ff_escape(R, p);
             continue;

@@ -95,24 +95,25 @@ __device__ __forceinline__ bool ffb_overflow(const RenderDev& R, const FFRay& f,
 }
 
 template <bool STOCH, bool COUNT, bool FOV, bool CAM>
-__global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int32_t depth) {
+__global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int32_t depth, const uint32_t* __restrict__ q_in,
+                                               int cnt_slot, int cur_slot) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];
     __shared__ float s_f[4][kNF * 32];
     __shared__ uint16_t s_w[4][kWinCap];
     const unsigned FULL = 0xFFFFFFFFu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t count = R.qcount[QC_W], cap = (uint32_t)R.rec_cap;
+    const uint32_t count = R.qcount[cnt_slot], cap = (uint32_t)R.rec_cap;
     const size_t gw = (size_t)blockIdx.x * 4 + wid;
     float4* __restrict__ rec = R.wrec + gw * cap * 2;
     float4* __restrict__ aux = R.waux + gw * cap;
     Work wk;
     while (true) {
         uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(R.qcount + CUR_W, 1u);
+        if (lane == 0) idx = atomicAdd(R.qcount + cur_slot, 1u);
         idx = __shfl_sync(FULL, idx, 0);
         if (idx >= count) break;
-        const uint32_t p = R.qW[idx];
+        const uint32_t p = q_in[idx];
         FFRay f;
         ff_begin<STOCH, FOV>(R, p, sample, depth, f);  // the same set-up as pass A
         f.mask &= R.ffg[p];  // only the groups with chords in the window (pass A): other subtrees pruned at the top
@@ -122,12 +123,12 @@ __global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int3
         const CamPt cp = cam_point(R, f.d);
         uint32_t ng = 0, nb = 0;
         double tot = 0.0;
-        float t = 0.0f;
+        float t = 0.0f, kap = 0.0f;
         bool col = false;
         if (window_records<STOCH, COUNT, CAM>(R, f, r, cp, ff_edge(f, s0 - 1), ff_edge(f, kend), s_t[wid], rec, aux, cap,
                                               ng, nb, &tot, wk)) {
             col = resolve_records<COUNT>(rec, aux, cap, ng, nb, f, s0, kend, cstart, s_f[wid], s_w[wid], s_e[wid], wk, t,
-                                         true);
+                                         true, &kap);
         } else {  // more chords than the buffer holds: k_ffb_over (queue qV)
             if (lane == 0) {
                 if (COUNT) ++wk.overflow;
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int3
         }
         if (lane == 0) {
             if (col) {
-                ff_collide(R, p, f, t);
+                ff_collide(R, p, f, t, kap);
                 R.qB[atomicAdd(R.qcount + QC_B, 1u)] = p;
             } else {
                 ff_escape(R, p);  // no fine edge reached tau* (a coarse bin's bound only)
@@ -343,9 +344,11 @@ unsigned gf_rec_grid(int64_t n_paths) {
 
 void gf_launch_ffb(RenderDev& R, int32_t sample, int d, bool stoch, bool count, bool cam, cudaStream_t st) {
     const unsigned g = gf_rec_grid(R.n_paths);
+    uint32_t* const q = R.qW;
+    const int cs = QC_W, cu = CUR_W;
 #define GF_FFB(S_, C_, F_, M_)                                              \
     do {                                                                    \
-        k_ffb_w<S_, C_, F_, M_><<<g, 128, 0, st>>>(R, sample, d);           \
+        k_ffb_w<S_, C_, F_, M_><<<g, 128, 0, st>>>(R, sample, d, q, cs, cu); \
         k_ffb_over<S_, C_, F_, M_><<<gf_persist_blocks() / 16, 128, 0, st>>>(R, sample, d); \
     } while (0)
 #define GF_FFB2(S_, C_)                                                         \

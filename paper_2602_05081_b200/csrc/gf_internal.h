@@ -102,6 +102,7 @@ struct RenderDev {
     int32_t* ffk;    // free flight: the bin of the first crossing (pass A -> pass B)
     double* ffc;     // free flight: tau before that bin
     uint32_t* ffg;   // free flight: the groups with chords overlapping that bin (pass B's traversal mask)
+    float* fkap;     // free flight: kappa at the path's last collision (0: unknown), the next pass A's first cut
     float4* wrec;    // [warp][rec_cap] x 2 float4 hit records (pass-B windows, tracking; reused per path)
     float4* waux;    // [warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;
@@ -138,6 +139,9 @@ struct RenderDev {
     // (appended last, so the hot kernels' parameter offsets stay as measured)
     int32_t tomo_pkt_min;  // tomography chunks with at least this many paths take k_tomo_pkt
     int32_t ffb_cam;       // pass B of depth-0 rays walks the camera BVH (1) or the world BVH (0)
+    int32_t ff_win;        // pass A of extension rays in windows: 0 one sweep; 1 split at the bin predicted from
+                           // kappa at the path's last collision; 2 windows of 1, 2, 4, .. bins on every ray
+    float win_scale;       // ff_win 1: the split bin is win_scale x the predicted crossing bin
 };
 
 cudaError_t gf_launch_load(const LoadArgs& A, void* out, uint8_t* group, uint32_t* err, uint32_t* lfmax_bits,

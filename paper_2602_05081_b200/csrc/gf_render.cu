@@ -108,6 +108,7 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     int32_t* ffk = (int32_t*)take(nu);
     double* ffc = (double*)take(sizeof(double) * (size_t)n);
     uint32_t* ffg = (uint32_t*)take(nu);
+    float* fkap = (float*)take(nf);
     const size_t nw = (size_t)4 * (size_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)rec_max_blocks(), (n + 3) / 4));
     float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
     float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
@@ -132,7 +133,7 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     if (LS) *LS = gf_scratch_layout(n_prims, lscratch);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
-        R->pix = pix; R->ffk = ffk; R->ffc = ffc; R->ffg = ffg;
+        R->pix = pix; R->ffk = ffk; R->ffc = ffc; R->ffg = ffg; R->fkap = fkap;
         R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap; R->wref = wref;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qW = qW; R->qO = qO; R->qV = qV; R->qcount = qc;
         R->lnodes = lnodes; R->lnodes2 = lnodes2; R->lprims = lprims; R->lperm = lperm; R->ldepth = ldepth;

@@ -31,7 +31,7 @@ constexpr int kRecCap = GF_REC_CAP;  // records per warp buffer: pass-B windows 
 #endif
 constexpr int kRefCapW = 4096;  // hit-list entries per ray of the warp-per-ray pass A (more: re-traversal)
 constexpr int kRefCapL = 512;   // hit-list entries per lane of the packet pass A
-constexpr int kRefWarp = kRefCapW > 32 * kRefCapL ? kRefCapW : 32 * kRefCapL;  // u32 per warp buffer
+constexpr int kRefWarp = GF_REFS ? (kRefCapW > 32 * kRefCapL ? kRefCapW : 32 * kRefCapL) : 32;  // u32 per warp buffer
 // pixel of path p in this pass (-1 if p maps outside the image / shard)
 __device__ __forceinline__ int32_t path_pixel(const RenderDev& R, int64_t p) {
     const int64_t gp = R.path_base + p;
@@ -157,7 +157,8 @@ __device__ __forceinline__ void ff_escape(const RenderDev& R, uint32_t p) {
     if (R.tout) R.tout[R.path_base + p] = INFINITY;
 }
 // the collision point becomes the path's new origin
-__device__ __forceinline__ void ff_collide(const RenderDev& R, uint32_t p, const FFRay& f, float t) {
+__device__ __forceinline__ void ff_collide(const RenderDev& R, uint32_t p, const FFRay& f, float t, float kap = 0.0f) {
+    R.fkap[p] = kap;
     R.ox[p] = fmaf(t, f.d.x, f.o.x);
     R.oy[p] = fmaf(t, f.d.y, f.o.y);
     R.oz[p] = fmaf(t, f.d.z, f.o.z);
@@ -547,20 +548,23 @@ __device__ __forceinline__ void bin_records(const float4* __restrict__ rec, cons
 
 // Uniform bins (kNF == 1), warp version: the first coarse edge whose cumulative tau reaches tau* from the
 // lane columns (rows G and Gabor): lane m holds bin m, an inclusive scan gives the edge values.
-// Returns k1 | k1 << 8 (kNC: escape), *cstart = tau before bin k1.
-__device__ __forceinline__ int coarse_first_warp(const float* cols, double tstar, double* cstart) {
+// Only the edges of bins 0 .. kmax count (their chords all in).  Returns k1 | k1 << 8 (kNC: escape),
+// *cstart = tau before bin k1.
+__device__ __forceinline__ int coarse_first_warp(const float* cols, double tstar, double* cstart, int kmax = kNC - 1,
+                                                 double* upto = nullptr) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
-    const double v = lane < kNC ? row_sum(cols, lane) + row_sum(cols + kNC * 32, lane) : 0.0;
+    const double v = lane <= kmax ? row_sum(cols, lane) + row_sum(cols + kNC * 32, lane) : 0.0;
     double incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const double u = __shfl_up_sync(FULL, incl, o);
         if (lane >= o) incl += u;
     }
-    const unsigned hit = __ballot_sync(FULL, lane < kNC && incl >= tstar);
+    const unsigned hit = __ballot_sync(FULL, lane <= kmax && incl >= tstar);
     const int k1 = hit ? __ffs(hit) - 1 : kNC;
     *cstart = __shfl_sync(FULL, incl - v, hit ? k1 : 0);
+    if (upto) *upto = __shfl_sync(FULL, incl, max(kmax, 0));  // tau at the right edge of bin kmax
     return k1 | (k1 << 8);
 }
 
@@ -777,7 +781,7 @@ __device__ __noinline__ float window_root(const float4* __restrict__ rec, float4
 template <bool COUNT>
 __device__ __forceinline__ float window_root_clip(const float4* __restrict__ rec, const float4* __restrict__ aux,
                                                   uint32_t cap, uint32_t ng, uint32_t nb, float a, float b, double c0,
-                                                  double tstar, WarpEnd& q, Work& wk) {
+                                                  double tstar, WarpEnd& q, Work& wk, float* kap_out = nullptr) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -877,6 +881,7 @@ __device__ __forceinline__ float window_root_clip(const float4* __restrict__ rec
         t = tn;
         if (small) break;
     }
+    if (kap_out) *kap_out = (float)kap;  // (at the last evaluated t)
     return t;
 }
 
@@ -946,13 +951,14 @@ template <bool COUNT>
 __device__ __forceinline__ bool resolve_records(const float4* __restrict__ rec, float4* __restrict__ aux, uint32_t cap,
                                                 uint32_t ng, uint32_t nb, const FFRay& f, int s0, int kend,
                                                 double cstart, float* cf, uint16_t* wl, WarpEnd& q, Work& wk,
-                                                float& tout, bool clipped = false) {
+                                                float& tout, bool clipped = false, float* kap_out = nullptr) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     if (kNF == 1) {  // uniform bins: the root inside coarse bin s0 (= the first crossing edge), tau before it cstart
         if (s0 >= kNC) return false;
         if (clipped)  // pass B: the records are exactly the window's chords, clipped to it
-            tout = window_root_clip<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, q, wk);
+            tout = window_root_clip<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, q, wk,
+                                            kap_out);
         else
             tout = window_root<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, wl, q, wk);
         return true;

@@ -33,6 +33,14 @@ def gfm():
     return gf
 
 
+@pytest.fixture(autouse=True, params=["0", "2"], ids=["one_sweep", "windows"])
+def windows(request, monkeypatch):
+    """Pass A of the warp kernel in one sweep, and in front-to-back windows of 1, 2, 4, .. bins on every ray
+    (each window's chords clipped to it, a decision after each): the same first crossings."""
+    monkeypatch.setenv("GF_FF_WIN", request.param)
+    return request.param
+
+
 def field(gfm, scene):
     f = gfm.GaborField(0)
     f.load_primitives(scene)
