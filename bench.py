@@ -212,8 +212,9 @@ def main():
                          "(each rank renders its own sample of every frame, weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--estimator", default="analytic", choices=["analytic", "tracking"],
-                    help="scatter estimator: closed-form tau + root (default) or delta/ratio tracking")
+    ap.add_argument("--estimator", default="analytic", choices=["analytic", "tracking", "uniform"],
+                    help="scatter estimator: closed-form tau + root (default), delta/ratio tracking, or the "
+                         "paper's biased uniform-in-segment free flight (reading U1)")
     ap.add_argument("--foveation", action="store_true",
                     help="foveated rendering variant: gaze at the image centre, all levels in the fovea, "
                          "threshold falling linearly to 0 at eccentricity 0.7 (jitter 0.2)")
@@ -250,6 +251,9 @@ def main():
     if args.estimator == "tracking":
         descs = [dict(d, estimator=1) for d in descs]
         name += " [delta/ratio tracking estimator]"
+    if args.estimator == "uniform":
+        descs = [dict(d, estimator=2) for d in descs]
+        name += " [biased uniform-in-segment free flight (U1)]"
     if args.motion_blur:
         if args.motion_blur == "reference":
             descs = [dict(d, motion_blur=I.motion_blur((1.0, 0.2, 0.0), 0.02)) for d in descs]

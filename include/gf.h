@@ -242,7 +242,9 @@ gf_status gf_grad_params_finish(gf_ctx *ctx, const float *accum, const float *qu
  * equal t-bins of the ray's scene interval -- the root box within [tmin, tmax] -- whose right edge
  * reaches tau*, then the root inside it), +inf if no bin edge reaches tau* (escape).  rays as gf_trace_transmittance (tmax = +inf allowed); t_out: device n floats.
  * flags: 0, or GF_TRACE_PACKETS (32 consecutive rays walk the BVH together, as gf_render's camera
- * rays do).  scratch: device, >= gf_free_flight_scratch_bytes(n). */
+ * rays do), | GF_FF_UNIFORM (the GF_EST_UNIFORM estimator: t* uniform in the crossing bin, u from
+ * stream 8 of (pixel = i, sample 0, depth 0)).  scratch: device, >= gf_free_flight_scratch_bytes(n). */
+#define GF_FF_UNIFORM 4u
 gf_status gf_trace_free_flight(gf_ctx *ctx, const float *rays, int64_t n, uint64_t seed, uint32_t flags,
                                float *t_out, void *scratch, size_t scratch_bytes, gf_stream stream);
 /* Number of t-bins of the free-flight pass A (reading C17: t* is the root inside the first of these
@@ -266,8 +268,9 @@ typedef enum { GF_SHARD_NONE = 0, GF_SHARD_TILES = 1, GF_SHARD_SAMPLES = 2 } gf_
  * with right/up pre-scaled by tan(vfov/2) (*aspect), evaluated in fp32 with
  * correctly rounded operations.  jitter = 0 -> pixel centres.
  * TOMOGRAPHY: per sample tau-hat of the camera ray.
- * SCATTER: free flight (Eq. 5: exact tau_total for the escape test, then the root of
- *   tau(t) = tau* over the whole ray by safeguarded Halley/Newton/bisection, C17), NEE to the
+ * SCATTER: free flight (Eq. 5, C17: tau integrated exactly into the gf_free_flight_bins() t-bins of
+ *   the ray's scene interval, escape if no bin edge reaches tau*, else the root of tau(t) = tau*
+ *   inside the first bin whose right edge does, by safeguarded Halley / bisection), NEE to the
  *   directional light (sun_dir towards the light, irradiance sun_E) with the
  *   nee policy, Henyey-Greenstein phase (g), grey albedo, constant env_L on
  *   escape, max_depth vertices (1 = single scattering), no Russian roulette (C19).
@@ -277,8 +280,11 @@ typedef enum { GF_SHARD_NONE = 0, GF_SHARD_TILES = 1, GF_SHARD_SAMPLES = 2 } gf_
  *   free flight and ratio tracking for NEE against a per-ray piecewise-constant majorant (64 bins
  *   of the summed per-primitive density bounds); unbiased only where kappa >= 0 (C18); tracking
  *   step j of a segment uses Philox block k = 4j of stream 4 (free flight: u0 distance, u1
- *   acceptance) or stream 5 (NEE: u0 distance). */
-typedef enum { GF_EST_ANALYTIC = 0, GF_EST_TRACKING = 1 } gf_estimator;
+ *   acceptance) or stream 5 (NEE: u0 distance).  GF_EST_UNIFORM = the paper's biased alternative
+ *   ("uniform sampling along the candidate segment containing a path vertex"), reading
+ *   U1: the candidate segment is the crossing t-bin of C17 (found exactly, as above) and t* is uniform
+ *   in it, u = Philox stream 8, k = 0 -- no root finding; NEE as GF_EST_ANALYTIC. */
+typedef enum { GF_EST_ANALYTIC = 0, GF_EST_TRACKING = 1, GF_EST_UNIFORM = 2 } gf_estimator;
 #define GF_FOV_LEVELS 1u
 #define GF_FOV_CONTINUOUS 2u
 typedef struct {

@@ -572,7 +572,7 @@ static gf_status check_desc(gf_ctx* c, const gf_render_desc* d) {
     if (d->probe_pixels && (d->n_probe < 0 || d->shard_kind == GF_SHARD_TILES))
         return fail(c, GF_E_INVALID_ARGUMENT, "probe mode: n_probe >= 0 and no tile sharding");
     if (!(d->hg_g > -1.0f && d->hg_g < 1.0f)) return fail(c, GF_E_INVALID_ARGUMENT, "hg_g must be in (-1,1)");
-    if (d->estimator != GF_EST_ANALYTIC && d->estimator != GF_EST_TRACKING)
+    if (d->estimator != GF_EST_ANALYTIC && d->estimator != GF_EST_TRACKING && d->estimator != GF_EST_UNIFORM)
         return fail(c, GF_E_INVALID_ARGUMENT, "bad estimator");
     if (d->motion_blur && !(d->mb_m >= 0.0f && std::isfinite(d->mb_m)))
         return fail(c, GF_E_INVALID_ARGUMENT, "motion blur: mb_m must be finite and >= 0");
@@ -653,7 +653,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     cudaStream_t st = (cudaStream_t)stream;
     // NEE light BVH: a second tree over the primitives with boxes in a frame whose third axis is
     // the light direction (shadow rays become axis-parallel); rebuilt per call, asynchronously
-    R.light = d->mode == GF_MODE_SCATTER && d->estimator == GF_EST_ANALYTIC && c->n > 0 &&
+    R.light = d->mode == GF_MODE_SCATTER && d->estimator != GF_EST_TRACKING && c->n > 0 &&
               env_int("GF_DEBUG_NO_LIGHT_BVH", 0) == 0;
     if (R.light) {
         double z[3] = {d->sun_dir[0], d->sun_dir[1], d->sun_dir[2]};
@@ -675,7 +675,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         }
     }
     // camera BVH for the depth-0 packet kernel (static ext mask, analytic): projective boxes at the eye
-    R.camb = (d->mode == GF_MODE_TOMOGRAPHY || d->estimator == GF_EST_ANALYTIC) && c->n > 0 && !d->motion_blur &&
+    R.camb = (d->mode == GF_MODE_TOMOGRAPHY || d->estimator != GF_EST_TRACKING) && c->n > 0 && !d->motion_blur &&
              env_int("GF_DEBUG_NO_CAMERA_BVH", 0) == 0;  // (motion blur moves the eye per sample)
     // packets pay off once the chunk fills the GPU (small images: one warp per pixel, k_tomo_w)
     R.tomo_pkt_min = env_int("GF_DEBUG_TOMO_PKT_MIN", 1 << 16);
@@ -721,7 +721,7 @@ gf_status gf_free_flight_scratch_bytes(gf_ctx* c, int64_t n, size_t* bytes) {
 gf_status gf_trace_free_flight(gf_ctx* c, const float* rays, int64_t n, uint64_t seed, uint32_t flags, float* t_out,
                                void* scratch, size_t scratch_bytes, gf_stream stream) {
     if (!c) return GF_E_INVALID_ARGUMENT;
-    if (flags & ~GF_TRACE_PACKETS) return fail(c, GF_E_INVALID_ARGUMENT, "bad gf_trace_free_flight flags");
+    if (flags & ~(GF_TRACE_PACKETS | GF_FF_UNIFORM)) return fail(c, GF_E_INVALID_ARGUMENT, "bad gf_trace_free_flight flags");
     if (!c->loaded || !c->built) return fail(c, GF_E_STATE, "free flight before gf_load_primitives / gf_build_bvh");
     if (n < 0 || (n > 0 && (!rays || !t_out || !scratch))) return fail(c, GF_E_INVALID_ARGUMENT, "bad buffers");
     if (((uintptr_t)rays & 15u) != 0) return fail(c, GF_E_INVALID_ARGUMENT, "rays must be 16-byte aligned");
@@ -754,6 +754,7 @@ gf_status gf_trace_free_flight(gf_ctx* c, const float* rays, int64_t n, uint64_t
     R.trays = rays;
     R.tout = t_out;
     R.packets = (flags & GF_TRACE_PACKETS) ? 1 : 2;
+    R.estimator = (flags & GF_FF_UNIFORM) ? GF_EST_UNIFORM : GF_EST_ANALYTIC;
     cudaStream_t st = (cudaStream_t)stream;
     for (int64_t base = 0; base < n; base += chunk) {
         R.path_base = base;

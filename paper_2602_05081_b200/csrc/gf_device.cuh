@@ -83,7 +83,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     }
     return c;
 }
-enum { ST_EXT = 0, ST_NEE = 1, ST_SCAT = 2, ST_CAM = 3, ST_TRK = 4, ST_TRK_NEE = 5, ST_FOV = 6, ST_MB = 7 };
+enum { ST_EXT = 0, ST_NEE = 1, ST_SCAT = 2, ST_CAM = 3, ST_TRK = 4, ST_TRK_NEE = 5, ST_FOV = 6, ST_MB = 7, ST_UNI = 8 };
 // 4 uniforms k0..k0+3 of a stream (k0 multiple of 4) -- one Philox call
 __device__ __forceinline__ uint4 stream_block(uint64_t seed, uint32_t pix, uint32_t smp, uint32_t d, uint32_t st,
                                               uint32_t k0) {

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
         }
         int ks = 0;
         double cstart = 0.0;
+        bool uni = false;
         if (act) {
             if (kNF == 1) {  // uniform bins: the first edge reaching tau*, lane-local over this lane's columns
                 double c = 0.0;
@@ -152,6 +153,10 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
             if ((ks >> 8) == kNC) {  // no coarse bin can reach tau*: escape
                 ff_escape(R, p);
                 act = false;
+            } else if (R.estimator == GF_EST_UNIFORM && kNF == 1) {  // biased: uniform in the crossing bin (U1)
+                ff_collide(R, p, f, ff_uniform_t(R, f, sample, depth, ks & 0xFF));
+                act = false;
+                uni = true;
             } else {
                 R.ffk[p] = ks;
                 R.ffc[p] = cstart;
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(128, GF_MINB_PKT) k_ffa_pkt(RenderDev R, int32
             }
             __syncwarp();
         }
-        push(R.qB, R.qcount + QC_B, done, p);
+        push(R.qB, R.qcount + QC_B, done || uni, p);
         push(R.qW, R.qcount + QC_W, act && !done, p);
         __syncwarp();
     }

@@ -223,6 +223,11 @@ __global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int3
                 ff_collide(R, p, f, t);
                 R.qB[atomicAdd(R.qcount + QC_B, 1u)] = p;
             }
+        } else if (R.estimator == GF_EST_UNIFORM && kNF == 1) {  // biased: uniform in the crossing bin (U1)
+            if (lane == 0) {
+                ff_collide(R, p, f, ff_uniform_t(R, f, sample, depth, ks & 0xFF));
+                R.qB[atomicAdd(R.qcount + QC_B, 1u)] = p;
+            }
         } else if (lane == 0) {  // the crossing bin is re-traversed by pass B (k_ffb_w)
             R.ffk[p] = ks;
             R.ffc[p] = cstart;

@@ -163,9 +163,11 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, bool S, bool C, un
         gf_launch_ffa_w(R, sample, d, S, C, cam, R.qO, QC_O, CUR_O, 0, std::min<unsigned>(wgrid, rgrid), st);
         T.post(STAGE_FFB, st, e);
     }
-    T.pre(STAGE_FFB, st, e);
-    gf_launch_ffb(R, sample, d, S, C, cam && R.ffb_cam, st);
-    T.post(STAGE_FFB, st, e);
+    if (R.estimator != GF_EST_UNIFORM) {
+        T.pre(STAGE_FFB, st, e);
+        gf_launch_ffb(R, sample, d, S, C, cam && R.ffb_cam, st);
+        T.post(STAGE_FFB, st, e);
+    }
     if (R.mode == 2) return;  // gf_trace_free_flight: no NEE
     T.pre(STAGE_NEE, st, e);
     if (R.estimator == 1) gf_launch_nee_rt(R, sample, d, stoch_nee, C, st);  // ratio tracking (record buffers)

@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "gf_device.cuh"
+#include "gf.h"
 #include "gf_internal.h"
 
 namespace gfk {
@@ -150,6 +151,13 @@ __device__ __forceinline__ int ff_begin(const RenderDev& R, uint32_t p, int32_t 
     f.bw = (f.thi - f.tlo) * (1.0f / GF_FF_COARSE);  // coarse bin width (kNC coarse bins, below)
     f.ibw = f.bw > 0.0f ? 1.0f / f.bw : 0.0f;
     return 2;
+}
+
+// GF_EST_UNIFORM (reading U1): t* uniform in the crossing bin k, no root finding
+__device__ __forceinline__ float ff_uniform_t(const RenderDev& R, const FFRay& f, int32_t sample, int32_t depth, int k) {
+    const float a = k <= 0 ? f.tlo : fmaf((float)k, f.bw, f.tlo);
+    const float b = k >= GF_FF_COARSE - 1 ? f.thi : fmaf((float)(k + 1), f.bw, f.tlo);
+    return fminf(fmaf(stream_u(R.seed, f.pix, (uint32_t)sample, (uint32_t)depth, ST_UNI, 0), b - a, a), b);
 }
 
 __device__ __forceinline__ void ff_escape(const RenderDev& R, uint32_t p) {

@@ -21,6 +21,7 @@ MODE_TOMOGRAPHY, MODE_SCATTER = 0, 1
 SHARD_NONE, SHARD_TILES, SHARD_SAMPLES = 0, 1, 2
 TRACE_BRUTE_FORCE = 1
 TRACE_PACKETS = 2
+FF_UNIFORM = 4  # gf_trace_free_flight: GF_EST_UNIFORM (t uniform in the crossing bin)
 
 
 class GFError(RuntimeError):
@@ -267,8 +268,9 @@ class GaborField:
                                                      _ptr(tau), _ptr(T), _ptr(cnt), _stream()))
         return tau, T, cnt
 
-    def trace_free_flight(self, rays, seed=0, packets=False):
-        """gf_trace_free_flight: first t with tau(tmin, t) = tau* per ray (+inf: escape)."""
+    def trace_free_flight(self, rays, seed=0, packets=False, uniform=False):
+        """gf_trace_free_flight: first t with tau(tmin, t) = tau* per ray (+inf: escape); uniform: the
+        GF_EST_UNIFORM estimator (t uniform in the crossing bin)."""
         torch = self.torch
         rays = torch.as_tensor(rays).to(device=self.device, dtype=torch.float32).contiguous().view(-1, 8)
         n = rays.shape[0]
@@ -277,7 +279,8 @@ class GaborField:
         self._check(self.L.gf_free_flight_scratch_bytes(self.ctx, n, ctypes.byref(nb)))
         scratch = self._buf(nb.value)
         self._check(self.L.gf_trace_free_flight(self.ctx, _ptr(rays), n, seed & 0xFFFFFFFFFFFFFFFF,
-                                                TRACE_PACKETS if packets else 0, _ptr(t), _ptr(scratch), nb.value,
+                                                (TRACE_PACKETS if packets else 0) | (FF_UNIFORM if uniform else 0),
+                                                _ptr(t), _ptr(scratch), nb.value,
                                                 _stream()))
         return t[:n]
 

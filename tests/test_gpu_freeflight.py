@@ -185,3 +185,54 @@ def test_free_flight_edge_cases(gfm, orc):
     rays = I.rays_through_box(2, 64)
     rays[:, 7] = rays[:, 3]  # tmax == tmin: nothing to integrate
     assert np.all(np.isinf(f.trace_free_flight(rays).cpu().numpy()))
+
+
+@pytest.mark.parametrize("packets", [False, True])
+def test_free_flight_uniform_in_bin(gfm, orc, packets):
+    """GF_EST_UNIFORM (reading U1, the paper's biased alternative): the crossing bin is
+    the exact one of C17 and t* = e_{k-1} + u (e_k - e_{k-1}) with u = Philox stream 8 -- per sample,
+    from the oracle's tau at the bin edges and the oracle's own Philox.  A flip (different bin or
+    escape decision) is allowed only where the deciding edge's tau is within the fp32 floor of tau*."""
+    sc = I.scene_cfg1()
+    desc = I.render_desc_cfg1()
+    idx = np.arange(64 * 64)
+    o, d = I.camera_rays_f64(desc, idx % 64, idx // 64)
+    rays = np.concatenate([I.pack_rays(o, d), I.rays_through_box(4, 1024)]) if not packets else I.pack_rays(o, d)
+    seed = 0xF1F7
+    f = field(gfm, sc)
+    info = f.scene_info()
+    nb = f.L.gf_free_flight_bins()
+    t_g = f.trace_free_flight(rays, seed=seed, packets=packets, uniform=True).cpu().numpy().astype(np.float64)
+    S = orc.Scene(sc)
+    m = I.policy()["static_mask"]
+    flips, ncol = 0, 0
+    for i in range(len(rays)):
+        xi = orc.uniform(seed, i, 0, 0, 0, 0)
+        tstar = -math.log1p(-xi)
+        edges = _bin_edges(rays[i], info["root_lo"], info["root_hi"], nb)
+        if edges is None:
+            assert np.isinf(t_g[i])
+            continue
+        tau_e = np.array([S.free_flight_diag(rays[i], xi, e, m, None)[0] for e in edges])
+        A = S.trace(rays[i:i + 1], mask=m, nthreads=1)["A"][0]
+        floor = 1e-5 * (1.0 + A)
+        reach = np.nonzero(tau_e >= tstar)[0]
+        if len(reach) == 0:
+            if np.isinf(t_g[i]):
+                continue
+            flips += 1
+            assert np.max(tau_e) >= tstar - floor, (i, t_g[i])
+            continue
+        k = int(reach[0])
+        ncol += 1
+        lo = edges[k - 1] if k > 0 else edges[0] - (edges[-1] - edges[0]) / (nb - 1)  # (k = 0: t_lo)
+        u = orc.uniform(seed, i, 0, 0, 8, 0)
+        t_exp = lo + u * (edges[k] - lo)
+        span = edges[-1] - edges[0] + (edges[1] - edges[0])
+        if np.isfinite(t_g[i]) and abs(t_g[i] - t_exp) <= 1e-5 * span + 1e-6:
+            continue
+        flips += 1  # a neighbouring bin decided in fp32: its deciding edge must be at tau* within the floor
+        assert np.min(np.abs(tau_e - tstar)) <= floor, (i, t_g[i], t_exp, k)
+    assert ncol > len(rays) // 10
+    assert flips <= 0.005 * len(rays), flips
+    print(f"uniform-in-bin packets={packets}: {flips} flips / {len(rays)}")
