@@ -205,17 +205,21 @@ def test_free_flight_uniform_in_bin(gfm, orc, packets):
     t_g = f.trace_free_flight(rays, seed=seed, packets=packets, uniform=True).cpu().numpy().astype(np.float64)
     S = orc.Scene(sc)
     m = I.policy()["static_mask"]
+    # the oracle's tau(tmin, e) at every bin edge of every ray, in one batch (rays cut at the edges)
+    E = [_bin_edges(r, info["root_lo"], info["root_hi"], nb) for r in rays]
+    cut = np.repeat(rays, nb, axis=0)
+    cut[:, 7] = np.concatenate([e if e is not None else np.full(nb, r[3]) for e, r in zip(E, rays)])
+    tr = S.trace(cut, mask=m)
+    tau_all, A_all = tr["tau"].reshape(-1, nb), tr["A"].reshape(-1, nb)[:, -1]
     flips, ncol = 0, 0
     for i in range(len(rays)):
-        xi = orc.uniform(seed, i, 0, 0, 0, 0)
-        tstar = -math.log1p(-xi)
-        edges = _bin_edges(rays[i], info["root_lo"], info["root_hi"], nb)
+        edges = E[i]
         if edges is None:
             assert np.isinf(t_g[i])
             continue
-        tau_e = np.array([S.free_flight_diag(rays[i], xi, e, m, None)[0] for e in edges])
-        A = S.trace(rays[i:i + 1], mask=m, nthreads=1)["A"][0]
-        floor = 1e-5 * (1.0 + A)
+        tstar = -math.log1p(-orc.uniform(seed, i, 0, 0, 0, 0))
+        tau_e = tau_all[i]
+        floor = 1e-5 * (1.0 + A_all[i])
         reach = np.nonzero(tau_e >= tstar)[0]
         if len(reach) == 0:
             if np.isinf(t_g[i]):
