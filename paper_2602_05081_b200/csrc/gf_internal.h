@@ -103,6 +103,8 @@ struct RenderDev {
     double* ffc;     // free flight: tau before that bin
     uint32_t* ffg;   // free flight: the groups with chords overlapping that bin (pass B's traversal mask)
     float* fkap;     // free flight: kappa at the path's last collision (0: unknown), the next pass A's first cut
+    uint32_t* pmask; // stochastic extension masks of the current depth (k_policy) ...
+    float* pw;       // ... and their group weights, kMaxGroups per path
     float4* wrec;    // [warp][rec_cap] x 2 float4 hit records (pass-B windows, tracking; reused per path)
     float4* waux;    // [warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;

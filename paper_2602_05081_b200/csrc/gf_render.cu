@@ -59,6 +59,20 @@ __global__ void __launch_bounds__(128) k_gen_rays(RenderDev R) {
     push(R.qA, R.qcount + QC_A, ok, (uint32_t)p);
 }
 
+// a3 for the free flight of depth `depth`: the extension policy's mask and group weights of every path of
+// queue qA (Tables B1/B2, stream 0 of the path vertex), read by pass A and pass B through ff_begin
+__global__ void __launch_bounds__(128) k_policy(RenderDev R, int32_t sample, int32_t depth) {
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= R.qcount[QC_A]) return;
+    const uint32_t p = R.qA[idx];
+    float w[kMaxGroups];
+    const uint32_t m = policy_for(R.ext, R.sc, ld3(R.dx, R.dy, R.dz, p), R.seed, R.pix[p], (uint32_t)sample,
+                                  (uint32_t)depth, ST_EXT, 1, w);
+    R.pmask[p] = m;
+    float* o = R.pw + (size_t)p * kMaxGroups;
+    for (int g = 0; g < R.sc.G; ++g) o[g] = w[g];
+}
+
 __global__ void k_rotate(uint32_t* qc) {
     qc[QC_A] = qc[QC_NEXT];
     qc[QC_B] = 0; qc[QC_NEXT] = 0; qc[QC_W] = 0;
@@ -109,6 +123,8 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     double* ffc = (double*)take(sizeof(double) * (size_t)n);
     uint32_t* ffg = (uint32_t*)take(nu);
     float* fkap = (float*)take(nf);
+    uint32_t* pmask = (uint32_t*)take(nu);
+    float* pw = (float*)take(nf * kMaxGroups);
     const size_t nw = (size_t)4 * (size_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)rec_max_blocks(), (n + 3) / 4));
     float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
     float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
@@ -133,7 +149,7 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     if (LS) *LS = gf_scratch_layout(n_prims, lscratch);
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
-        R->pix = pix; R->ffk = ffk; R->ffc = ffc; R->ffg = ffg; R->fkap = fkap;
+        R->pix = pix; R->ffk = ffk; R->ffc = ffc; R->ffg = ffg; R->fkap = fkap; R->pmask = pmask; R->pw = pw;
         R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap; R->wref = wref;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qW = qW; R->qO = qO; R->qV = qV; R->qcount = qc;
         R->lnodes = lnodes; R->lnodes2 = lnodes2; R->lprims = lprims; R->lperm = lperm; R->ldepth = ldepth;
@@ -153,6 +169,7 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, bool S, bool C, un
     // camera packets, and for the rays whose chords overflow a record buffer (queue qO)
     const bool onepass = !packet && R.estimator == 0 && gf_ff_onepass() && R.packets != 2;
     T.pre(STAGE_FFA, st, e);
+    if (S && R.estimator != 1) k_policy<<<(unsigned)((R.n_paths + 127) / 128), 128, 0, st>>>(R, sample, d);
     if (R.estimator == 1) gf_launch_ff_trk(R, sample, d, S, C, st);
     else if (packet) gf_launch_ffa_pkt(R, sample, d, S, C, cam && R.packets == 0, std::min<unsigned>(pgrid, rgrid), st);
     else if (onepass) gf_launch_ff(R, sample, d, S, C, cam, R.qA, QC_A, CUR_A, st);

@@ -124,7 +124,7 @@ struct FFRay {
     double tstar;        // tau* = -ln(1 - xi)
     float tlo, thi;      // the ray's scene interval (root box within [tmin, tmax])
     float bw, ibw;       // t-bin width and its inverse
-    float w[kMaxGroups]; // group weights (stochastic masks)
+    const float* w;      // group weights (stochastic masks: the path's row of R.pw, k_policy)
 };
 
 // Per-ray set-up, identical in both passes (recomputed, deterministic): mask and weights (a3),
@@ -136,9 +136,10 @@ __device__ __forceinline__ int ff_begin(const RenderDev& R, uint32_t p, int32_t 
     f.o = ld3(R.ox, R.oy, R.oz, p);
     f.d = ld3(R.dx, R.dy, R.dz, p);
     f.fth = fov_fmax<FOV>(R, f.pix, (uint32_t)sample);
-    f.mask = fov_mask<FOV>(R, f.fth) & (STOCH ? policy_for(R.ext, R.sc, f.d, R.seed, f.pix, (uint32_t)sample,
-                                                           (uint32_t)depth, ST_EXT, 1, f.w)
-                                              : R.ext.static_mask);
+    // stochastic masks: drawn once per path and depth by k_policy (out of the traversal kernels, whose
+    // instruction cache the Table B1/B2 code would share), the same for pass A and pass B
+    f.w = R.pw + (size_t)p * kMaxGroups;
+    f.mask = fov_mask<FOV>(R, f.fth) & (STOCH ? R.pmask[p] : R.ext.static_mask);
     const float xi = stream_u(R.seed, f.pix, (uint32_t)sample, (uint32_t)depth, ST_EXT, 0);
     f.tstar = -log1p(-(double)xi);  // tau* = -ln(1 - xi)   (Eq. 5, C16)
     const float t0 = R.trays ? R.trays[8 * (R.path_base + p) + 3] : 0.0f;  // gf_trace_free_flight: the ray's
