@@ -263,6 +263,11 @@ def main():
         f.load_primitives(sc)
         sc = dict(sc, extent=f.adaptive_extent(sc, args.adaptive_extent).cpu().numpy())
         name += f" [adaptive extents, eps {args.adaptive_extent:g}: mean E {float(np.mean(sc['extent'])):.2f}]"
+    # BVH keys: (band, level) subtrees (the paper's per-level structures) unless a policy samples orientation
+    # bins (Table B2), which then prune per-bin subtrees
+    orient = any((d.get(k) or {}).get("orient_strategy", 0) for d in descs for k in ("ext", "nee"))
+    bvh_keys = gf.BVH_KEYS_GROUP if orient else gf.BVH_KEYS_LEVEL
+    f.set_bvh_keys(bvh_keys)
     torch.cuda.synchronize()
     tb0 = time.perf_counter()
     f.load_primitives(sc)
@@ -417,6 +422,7 @@ def main():
         d2h = out_host.numel() * out_host.element_size()
         e2e_ms, e2e_rays, e2e_steps = 0.0, 0, []
         g2 = gf.GaborField(local)
+        g2.set_bvh_keys(bvh_keys)
         e2e_warm, e2e_n = 1, min(args.steps, 3)
         for k in range(e2e_warm + e2e_n):
             torch.cuda.synchronize()
@@ -457,6 +463,7 @@ def main():
                 "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded generators, paper_2602_05081_b200/inputs.py; no paper assets)",
                 "config": {"workload": name, "config_id": args.config, "n_prims": int(sc["n"]), "image": [W, H],
+                           "bvh_keys": "group" if bvh_keys == gf.BVH_KEYS_GROUP else "level",
                            "frames_per_step": len(descs),
                            "frame_masks": [f"{d['ext']['static_mask']:#010x}" for d in descs],
                            "paths_per_step": len(descs) * W * H * (spp if not tiles else 1),

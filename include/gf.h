@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 7
+#define GF_ABI_VERSION 8
 #define GF_MAX_GROUPS 32  /* 32-bit ray/group masks (C24); the paper's OptiX masks are 8-bit */
 #define GF_MAX_LEVELS 8
 
@@ -118,16 +118,26 @@ gf_status gf_load_primitives(gf_ctx *ctx, const gf_prims *prims, int64_t n, cons
                              void *prim_ws, size_t prim_ws_bytes, gf_stream stream);
 
 /* ---- a2: bounds + LBVH build ------------------------------- */
-/* Conservative world AABBs of the ellipsoids, 64-bit keys (group << 57 | Morton57
- * of the centre), radix sort (CUB), Karras hierarchy, bottom-up refit with group
+/* Conservative world AABBs of the ellipsoids, 64-bit keys (group or level class << 57 |
+ * Morton57 of the centre, gf_set_bvh_keys), radix sort (CUB), Karras hierarchy, bottom-up refit with group
  * masks, collapse to leaves of <= 4 single-group primitives, depth-first layout
- * with escape links.  Group bits are the top key bits, so the top of the tree
- * routes by group: one tree playing the role of the paper's per-level GAS +
+ * with escape links.  Class bits are the top key bits, so the top of the tree
+ * routes by level (or group): one tree playing the role of the paper's per-level GAS +
  * masked TLAS.  bvh_ws (device, >= bvh_bytes) holds the nodes and the reordered
  * primitives and must stay alive; scratch (device, >= scratch_bytes) may be
  * reused after the call.  Synchronises `stream`. */
 gf_status gf_build_bvh(gf_ctx *ctx, void *bvh_ws, size_t bvh_ws_bytes, void *scratch, size_t scratch_bytes,
                        gf_stream stream);
+/* Key prefix of the BVHs built after this call (gf_build_bvh, and the light / camera BVHs of gf_render):
+ * GF_BVH_KEYS_LEVEL (default) = (distance band, level): one spatial subtree per level and band, the
+ * paper's per-level acceleration structures, orientation bins mixed below it (leaves stay
+ * single-group, node masks prune); GF_BVH_KEYS_GROUP = the full group (level x bin x band): subtrees
+ * per orientation bin too -- for stochastic orientation masks (Table B2 Importance / Uniform), which
+ * then prune whole subtrees.  Results are identical either way; only traversal cost differs.
+ * GF_E_INVALID_ARGUMENT for another value.  Synchronous, no device work. */
+#define GF_BVH_KEYS_GROUP 0
+#define GF_BVH_KEYS_LEVEL 1
+gf_status gf_set_bvh_keys(gf_ctx *ctx, int32_t keys);
 
 /* Scene-derived quantities (synchronous; after gf_load_primitives, the BVH fields after
  * gf_build_bvh).  bvh_hash: a 64-bit hash of the whole BVH workspace (nodes, child pairs,

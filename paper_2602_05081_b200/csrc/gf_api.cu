@@ -15,6 +15,7 @@ using namespace gfk;
 
 struct gf_ctx {
     int device = 0;
+    int32_t bvh_keys = GF_BVH_KEYS_LEVEL;  // gf_set_bvh_keys
     std::string err;
     uint32_t* d_err = nullptr;            // [4] load error bits, first bad index
     unsigned long long* d_rays = nullptr;  // [3] dummy ray counters
@@ -191,6 +192,13 @@ extern "C" {
 
 int gf_abi_version(void) { return GF_ABI_VERSION; }
 
+gf_status gf_set_bvh_keys(gf_ctx* c, int32_t keys) {
+    if (!c) return GF_E_INVALID_ARGUMENT;
+    if (keys != GF_BVH_KEYS_GROUP && keys != GF_BVH_KEYS_LEVEL) return fail(c, GF_E_INVALID_ARGUMENT, "bad bvh keys");
+    c->bvh_keys = keys;
+    return GF_OK;
+}
+
 const char* gf_status_string(gf_status s) {
     switch (s) {
     case GF_OK: return "ok";
@@ -357,7 +365,7 @@ gf_status gf_build_bvh(gf_ctx* c, void* bvh_ws, size_t bvh_bytes, void* scratch,
     }
     uint32_t nn = 0, md = 0;
     GF_CUDA(c, gf_launch_build(c->prims, c->group, c->n, S, c->nodes, c->nodes2, c->sorted, c->perm, &nn, &md, c->root,
-                               st),
+                               gf_keymap(c->sc, c->bvh_keys), st),
             "gf_build_bvh");
     // warp traversal stack bound (gf_device.cuh: warp_traverse)
     if ((int)md + 34 + 64 > kWStk) return fail(c, GF_E_INVALID_ARGUMENT, "BVH deeper than the traversal stack allows");
@@ -669,7 +677,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         }
         if (!frame_cached(c->light_cache, (const char*)scratch, need, c->gen, R.lf, 9) || !d->reuse_accel) {
             GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.lf, nullptr, R.lnodes, R.lnodes2,
-                                             R.lprims, R.lperm, R.ldepth, st),
+                                             R.lprims, R.lperm, R.ldepth, gf_keymap(c->sc, c->bvh_keys), st),
                     "light BVH build");
             c->timer.launches += 7;  // k_bounds, k_keys, k_karras, k_refit, k_layout, k_pair_dev, k_gather (+ CUB)
         }
@@ -694,7 +702,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
         for (int k = 0; k < 3; ++k) key[9 + k] = d->cam_pos[k];
         if (!frame_cached(c->cam_cache, (const char*)scratch, need, c->gen, key, 12) || !d->reuse_accel) {
             GF_CUDA(c, gf_launch_build_frame(c->prims, c->group, c->n, LS, R.cb, d->cam_pos, R.cnodes, R.cnodes2,
-                                             R.cprims, R.cperm, R.cdepth, st),
+                                             R.cprims, R.cperm, R.cdepth, gf_keymap(c->sc, c->bvh_keys), st),
                     "camera BVH build");
             c->timer.launches += 7;
         }

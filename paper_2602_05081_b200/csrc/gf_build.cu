@@ -231,7 +231,7 @@ __device__ __forceinline__ uint64_t expand3(uint32_t x) {
 #define GF_VIEW_KEYS_2D 2  // bit 0: light frame, bit 1: camera frame (camera: cfg3 +4 %, cfg2 / cfg5 within noise; light: cfg2 NEE +18 %, so off)
 #endif
 __global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, const uint32_t* cbounds, uint64_t* keys,
-                       uint32_t* vals, Frame F, const float* center) {
+                       uint32_t* vals, Frame F, const float* center, KeyMap km) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     GPrim P = prims[i];
@@ -247,7 +247,7 @@ __global__ void k_keys(const GPrim* prims, const uint8_t* groups, int64_t n, con
         t = fminf(fmaxf(t, 0.0f), 1.0f);
         q[k] = min((uint32_t)(t * 524288.0f), 524287u);  // 19 bits
     }
-    uint32_t group = groups[i];
+    const uint32_t group = km.k[groups[i] & (kMaxGroups - 1)];
     if ((F.identity == 0 && (GF_VIEW_KEYS_2D & 1)) || (F.identity == 2 && (GF_VIEW_KEYS_2D & 2))) {
         // view frames: 2D Morton of the two axes across the rays (19 bits each), then the axis along
         // them (19 bits) -- the top of the tree partitions columns, the bottom orders a column
@@ -646,7 +646,7 @@ BuildScratch gf_scratch_layout(int64_t n, char* base) {
 // builds into nodes/sorted; returns node count via *n_nodes (host, after sync)
 cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes_v,
                             void* nodes2_v, void* sorted_v, int32_t* perm, uint32_t* n_nodes, uint32_t* max_depth,
-                            float* root_box, cudaStream_t st) {
+                            float* root_box, const KeyMap& km, cudaStream_t st) {
     const GPrim* prims = (const GPrim*)prims_v;
     GNode* nodes = (GNode*)nodes_v;
     cudaError_t e;
@@ -657,7 +657,7 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
     if ((e = cudaMemcpyAsync(S.cbounds, init, sizeof(init), cudaMemcpyHostToDevice, st))) return e;
     Frame I{{1, 0, 0, 0, 1, 0, 0, 0, 1}, 1, {0, 0, 0}};
     k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, I, S.center);
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, I, S.center);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, I, S.center, km);
     size_t tb = S.sort_temp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
                                              0, 64, st)))
@@ -698,7 +698,7 @@ static_assert(GF_CAM_LEAFMAX >= 1 && GF_CAM_LEAFMAX <= kLeafMax, "k_ff walks the
 // stays on the device (S.nsize[0]) and the tree depth is written to *depth (device).
 cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int64_t n, const BuildScratch& S,
                                   const float* F, const float* eye, void* nodes_v, void* nodes2_v, void* sorted_v,
-                                  int32_t* perm, uint32_t* depth, cudaStream_t st) {
+                                  int32_t* perm, uint32_t* depth, const KeyMap& km, cudaStream_t st) {
     const GPrim* prims = (const GPrim*)prims_v;
     GNode* nodes = (GNode*)nodes_v;
     cudaError_t e;
@@ -711,7 +711,7 @@ cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int
     if ((e = cudaMemsetAsync(S.cbounds, 0xFF, sizeof(uint32_t) * 3, st))) return e;
     if ((e = cudaMemsetAsync(S.cbounds + 3, 0, sizeof(uint32_t) * 3, st))) return e;
     k_bounds<<<nblk(n, 256), 256, 0, st>>>(prims, n, S.pbox, S.cbounds, Fr, S.center);
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, Fr, S.center);
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(prims, group, n, S.cbounds, S.keys_in, S.vals_in, Fr, S.center, km);
     size_t tb = S.sort_temp_bytes;
     if ((e = cub::DeviceRadixSort::SortPairs(S.sort_temp, tb, S.keys_in, S.keys_out, S.vals_in, S.vals_out, (int)n,
                                              0, 64, st)))
@@ -729,4 +729,15 @@ cudaError_t gf_launch_build_frame(const void* prims_v, const uint8_t* group, int
     k_pair_dev<<<nblk(2 * n - 1, 256), 256, 0, st>>>(nodes, S.nsize, 2 * n - 1, (GNode2*)nodes2_v);
     k_gather<<<nblk(n, 256), 256, 0, st>>>(prims, (const int32_t*)S.vals_out, n, (GPrim*)sorted_v, perm);
     return cudaGetLastError();
+}
+
+// key prefix of each group: mode GF_BVH_KEYS_GROUP the group, GF_BVH_KEYS_LEVEL its (band, level) class
+KeyMap gf_keymap(const SceneDev& sc, int mode) {
+    KeyMap m;
+    for (int g = 0; g < kMaxGroups; ++g) {
+        const int g0 = sc.G0 > 0 ? g % sc.G0 : 0, band = sc.G0 > 0 ? g / sc.G0 : 0;
+        const int level = g0 == 0 ? 0 : 1 + (g0 - 1) / (sc.K > 0 ? sc.K : 1);
+        m.k[g] = (uint8_t)((mode == 0 ? g : band * sc.P + level) & 127);
+    }
+    return m;
 }

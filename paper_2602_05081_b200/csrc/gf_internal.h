@@ -159,12 +159,18 @@ cudaError_t gf_launch_adaptive_extent(const float* scale, const float* alpha, co
 cudaError_t gf_launch_hash(const void* data, size_t bytes, unsigned long long* out_dev, cudaStream_t st);
 size_t gf_sort_temp_bytes(int64_t n);
 BuildScratch gf_scratch_layout(int64_t n, char* base);
+// Key prefix of each group in the LBVH keys (prefix << 57 | Morton): the group itself, or its
+// (band, level) class (gf_set_bvh_keys)
+struct KeyMap {
+    uint8_t k[gfk::kMaxGroups];
+};
+KeyMap gf_keymap(const gfk::SceneDev& sc, int mode);
 cudaError_t gf_launch_build(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S, void* nodes,
                             void* nodes2, void* sorted, int32_t* perm, uint32_t* n_nodes, uint32_t* max_depth,
-                            float* root_box, cudaStream_t st);
+                            float* root_box, const KeyMap& km, cudaStream_t st);
 cudaError_t gf_launch_build_frame(const void* prims, const uint8_t* group, int64_t n, const BuildScratch& S,
                                   const float* F, const float* eye, void* nodes, void* nodes2, void* sorted,
-                                  int32_t* perm, uint32_t* depth, cudaStream_t st);
+                                  int32_t* perm, uint32_t* depth, const KeyMap& km, cudaStream_t st);
 cudaError_t gf_launch_trace(const TraceArgs& A, bool brute, bool count, cudaStream_t st);
 cudaError_t gf_launch_candidates(const TraceArgs& A, bool brute, cudaStream_t st);
 cudaError_t gf_launch_grad_alpha(const TraceArgs& A, const float* dl, float* grad, cudaStream_t st);

@@ -22,6 +22,7 @@ SHARD_NONE, SHARD_TILES, SHARD_SAMPLES = 0, 1, 2
 TRACE_BRUTE_FORCE = 1
 TRACE_PACKETS = 2
 FF_UNIFORM = 4  # gf_trace_free_flight: GF_EST_UNIFORM (t uniform in the crossing bin)
+BVH_KEYS_GROUP, BVH_KEYS_LEVEL = 0, 1  # gf_set_bvh_keys
 
 
 class GFError(RuntimeError):
@@ -103,6 +104,7 @@ def lib():
     L.gf_query_workspace.argtypes = [i64, ctypes.POINTER(sz), ctypes.POINTER(sz), ctypes.POINTER(sz)]
     L.gf_load_primitives.argtypes = [vp, ctypes.POINTER(Prims), i64, ctypes.POINTER(Pyramid), vp, sz, vp]
     L.gf_build_bvh.argtypes = [vp, vp, sz, vp, sz, vp]
+    L.gf_set_bvh_keys.argtypes = [vp, ctypes.c_int32]
     L.gf_set_lod_mask.argtypes = [vp, ctypes.POINTER(LodPolicy), ctypes.POINTER(LodPolicy)]
     L.gf_trace_transmittance.argtypes = [vp, vp, i64, u64, vp, vp, vp, vp]
     L.gf_trace_transmittance_ex.argtypes = [vp, vp, i64, u64, u32, vp, vp, vp, vp]
@@ -208,6 +210,11 @@ class GaborField:
         self._sizes = (bb.value, sb.value)
         self.n, self.P, self.K, self.G = n, P, K, nb * (1 + (P - 1) * K)
         self._quat = arrs["quat"]  # kept for gf_grad_params_finish (the quaternions as loaded)
+        return self
+
+    def set_bvh_keys(self, keys):
+        """gf_set_bvh_keys: BVH_KEYS_LEVEL (default) or BVH_KEYS_GROUP for the BVHs built afterwards."""
+        self._check(self.L.gf_set_bvh_keys(self.ctx, int(keys)))
         return self
 
     def build_bvh(self):

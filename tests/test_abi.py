@@ -41,7 +41,7 @@ def test_sm100a_cubin_only():
 
 
 def test_host_only_entry_points(L):
-    assert L.gf_abi_version() == 7
+    assert L.gf_abi_version() == 8
     assert L.gf_status_string(0) == b"ok"
     # tile-interleaved ownership: 32x32 tiles, tile t -> t mod world
     assert gf.shard_pixel_owner(0, 0, 100, 100, 2) == 0

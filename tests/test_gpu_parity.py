@@ -124,16 +124,30 @@ def test_empty_scene_and_misses(gfm):
     assert torch.all(tau == 0)
 
 
-def test_candidate_sets_bvh_equal_brute_force(gfm, orc):
+@pytest.mark.parametrize("keys", ["level", "group"])
+def test_candidate_sets_bvh_equal_brute_force(gfm, orc, keys):
     """C21: BVH candidate sets == brute-force kernel sets bit-exactly (same fp32 predicate), and ==
-    the double oracle's up to grazing pairs (|r^2/E^2 - 1| <= 1e-5)."""
+    the double oracle's up to grazing pairs (|r^2/E^2 - 1| <= 1e-5) -- with (band, level) key classes
+    (orientation bins mixed below them) and with per-group subtrees (gf_set_bvh_keys)."""
     for sc, masks in ((I.scene_cfg1(), (0xFFFFFFFF, I.level_mask([0, 2]), 1 << 5)),
-                      (I.scene_cfg2(), (0xFFFFFFFF, I.level_mask([0, 1]))),):
-        f = field(gfm, sc)
+                      (I.scene_cfg2(), (0xFFFFFFFF, I.level_mask([0, 1]))),
+                      (I.scene_cfg5(copies=4, grid=(2, 2)), (0xFFFFFFFF, I.level_mask([0, 1], n_bands=3)))):
+        f = gfm.GaborField(0)
+        f.set_bvh_keys(gfm.BVH_KEYS_GROUP if keys == "group" else gfm.BVH_KEYS_LEVEL)
+        f.load_primitives(sc)
+        f.build_bvh()
         S = orc.Scene(sc)
-        desc = I.render_desc_cfg1() if sc["n"] == 1000 else I.render_desc_cfg2(3, 256, 256)
-        rays = camera_rays(desc, 300, seed=5)
-        rays[::4] = I.rays_through_box(9, len(rays[::4]))
+        if "band" in sc:  # 4 army copies, 3 distance bands: rays through the scene's root box
+            info = f.scene_info()
+            lo, hi = np.asarray(info["root_lo"], np.float64), np.asarray(info["root_hi"], np.float64)
+            rng = np.random.default_rng(5)
+            tgt = lo + (hi - lo) * rng.random((300, 3))
+            org = (lo + hi) / 2 + np.linalg.norm(hi - lo) * rng.normal(size=(300, 3))
+            rays = I.pack_rays(org, tgt - org)
+        else:
+            desc = I.render_desc_cfg1() if sc["n"] == 1000 else I.render_desc_cfg2(3, 256, 256)
+            rays = camera_rays(desc, 300, seed=5)
+            rays[::4] = I.rays_through_box(9, len(rays[::4]))
         for m in masks:
             f.set_lod_mask({"static_mask": m})
             ids_b, cnt_b = f.trace_candidates(rays, 4096)
