@@ -17,7 +17,12 @@ struct WarpBinQ {
 };
 
 template <bool STOCH, bool COUNT, bool FOV, bool CAM>
-__global__ void __launch_bounds__(128) k_ffa_w(RenderDev R, int32_t sample, int32_t depth,
+#ifdef GF_MINB_FFAW  // tuning variants: the blocks per SM the registers must allow
+#define GF_LB_FFAW __launch_bounds__(128, GF_MINB_FFAW)
+#else
+#define GF_LB_FFAW __launch_bounds__(128)
+#endif
+__global__ void GF_LB_FFAW k_ffa_w(RenderDev R, int32_t sample, int32_t depth,
                                                const uint32_t* __restrict__ q_in, int cnt_slot, int cur_slot,
                                                int ray_count) {
     __shared__ WarpTrav s_t[4];

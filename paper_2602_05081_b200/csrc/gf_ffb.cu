@@ -95,7 +95,10 @@ __device__ __forceinline__ bool ffb_overflow(const RenderDev& R, const FFRay& f,
 }
 
 template <bool STOCH, bool COUNT, bool FOV, bool CAM>
-__global__ void __launch_bounds__(128) k_ffb_w(RenderDev R, int32_t sample, int32_t depth, const uint32_t* __restrict__ q_in,
+#ifndef GF_MINB_FFB
+#define GF_MINB_FFB 8  // 64 registers, 8 blocks per SM: ffB -2..-4 % against 72 registers / 7 blocks (cfg4, cfg5)
+#endif
+__global__ void __launch_bounds__(128, GF_MINB_FFB) k_ffb_w(RenderDev R, int32_t sample, int32_t depth, const uint32_t* __restrict__ q_in,
                                                int cnt_slot, int cur_slot) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];

@@ -6,13 +6,19 @@
 
 namespace gfk {
 
+
 // NEE, one warp per path (warp_tau): shadow-ray transmittance, HG phase sampling of the next
 // direction.  Replaces the per-lane k_nee on the production path.
 // LIGHT: traverse the light BVH (boxes in a frame whose third axis is the light direction, built
 // per gf_render call by gf_launch_build_frame): the shadow ray is axis-parallel there, so a box test
 // is two interval tests and one compare, and the boxes are tight across the rays' direction.
 template <bool STOCH, bool COUNT, bool LIGHT, bool FOV>
-__global__ void __launch_bounds__(128) k_nee_w(RenderDev R, int32_t sample, int32_t depth) {
+#ifdef GF_MINB_NEE  // tuning variants: the blocks per SM the registers must allow
+#define GF_LB_NEE __launch_bounds__(128, GF_MINB_NEE)
+#else
+#define GF_LB_NEE __launch_bounds__(128)
+#endif
+__global__ void GF_LB_NEE k_nee_w(RenderDev R, int32_t sample, int32_t depth) {
     __shared__ WarpTrav s_t[4];
     __shared__ WarpEnd s_e[4];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
