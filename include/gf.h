@@ -120,7 +120,7 @@ gf_status gf_load_primitives(gf_ctx *ctx, const gf_prims *prims, int64_t n, cons
 /* ---- a2: bounds + LBVH build ------------------------------- */
 /* Conservative world AABBs of the ellipsoids, 64-bit keys (group or level class << 57 |
  * Morton57 of the centre, gf_set_bvh_keys), radix sort (CUB), Karras hierarchy, bottom-up refit with group
- * masks, collapse to leaves of <= 4 single-group primitives, depth-first layout
+ * masks, collapse to leaves of <= 3 single-group primitives, depth-first layout
  * with escape links.  Class bits are the top key bits, so the top of the tree
  * routes by level (or group): one tree playing the role of the paper's per-level GAS +
  * masked TLAS.  bvh_ws (device, >= bvh_bytes) holds the nodes and the reordered

@@ -687,10 +687,10 @@ cudaError_t gf_launch_build(const void* prims_v, const uint8_t* group, int64_t n
 }
 
 #ifndef GF_LIGHT_LEAFMAX
-#define GF_LIGHT_LEAFMAX 4  // primitives per leaf of the NEE light BVH (measured: 1/2/3 slower)
+#define GF_LIGHT_LEAFMAX 3  // primitives per leaf of the NEE light BVH (r2, level keys: 2 slower, 4 -2 %)
 #endif
 #ifndef GF_CAM_LEAFMAX
-#define GF_CAM_LEAFMAX 4  // primitives per leaf of the camera BVH (measured: 2/3/6 no better)
+#define GF_CAM_LEAFMAX 3  // primitives per leaf of the camera BVH
 #endif
 static_assert(GF_LIGHT_LEAFMAX >= 1 && GF_LIGHT_LEAFMAX <= kLeafMax, "warp traversal buffers hold kLeafMax per leaf");
 static_assert(GF_CAM_LEAFMAX >= 1 && GF_CAM_LEAFMAX <= kLeafMax, "k_ff walks the camera BVH with kLeafMax buffers");

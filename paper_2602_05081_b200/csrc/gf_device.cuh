@@ -37,7 +37,7 @@ namespace gfk {
 constexpr int kMaxGroups = 32;
 constexpr int kMaxLevels = 8;
 #ifndef GF_LEAFMAX
-#define GF_LEAFMAX 4
+#define GF_LEAFMAX 3
 #endif
 constexpr int kLeafMax = GF_LEAFMAX;  // primitives per BVH leaf (<= 7: 3-bit count)
 constexpr uint32_t kLeafBit = 0x80000000u;
