@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(128, GF_MINB_FFB) k_ffb_w(RenderDev R, int32_t
         if (window_records<STOCH, COUNT, CAM>(R, f, r, cp, ff_edge(f, s0 - 1), ff_edge(f, kend), s_t[wid], rec, aux, cap,
                                               ng, nb, &tot, wk)) {
             col = resolve_records<COUNT>(rec, aux, cap, ng, nb, f, s0, kend, cstart, s_f[wid], s_w[wid], s_e[wid], wk, t,
-                                         true, &kap);
+                                         true, &kap, tot);
         } else {  // more chords than the buffer holds: k_ffb_over (queue qV)
             if (lane == 0) {
                 if (COUNT) ++wk.overflow;

@@ -790,7 +790,8 @@ __device__ __noinline__ float window_root(const float4* __restrict__ rec, float4
 template <bool COUNT>
 __device__ __forceinline__ float window_root_clip(const float4* __restrict__ rec, const float4* __restrict__ aux,
                                                   uint32_t cap, uint32_t ng, uint32_t nb, float a, float b, double c0,
-                                                  double tstar, WarpEnd& q, Work& wk, float* kap_out = nullptr) {
+                                                  double tstar, WarpEnd& q, Work& wk, float* kap_out = nullptr,
+                                                  double wtot = 0.0) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -874,7 +875,9 @@ __device__ __forceinline__ float window_root_clip(const float4* __restrict__ rec
         return c0 + xs - tstar;
     };
     const float wlen = b - a;
-    float lo = a, hi = b, t = a + 0.5f * wlen;
+    // start where tau, linear over the window (wtot = tau over it), reaches tau*; the midpoint without it
+    const double fr = wtot > 0.0 ? fmin(0.95, fmax(0.05, (tstar - c0) / wtot)) : 0.5;
+    float lo = a, hi = b, t = a + (float)fr * wlen;
     const float tol = fmaxf(1e-6f * wlen, 2.4e-7f * fmaxf(fabsf(a), fabsf(b)));
     double kap = 0.0, dkap = 0.0;
     for (int it = 0; it < 40; ++it) {
@@ -960,14 +963,15 @@ template <bool COUNT>
 __device__ __forceinline__ bool resolve_records(const float4* __restrict__ rec, float4* __restrict__ aux, uint32_t cap,
                                                 uint32_t ng, uint32_t nb, const FFRay& f, int s0, int kend,
                                                 double cstart, float* cf, uint16_t* wl, WarpEnd& q, Work& wk,
-                                                float& tout, bool clipped = false, float* kap_out = nullptr) {
+                                                float& tout, bool clipped = false, float* kap_out = nullptr,
+                                                double wtot = 0.0) {
     const unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     if (kNF == 1) {  // uniform bins: the root inside coarse bin s0 (= the first crossing edge), tau before it cstart
         if (s0 >= kNC) return false;
         if (clipped)  // pass B: the records are exactly the window's chords, clipped to it
             tout = window_root_clip<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, q, wk,
-                                            kap_out);
+                                            kap_out, wtot);
         else
             tout = window_root<COUNT>(rec, aux, cap, ng, nb, ff_edge(f, s0 - 1), ff_edge(f, s0), cstart, f.tstar, wl, q, wk);
         return true;
