@@ -689,6 +689,7 @@ gf_status gf_render(gf_ctx* c, const gf_render_desc* d, float* accum, void* scra
     R.tomo_pkt_min = env_int("GF_DEBUG_TOMO_PKT_MIN", 1 << 16);
     R.ffb_cam = env_int("GF_FFB_CAM", 1);
     R.ff_win = env_int("GF_FF_WIN", 1);
+    R.reorder = env_int("GF_REORDER", 0);
     R.win_scale = 0.1f * (float)env_int("GF_FF_WIN_SCALE10", 12);
     if (R.camb) {
         const float* axes[3] = {d->cam_right, d->cam_up, d->cam_fwd};

@@ -86,9 +86,10 @@ __global__ void GF_LB_FFAW k_ffa_w(RenderDev R, int32_t sample, int32_t depth,
         // the exact prefix at its edges decides -- a ray whose first crossing lies in an early window never
         // visits the rest of the scene (the edge values are the same sums as in one sweep: C17 unchanged).
         // R.ff_win 1: one split, after the bin where tau*/kappa (kappa at the path's last collision, scaled
-        // by win_scale) predicts the crossing; 2: windows of 1, 2, 4, .. bins; 0: one sweep.
+        // by win_scale) predicts the crossing; 3: two splits (there and at 3x; measured no better); 2: windows
+        // of 1, 2, 4, .. bins; 0: one sweep.
         int split = kNC;  // first bin of the second window (kNC: one window)
-        if (kNF == 1 && R.ff_win == 1 && depth > 0) {
+        if (kNF == 1 && (R.ff_win == 1 || R.ff_win == 3) && depth > 0) {
             const float k0 = R.fkap[p];
             if (k0 > 0.0f)
                 split = (int)fmin((double)kNC, fmax(1.0, R.win_scale * (f.tstar / k0 - (double)f.tlo) * f.ibw + 1.0));
@@ -96,7 +97,8 @@ __global__ void GF_LB_FFAW k_ffa_w(RenderDev R, int32_t sample, int32_t depth,
         int ks = kNC;
         double cstart = 0.0;
         for (int wa = 0; wa < kNC;) {
-        const int wb = kNF > 1 ? kNC - 1 : R.ff_win == 2 ? min(kNC - 1, 2 * wa) : (wa < split ? split - 1 : kNC - 1);
+        const int wb = kNF > 1 ? kNC - 1 : R.ff_win == 2 ? min(kNC - 1, 2 * wa)
+                     : wa < split ? split - 1 : (R.ff_win == 3 && wa < 3 * split) ? min(kNC - 1, 3 * split - 1) : kNC - 1;
         const float wlo = ff_edge(f, wa - 1), whi = ff_edge(f, wb);
         auto run = [&](int, int take) {
             const bool v = lane < take;

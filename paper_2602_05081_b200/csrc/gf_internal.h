@@ -105,6 +105,9 @@ struct RenderDev {
     float* fkap;     // free flight: kappa at the path's last collision (0: unknown), the next pass A's first cut
     uint32_t* pmask; // stochastic extension masks of the current depth (k_policy) ...
     float* pw;       // ... and their group weights, kMaxGroups per path
+    uint32_t *skey, *skey2, *sval;  // extension-ray reordering (R.reorder): keys, sorted keys, path ids
+    void* sort_temp;                // CUB temp storage of that sort
+    size_t sort_bytes;
     float4* wrec;    // [warp][rec_cap] x 2 float4 hit records (pass-B windows, tracking; reused per path)
     float4* waux;    // [warp][rec_cap] per-record full integral, amp G(u0), amp cos, -amp sin
     int32_t rec_cap;
@@ -143,6 +146,7 @@ struct RenderDev {
     int32_t ffb_cam;       // pass B of depth-0 rays walks the camera BVH (1) or the world BVH (0)
     int32_t ff_win;        // pass A of extension rays in windows: 0 one sweep; 1 split at the bin predicted from
                            // kappa at the path's last collision; 2 windows of 1, 2, 4, .. bins on every ray
+    int32_t reorder;       // sort extension rays by direction octant and origin before pass A (A/B)
     float win_scale;       // ff_win 1: the split bin is win_scale x the predicted crossing bin
 };
 

@@ -16,6 +16,8 @@
 // fetch paths dynamically from the queues.
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "gf_render.cuh"
 
 namespace gfk {
@@ -73,6 +75,34 @@ __global__ void __launch_bounds__(128) k_policy(RenderDev R, int32_t sample, int
     for (int g = 0; g < R.sc.G; ++g) o[g] = w[g];
 }
 
+// Extension-ray reordering (R.reorder, A/B): 24-bit keys = direction octant << 21 | Morton of the origin
+// (7 bits per axis over the root box), sentinel 0xFFFFFF past the queue's count; CUB sorts queue qA by
+// them before pass A, so that neighbouring warps trace nearby, similar rays.
+__device__ __forceinline__ uint32_t spread7(uint32_t v) {
+    uint32_t r = 0;
+    for (int b = 0; b < 7; ++b) r |= ((v >> b) & 1u) << (3 * b);
+    return r;
+}
+__global__ void __launch_bounds__(256) k_ext_keys(RenderDev R) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R.n_paths) return;
+    uint32_t key = 0xFFFFFFu, val = 0u;
+    if (i < (int64_t)R.qcount[QC_A]) {
+        val = R.qA[i];
+        const float3 o = ld3(R.ox, R.oy, R.oz, val), d = ld3(R.dx, R.dy, R.dz, val);
+        const float lo[3] = {R.root_lo.x, R.root_lo.y, R.root_lo.z}, hi[3] = {R.root_hi.x, R.root_hi.y, R.root_hi.z};
+        const float x[3] = {o.x, o.y, o.z};
+        uint32_t m = 0;
+        for (int a = 0; a < 3; ++a) {
+            const float u = fminf(fmaxf((x[a] - lo[a]) / fmaxf(hi[a] - lo[a], 1e-30f), 0.0f), 1.0f);
+            m |= spread7((uint32_t)(u * 127.0f)) << (2 - a);
+        }
+        key = ((uint32_t)(d.x < 0.0f) | ((uint32_t)(d.y < 0.0f) << 1) | ((uint32_t)(d.z < 0.0f) << 2)) << 21 | m;
+    }
+    R.skey[i] = key;
+    R.sval[i] = val;
+}
+
 __global__ void k_rotate(uint32_t* qc) {
     qc[QC_A] = qc[QC_NEXT];
     qc[QC_B] = 0; qc[QC_NEXT] = 0; qc[QC_W] = 0;
@@ -125,6 +155,12 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     float* fkap = (float*)take(nf);
     uint32_t* pmask = (uint32_t*)take(nu);
     float* pw = (float*)take(nf * kMaxGroups);
+    uint32_t* skey = (uint32_t*)take(nu); uint32_t* skey2 = (uint32_t*)take(nu); uint32_t* sval = (uint32_t*)take(nu);
+    size_t sb = 0;
+    if (n > 0)
+        cub::DeviceRadixSort::SortPairs(nullptr, sb, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                        (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 24);
+    void* sort_temp = take(sb + 256);
     const size_t nw = (size_t)4 * (size_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)rec_max_blocks(), (n + 3) / 4));
     float4* wrec = (float4*)take(sizeof(float4) * 2 * (size_t)kRecCap * nw);
     float4* waux = (float4*)take(sizeof(float4) * (size_t)kRecCap * nw);
@@ -150,6 +186,7 @@ size_t gf_render_state_bytes(int64_t n, int64_t n_prims, char* base, RenderDev* 
     if (R) {
         R->ox = ox; R->oy = oy; R->oz = oz; R->dx = dx; R->dy = dy; R->dz = dz; R->beta = beta; R->L = L;
         R->pix = pix; R->ffk = ffk; R->ffc = ffc; R->ffg = ffg; R->fkap = fkap; R->pmask = pmask; R->pw = pw;
+        R->skey = skey; R->skey2 = skey2; R->sval = sval; R->sort_temp = sort_temp; R->sort_bytes = sb;
         R->wrec = wrec; R->waux = waux; R->rec_cap = kRecCap; R->wref = wref;
         R->qA = qA; R->qB = qB; R->qNext = qN; R->qW = qW; R->qO = qO; R->qV = qV; R->qcount = qc;
         R->lnodes = lnodes; R->lnodes2 = lnodes2; R->lprims = lprims; R->lperm = lperm; R->ldepth = ldepth;
@@ -169,6 +206,11 @@ static void launch_depth(RenderDev& R, int32_t sample, int d, bool S, bool C, un
     // camera packets, and for the rays whose chords overflow a record buffer (queue qO)
     const bool onepass = !packet && R.estimator == 0 && gf_ff_onepass() && R.packets != 2;
     T.pre(STAGE_FFA, st, e);
+    if (R.reorder && d > 0 && R.mode == 1 && !packet) {  // extension rays sorted by direction octant and origin
+        k_ext_keys<<<(unsigned)((R.n_paths + 255) / 256), 256, 0, st>>>(R);
+        size_t tb = R.sort_bytes;
+        cub::DeviceRadixSort::SortPairs(R.sort_temp, tb, R.skey, R.skey2, R.sval, R.qA, (int)R.n_paths, 0, 24, st);
+    }
     if (S && R.estimator != 1) k_policy<<<(unsigned)((R.n_paths + 127) / 128), 128, 0, st>>>(R, sample, d);
     if (R.estimator == 1) gf_launch_ff_trk(R, sample, d, S, C, st);
     else if (packet) gf_launch_ffa_pkt(R, sample, d, S, C, cam && R.packets == 0, std::min<unsigned>(pgrid, rgrid), st);
