@@ -716,7 +716,10 @@ __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const 
 // full warps instead of the divergent per-lane depth-first walk.  Stack bound: a full step grows
 // the stack by <= 32; above `stk_limit` one node per step is popped (depth-first, growth <= 1
 // per level), and stk_limit = kWStk - 34 - max_depth keeps it in bounds (gf_build_bvh).
-constexpr int kWStk = 512;
+#ifndef GF_WSTK
+#define GF_WSTK 256  // warp traversal stack entries per warp (512: -2 % -- the shared memory it frees goes to L1)
+#endif
+constexpr int kWStk = GF_WSTK;
 constexpr int kWPrm = 32 + 64 * kLeafMax;
 struct WarpTrav {
     uint32_t stk[kWStk];
