@@ -476,6 +476,27 @@ def test_reused_view_bvhs(gfm):
         assert torch.equal(x, y)
 
 
+def test_reused_view_bvhs_probe_and_full_layouts(gfm):
+    """a probe render, a full-image render and the probe render again on ONE scratch with
+    reuse_accel = 1.  The two calls lay the scratch out differently (per-path arrays sized by their path
+    counts), so the full render overwrites the probe call's view BVHs; the cache is keyed on the layout
+    and must rebuild -- every result equals a fresh build's."""
+    sc = I.scene_cfg2()
+    f = field(gfm, sc)
+    d = I.render_desc_cfg2(3, 96, 96)
+    rng = np.random.default_rng(3)
+    probes = rng.choice(96 * 96, 200, replace=False).astype(np.int32)
+    scratch = f.render_scratch(d, 1)
+    ref_p, _ = f.render(d, 0, 2, probes=probes)
+    ref_f, _ = f.render(d, 0, 1)
+    seq = [("p", f.render(dict(d, reuse_accel=1), 0, 2, probes=probes, scratch=scratch)[0]),
+           ("f", f.render(dict(d, reuse_accel=1), 0, 1, scratch=scratch)[0]),
+           ("p", f.render(dict(d, reuse_accel=1), 0, 2, probes=probes, scratch=scratch)[0]),
+           ("f", f.render(dict(d, reuse_accel=1), 0, 1, scratch=scratch)[0])]
+    for kind, x in seq:
+        assert torch.equal(x, ref_p if kind == "p" else ref_f), kind
+
+
 def test_warp_traversal_depth_first_mode(gfm, orc, monkeypatch):
     """The warp traversal pops one node per step above its stack threshold (bounded stack);
     forcing that mode everywhere gives the same hits and transmittance."""
