@@ -193,7 +193,8 @@ def run_reference(args, rank, world):
             "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
             "scaling": "strong" if args.config == 5 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, paper_2602_05081_b200/inputs.py)",
-            "config": {"workload": name + " -- bounded oracle sample per step", "paths_per_step": paths},
+            "config": {"workload": name + " -- bounded oracle sample per step",
+                       "paths_per_step": max(1, paths // len(descs)) * len(descs)},
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
