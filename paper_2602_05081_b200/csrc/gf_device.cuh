@@ -716,6 +716,9 @@ __device__ __forceinline__ void flat_loop(uint32_t* work, uint32_t count, const 
 // full warps instead of the divergent per-lane depth-first walk.  Stack bound: a full step grows
 // the stack by <= 32; above `stk_limit` one node per step is popped (depth-first, growth <= 1
 // per level), and stk_limit = kWStk - 34 - max_depth keeps it in bounds (gf_build_bvh).
+#ifndef GF_NODE_PREFETCH
+#define GF_NODE_PREFETCH 0  // warp traversal: L1 prefetch of the pushed children's child pairs
+#endif
 #ifndef GF_WSTK
 #define GF_WSTK 256  // warp traversal stack entries per warp (512: -2 % -- the shared memory it frees goes to L1)
 #endif
@@ -777,6 +780,11 @@ __device__ __forceinline__ void warp_traverse_b(const GNode* __restrict__ nodes,
                 if (COUNT) wk.nodes += 2;
             }
             const bool i0 = h0 && !(ref0 & kLeafBit), i1 = h1 && !(ref1 & kLeafBit);
+#if GF_NODE_PREFETCH
+            // the children pushed now are the next steps' pops: start their child-pair loads into L1
+            if (i0) asm volatile("prefetch.global.L1 [%0];" ::"l"(n2 + ref0));
+            if (i1) asm volatile("prefetch.global.L1 [%0];" ::"l"(n2 + ref1));
+#endif
             const unsigned b0 = __ballot_sync(FULL, i0), b1 = __ballot_sync(FULL, i1);
             if (i0) sm.stk[ns + __popc(b0 & lt)] = ref0;
             if (i1) sm.stk[ns + __popc(b0) + __popc(b1 & lt)] = ref1;
